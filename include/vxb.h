@@ -1,0 +1,253 @@
+/*
+ * vxb.h — C ABI of the B200 voxel-network simulation step (the drop-in
+ * boundary for the reference's SimInstance hot path).
+ *
+ * Every entry point replaces one member of the reference C++ host API
+ * (/root/reference/proj/include/voxsim/engine.hpp):
+ *
+ *   vxb_create              <- SimInstance::SimInstance(tables, layout, options)
+ *                              engine.hpp:70-71, load engine.cpp:175-293
+ *   vxb_advance             <- RunResult SimInstance::advance(uint32_t steps)
+ *                              engine.hpp:76, engine.cpp:763-827
+ *   vxb_result_*            <- the RunResult fields (engine.hpp:55-63)
+ *   vxb_current_step        <- SimInstance::current_step()  engine.hpp:77
+ *   vxb_set_conductances    <- SimInstance::set_conductances  engine.hpp:81-82,
+ *                              engine.cpp:829-844
+ *   vxb_membrane_snapshot   <- SimInstance::membrane_snapshot engine.hpp:84,
+ *                              engine.cpp:846-849
+ *   vxb_run_simulation      <- run_simulation(tables, layout, options)
+ *                              engine.hpp:92-93
+ *   vxb_last_error          <- what() of the ConfigError / SimError thrown
+ *                              (util.hpp:14-21)
+ *   vxb_destroy             <- ~SimInstance
+ *
+ * Inputs are plain arrays in the reference's own table layout
+ * (NetworkTables / WorkerTable / NeuronRecord / SynEntry, netgen.hpp:27-71;
+ * NetworkLayout::units, layout.hpp:53-60) so a caller holding reference
+ * tables passes pointers into them without conversion.
+ *
+ * Return codes mirror the CLI's exception mapping (voxsim.cpp:476-485):
+ * 0 = ok, 2 = ConfigError, 3 = SimError.  A failed engine rejects further
+ * vxb_advance calls (engine.cpp:765-766).
+ *
+ * There is no CPU fallback: vxb_create fails with VXB_ESIM when no CUDA
+ * device is usable.
+ */
+#ifndef VXB_H
+#define VXB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VXB_OK 0
+#define VXB_ECONFIG 2
+#define VXB_ESIM 3
+
+#define VXB_RECEPTORS 4 /* AMPA, NMDA, GABAA, GABAB (model.hpp:13-15) */
+#define VXB_ABI_VERSION 1
+
+/* One in-synapse of a worker table: byte-identical to voxsim::SynEntry
+ * (netgen.hpp:27-36, 16 bytes, packed). */
+#pragma pack(push, 1)
+typedef struct vxb_syn_entry {
+    uint32_t src_local;
+    uint16_t src_worker;
+    uint8_t cls; /* 0 = excitatory source (AMPA/NMDA), 1 = inhibitory (GABAA/GABAB) */
+    uint8_t pad;
+    int32_t wq_fast; /* Q16 weight, AMPA or GABAA */
+    int32_t wq_slow; /* Q16 weight, NMDA or GABAB */
+} vxb_syn_entry;
+#pragma pack(pop)
+
+/* One neuron record: the fields of voxsim::NeuronRecord (netgen.hpp:40-53)
+ * in a fixed, padding-free 136-byte layout. */
+typedef struct vxb_neuron {
+    uint64_t gid;
+    uint64_t dst_mask; /* bit w: has >= 1 target on worker w */
+    uint32_t voxel;
+    uint32_t unit;
+    uint32_t row_len;
+    uint32_t refractory_steps;
+    uint16_t pop;
+    uint8_t excitatory;
+    uint8_t pad0;
+    float capacitance, g_leak, e_leak, v_threshold, v_reset;
+    float e_rev[VXB_RECEPTORS];
+    float tau[VXB_RECEPTORS];
+    float omega[VXB_RECEPTORS];
+    float g[VXB_RECEPTORS];
+    float ou_mean, ou_sigma, ou_tau;
+    float v_init;
+} vxb_neuron;
+
+/* voxsim::WorkerTable (netgen.hpp:55-64). */
+typedef struct vxb_worker_table {
+    uint16_t worker;
+    uint16_t worker_count;
+    uint32_t n_neurons;
+    uint64_t seed;
+    uint64_t n_synapses;
+    const vxb_neuron* neurons;     /* n_neurons, local id order */
+    const vxb_syn_entry* synapses; /* n_synapses, row-major by target */
+    const uint64_t* row_base;      /* n_neurons + 1 prefix sums */
+} vxb_worker_table;
+
+/* voxsim::Unit (layout.hpp:53-60). */
+typedef struct vxb_unit {
+    uint64_t gid_base;
+    uint32_t voxel;
+    uint32_t neurons;
+    uint16_t pop;
+    uint8_t excitatory;
+    uint8_t pad0;
+    uint32_t pad1;
+} vxb_unit;
+
+/* NetworkTables + the parts of NetworkLayout the engine reads at load
+ * (engine.cpp:180-192, 276-290). */
+typedef struct vxb_network {
+    uint32_t n_workers;
+    uint32_t n_units;
+    uint32_t n_voxels;
+    uint32_t pad0;
+    const vxb_worker_table* workers;  /* NetworkTables::workers */
+    const uint16_t* unit_worker;      /* NetworkTables::unit_worker */
+    const uint32_t* unit_local_base;  /* NetworkTables::unit_local_base */
+    const vxb_unit* units;            /* NetworkLayout::units */
+} vxb_network;
+
+/* voxsim::Injection (engine.hpp:16-21). */
+typedef struct vxb_injection {
+    uint32_t from_step;
+    uint32_t to_step;
+    uint32_t voxel;
+    float current_pa;
+} vxb_injection;
+
+/* voxsim::ForcedSpike (engine.hpp:25-28). */
+typedef struct vxb_forced_spike {
+    uint32_t step;
+    uint32_t pad0;
+    uint64_t gid;
+} vxb_forced_spike;
+
+/* voxsim::SimOptions (engine.hpp:30-45) plus device placement. */
+typedef struct vxb_options {
+    double dt_ms;
+    const char* scheduler;   /* "cuda" (also accepts "threads"/"loopback") */
+    const char* transport;   /* "queue" | "nvlink" */
+    uint16_t workers_per_node;
+    uint16_t pad0;
+    int32_t recv_timeout_ms;
+    int32_t record_raster;
+    int32_t record_timings;
+    const uint64_t* probe_gids;
+    uint32_t n_probes;
+    uint32_t n_injections;
+    const vxb_injection* injections;
+    const vxb_forced_spike* forced_spikes;
+    uint32_t n_forced;
+    int32_t device;          /* CUDA device of shard 0; -1 = current device */
+    int32_t n_devices;       /* GPUs the workers are spread over; <= 1 = one */
+    int32_t pad1;
+} vxb_options;
+
+/* voxsim::RasterEvent (stats.hpp:84-89). */
+typedef struct vxb_raster_event {
+    uint32_t step;
+    uint16_t worker;
+    uint16_t pad0;
+    uint32_t local;
+    uint32_t pad1;
+    uint64_t gid;
+} vxb_raster_event;
+
+/* voxsim::FlopCounters (stats.hpp:41-52). */
+typedef struct vxb_flops {
+    uint64_t membrane;
+    uint64_t gating_inner;
+    uint64_t gating_outer;
+    uint64_t gating_decay;
+    uint64_t current;
+} vxb_flops;
+
+/* voxsim::StepTimings (stats.hpp:17-38). t[0..10] = t1..t11. */
+typedef struct vxb_step_timings {
+    uint32_t step;
+    uint16_t worker;
+    uint16_t pad0;
+    int64_t t[11];
+    int64_t send_intra_ns, send_inter_ns, recv_intra_ns, recv_inter_ns;
+    uint64_t bytes_sent_intra, bytes_sent_inter, bytes_recv_intra, bytes_recv_inter;
+    uint32_t spikes;
+    uint32_t pad1;
+} vxb_step_timings;
+
+typedef struct vxb_engine vxb_engine;
+
+/* ---- lifecycle ----------------------------------------------------------- */
+int vxb_create(const vxb_network* net, const vxb_options* opt, vxb_engine** out);
+void vxb_destroy(vxb_engine* e);
+/* Error text of the last failing call on `e` (or of the last failed
+ * vxb_create on this thread when e == NULL). */
+const char* vxb_last_error(const vxb_engine* e);
+int vxb_abi_version(void);
+
+/* ---- stepping ------------------------------------------------------------ */
+/* Advances `steps` steps; results are kept inside the engine until the next
+ * vxb_advance and read with vxb_result_*. */
+int vxb_advance(vxb_engine* e, uint32_t steps);
+uint32_t vxb_current_step(const vxb_engine* e);
+
+/* ---- RunResult of the last vxb_advance ------------------------------------ */
+uint32_t vxb_result_steps_done(const vxb_engine* e);
+uint64_t vxb_result_total_spikes(const vxb_engine* e);
+uint64_t vxb_result_raster_size(const vxb_engine* e);
+/* Raster sorted (step, worker, local) (engine.cpp:812-817). */
+int vxb_result_raster(const vxb_engine* e, vxb_raster_event* out, uint64_t cap);
+/* RateSeries::counts as [n_units][steps] row-major. */
+int vxb_result_rates(const vxb_engine* e, uint32_t* counts, uint64_t cap);
+/* ProbeTrace v / i_syn as [n_probes][steps]. */
+int vxb_result_probes(const vxb_engine* e, float* v, float* i_syn, uint64_t cap);
+int vxb_result_flops(const vxb_engine* e, vxb_flops* out);
+uint64_t vxb_result_timings_size(const vxb_engine* e);
+int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap);
+/* Device time of the last advance's step kernel(s), milliseconds (CUDA
+ * events on the launching stream; max over shards). */
+double vxb_result_device_ms(const vxb_engine* e);
+/* Bytes copied host->device / device->host by the last vxb_advance. */
+uint64_t vxb_result_h2d_bytes(const vxb_engine* e);
+uint64_t vxb_result_d2h_bytes(const vxb_engine* e);
+/* Kernel launches issued by the last vxb_advance. */
+uint64_t vxb_result_launches(const vxb_engine* e);
+
+/* ---- state access -------------------------------------------------------- */
+int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor,
+                         const float* values, uint32_t n);
+int vxb_membrane_snapshot(const vxb_engine* e, uint16_t worker, float* out,
+                          uint32_t cap);
+uint32_t vxb_worker_neurons(const vxb_engine* e, uint16_t worker);
+uint16_t vxb_workers(const vxb_engine* e);
+uint32_t vxb_units(const vxb_engine* e);
+uint32_t vxb_probes(const vxb_engine* e);
+
+/* ---- diagnostics --------------------------------------------------------- */
+/* Device evaluation of stream_normal(base[i], k[i]) (rng.hpp:63-67) exactly as
+ * the step kernel computes it, for noise-parity checks against the host. */
+int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
+                            double* out);
+
+/* ---- one-call convenience (run_simulation, engine.hpp:92-93) ------------- */
+/* Creates, advances `steps` and returns the engine holding the results. */
+int vxb_run_simulation(const vxb_network* net, const vxb_options* opt,
+                       uint32_t steps, vxb_engine** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VXB_H */

@@ -1,0 +1,987 @@
+// vxb_engine.cu — host side of the B200 simulation step and the C ABI of
+// include/vxb.h.
+//
+// The engine mirrors voxsim::SimInstance (engine.hpp:68-89, engine.cpp):
+//   load      (engine.cpp:175-293)  -> Engine::load: validation with the same
+//             error kinds/messages, per-segment parameter tables, SoA state
+//             upload, out-CSR built on the device (engine.cpp:295-344)
+//   advance   (engine.cpp:763-827)  -> Engine::advance: one cooperative
+//             persistent kernel per chunk of steps (vxb_kernels.cuh), results
+//             read back into RunResult-shaped buffers
+//   set_conductances / membrane_snapshot (engine.cpp:829-849)
+// All workers of the tables are concatenated on one device ("shard"): worker
+// w occupies shard-local indices [wbase[w], wbase[w] + n_w), so the raster's
+// (step, worker, local) order is the shard-local order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "vxb.h"
+#include "vxb_kernels.cuh"
+
+namespace {
+
+using namespace vxb;
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct SimError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw SimError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                           #x + ")");                                                  \
+    } while (0)
+
+thread_local std::string g_create_error;
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+struct Probe {
+    uint64_t gid;
+    uint32_t local;  // shard-local
+};
+
+struct Engine {
+    // ---------------------------------------------------------- static
+    uint16_t workers = 1;
+    uint32_t n_units = 0, n_voxels = 0;
+    uint64_t seed = 0;
+    double dt_ms = 1.0;
+    float dtf = 1.0f;
+    bool record_raster = true, record_timings = true;
+    uint16_t workers_per_node = 4;
+    int device = 0;
+    std::vector<vxb_unit> units;
+    std::vector<uint16_t> unit_worker;
+    std::vector<uint32_t> unit_local_base;
+    std::vector<uint32_t> wbase;  // per worker, shard-local base (size workers+1)
+    uint32_t n = 0;
+    std::vector<SegParams> segs;
+    std::vector<uint32_t> seg_start;
+    std::vector<Probe> probes;
+    std::vector<std::pair<uint32_t, uint32_t>> forced;  // (abs step, shard-local)
+    std::vector<vxb_injection> injections;
+    bool packed = true;
+    uint64_t n_syn = 0;
+
+    // ---------------------------------------------------------- device
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int grid = 0;
+    DevBuf<SegParams> d_seg;
+    DevBuf<uint32_t> d_seg_start;
+    DevBuf<uint32_t> d_v;
+    DevBuf<float4> d_j;
+    DevBuf<float> d_iou, d_isyn;
+    DevBuf<float4> d_g;
+    DevBuf<unsigned char> d_pend0, d_pend1;
+    DevBuf<uint64_t> d_off;
+    DevBuf<uint32_t> d_inner;
+    DevBuf<uint32_t> d_tgt;
+    DevBuf<uint64_t> d_w;
+    DevBuf<uint32_t> d_spk;
+    DevBuf<uint32_t> d_seg_end;
+    DevBuf<uint32_t> d_rates;
+    DevBuf<uint32_t> d_probe_local, d_probe_slot;
+    DevBuf<float> d_probe_v, d_probe_i;
+    DevBuf<uint32_t> d_forced_off, d_forced_local;
+    DevBuf<uint32_t> d_inj_epoch;
+    DevBuf<float> d_inj_table;
+    DevBuf<unsigned long long> d_phase_ns;
+    DevBuf<Control> d_ctl;
+    DevBuf<uint64_t> d_keys, d_keys_sorted;
+    DevBuf<unsigned char> d_cub_tmp;
+
+    // ---------------------------------------------------------- run state
+    uint32_t step_done = 0;
+    bool failed = false;
+    std::string err;
+
+    // last advance
+    uint32_t res_steps = 0;
+    uint32_t res_start = 0;
+    std::vector<uint64_t> raster_keys;  // (rel step << 32 | shard-local), sorted
+    std::vector<uint32_t> rates;        // [unit][steps]
+    std::vector<float> probe_v, probe_i;
+    vxb_flops flops{};
+    uint64_t total_spikes = 0;
+    std::vector<vxb_step_timings> timings;
+    double device_ms = 0;
+    uint64_t h2d = 0, d2h = 0, launches = 0;
+
+    ~Engine() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void load(const vxb_network* net, const vxb_options* opt);
+    void build_csr(const vxb_network* net);
+    void advance(uint32_t steps);
+    void run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps);
+    uint32_t seg_of(uint32_t local) const {
+        return (uint32_t)(std::upper_bound(seg_start.begin(), seg_start.end(), local) -
+                          seg_start.begin()) -
+               1;
+    }
+    // layout.cpp:119-128
+    const vxb_unit& unit_of_gid(uint64_t gid, uint32_t* uid) const {
+        uint64_t total = 0;
+        for (const auto& u : units) total = std::max<uint64_t>(total, u.gid_base + u.neurons);
+        if (gid >= total || units.empty()) throw SimError("gid out of range");
+        size_t lo = 0, hi = units.size();
+        while (lo < hi) {
+            size_t mid = (lo + hi) / 2;
+            if (gid < units[mid].gid_base)
+                hi = mid;
+            else
+                lo = mid + 1;
+        }
+        size_t i = lo - 1;
+        while (units[i].neurons == 0) --i;
+        *uid = (uint32_t)i;
+        return units[i];
+    }
+};
+
+std::string fmt(const char* f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+// NeuronParams::validate (model.cpp:7-26)
+void validate_params(const vxb_neuron& r, float dtf) {
+    if (!(r.capacitance > 0)) throw ConfigError("neuron params: capacitance must be > 0");
+    if (r.g_leak < 0) throw ConfigError("neuron params: leak conductance must be >= 0");
+    if (!(r.v_reset < r.v_threshold))
+        throw ConfigError("neuron params: V_reset must be below V_th");
+    for (int u = 0; u < 4; ++u) {
+        if (!(r.tau[u] > 0)) throw ConfigError("neuron params: receptor tau must be > 0");
+        if (!(dtf < r.tau[u]))
+            throw ConfigError(
+                "neuron params: dt must be below every receptor tau (explicit Euler)");
+        if (r.g[u] < 0 || r.omega[u] < 0)
+            throw ConfigError(
+                "neuron params: receptor conductance and jump weights must be >= 0");
+    }
+    if (r.e_rev[0] <= r.v_threshold || r.e_rev[1] <= r.v_threshold)
+        throw ConfigError("neuron params: excitatory reversals must lie above V_th");
+    if (r.e_rev[2] >= r.e_leak || r.e_rev[3] >= r.e_leak)
+        throw ConfigError("neuron params: inhibitory reversals must lie below E_L");
+}
+
+SegParams make_seg(const vxb_neuron& r, uint32_t start, uint32_t worker, float dtf) {
+    SegParams s;
+    std::memset(&s, 0, sizeof s);
+    s.gid_off = (int64_t)r.gid - (int64_t)start;
+    s.start = start;
+    s.unit = r.unit;
+    s.voxel = r.voxel;
+    s.worker = worker;
+    s.tref = r.refractory_steps;
+    // Host float arithmetic, one rounding per operation, as at the
+    // reference's load / kernel sites.
+    volatile float c = r.capacitance;
+    s.dt_over_c = dtf / c;  // engine.cpp:242
+    s.g_leak = r.g_leak;
+    s.e_leak = r.e_leak;
+    s.v_th = r.v_threshold;
+    s.v_reset = r.v_reset;
+    for (int u = 0; u < 4; ++u) {
+        volatile float q = dtf / r.tau[u];
+        s.decay[u] = 1.0f - q;  // gating_kernel: j * (1 - dt / tau)
+        s.omega[u] = r.omega[u];
+        s.e_rev[u] = r.e_rev[u];
+    }
+    s.ou_mu = r.ou_mean;
+    s.ou_a = dtf / r.ou_tau;  // ou_kernel: (dt / tau)
+    volatile float two_dt = 2.0f * dtf;
+    volatile float ratio = two_dt / r.ou_tau;
+    volatile float sq = std::sqrt((float)ratio);
+    s.ou_b = r.ou_sigma * sq;  // sigma * sqrt(2 dt / tau)
+    s.sigma_pos = r.ou_sigma > 0 ? 1u : 0u;
+    return s;
+}
+
+bool same_params(const SegParams& s, const vxb_neuron& r, uint32_t local, uint32_t worker,
+                 float dtf) {
+    SegParams t = make_seg(r, local, worker, dtf);
+    t.start = s.start;
+    t.gid_off = (int64_t)r.gid - (int64_t)local;
+    return std::memcmp(&s, &t, sizeof s) == 0;
+}
+
+void Engine::load(const vxb_network* net, const vxb_options* opt) {
+    if (!net || !opt) throw ConfigError("null network or options");
+    if (net->n_workers == 0) throw ConfigError("no worker tables");
+    if (net->n_workers > 64) throw ConfigError("worker counts above 64 are unsupported");
+    workers = (uint16_t)net->n_workers;
+    n_units = net->n_units;
+    n_voxels = net->n_voxels;
+    seed = net->workers[0].seed;
+    units.assign(net->units, net->units + n_units);
+    unit_worker.assign(net->unit_worker, net->unit_worker + n_units);
+    unit_local_base.assign(net->unit_local_base, net->unit_local_base + n_units);
+
+    dt_ms = opt->dt_ms;
+    if (!(opt->dt_ms > 0.0)) throw ConfigError("dt must be positive");
+    if (opt->workers_per_node == 0) throw ConfigError("workers_per_node must be >= 1");
+    workers_per_node = opt->workers_per_node;
+    const std::string sched = opt->scheduler ? opt->scheduler : "cuda";
+    if (sched != "cuda" && sched != "threads" && sched != "loopback")
+        throw ConfigError("unknown scheduler: " + sched);
+    dtf = (float)opt->dt_ms;
+    for (uint32_t k = 0; k < opt->n_injections; ++k) {
+        const vxb_injection& inj = opt->injections[k];
+        if (inj.voxel >= n_voxels) throw ConfigError("injection voxel out of range");
+        if (inj.to_step < inj.from_step) throw ConfigError("injection interval is reversed");
+        injections.push_back(inj);
+    }
+    record_raster = opt->record_raster != 0;
+    record_timings = opt->record_timings != 0;
+
+    // shard-local layout and parameter segments
+    wbase.assign(workers + 1, 0);
+    for (uint16_t wi = 0; wi < workers; ++wi) {
+        const vxb_worker_table& t = net->workers[wi];
+        if (t.worker != wi || t.worker_count != workers)
+            throw ConfigError("worker table ids are inconsistent");
+        wbase[wi + 1] = wbase[wi] + t.n_neurons;
+    }
+    if ((uint64_t)wbase[workers] >= (1ull << 31))
+        throw ConfigError("more than 2^31 neurons on one device");
+    n = wbase[workers];
+    std::vector<uint32_t> h_v(n);
+    std::vector<float4> h_g(n);
+    std::vector<float> h_iou(n);
+    std::vector<unsigned long long> h_mask(n);
+    for (uint16_t wi = 0; wi < workers; ++wi) {
+        const vxb_worker_table& t = net->workers[wi];
+        for (uint32_t i = 0; i < t.n_neurons; ++i) {
+            const vxb_neuron& r = t.neurons[i];
+            validate_params(r, dtf);
+            if (r.unit >= n_units || r.voxel >= n_voxels)
+                throw ConfigError("neuron record references unknown unit/voxel");
+            if (r.refractory_steps >= (1u << 23))
+                throw ConfigError("refractory_steps above 2^23 are unsupported");
+            const uint32_t loc = wbase[wi] + i;
+            bool extend = !segs.empty() && segs.back().worker == wi &&
+                          (int64_t)r.gid - (int64_t)loc == segs.back().gid_off &&
+                          same_params(segs.back(), r, loc, wi, dtf);
+            if (!extend) {
+                segs.push_back(make_seg(r, loc, wi, dtf));
+                seg_start.push_back(loc);
+            }
+            // Non-finite v_init: keep it non-finite but outside the
+            // refractory code space, so step 0 diverges like the reference.
+            float vi = r.v_init;
+            uint32_t bits;
+            std::memcpy(&bits, &vi, 4);
+            if (!std::isfinite(vi)) bits = 0x7f800000u;
+            h_v[loc] = bits;
+            h_g[loc] = make_float4(r.g[0], r.g[1], r.g[2], r.g[3]);
+            h_iou[loc] = r.ou_mean;  // stationary start (engine.cpp:265)
+            h_mask[loc] = r.dst_mask;
+        }
+    }
+
+    // device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw SimError("no CUDA device available (the cuda scheduler has no CPU fallback)");
+    device = opt->device >= 0 ? opt->device : 0;
+    if (opt->device < 0) CK(cudaGetDevice(&device));
+    if (device >= ndev) throw ConfigError("CUDA device out of range");
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+
+    d_seg.alloc(segs.size());
+    d_seg_start.alloc(seg_start.size());
+    CK(cudaMemcpyAsync(d_seg.p, segs.data(), segs.size() * sizeof(SegParams),
+                       cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_seg_start.p, seg_start.data(), seg_start.size() * 4,
+                       cudaMemcpyHostToDevice, stream));
+    d_v.alloc(n);
+    d_j.alloc(n);
+    d_iou.alloc(n);
+    d_isyn.alloc(n);
+    d_g.alloc(n);
+    CK(cudaMemcpyAsync(d_v.p, h_v.data(), 4ull * n, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_g.p, h_g.data(), 16ull * n, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_iou.p, h_iou.data(), 4ull * n, cudaMemcpyHostToDevice, stream));
+    d_j.zero(stream);
+    d_isyn.zero(stream);
+
+    // out-CSR + mask consistency
+    build_csr(net);
+    {
+        DevBuf<unsigned long long> d_mask, d_bad;
+        d_mask.alloc(n);
+        d_bad.alloc(1);
+        CK(cudaMemcpyAsync(d_mask.p, h_mask.data(), 8ull * n, cudaMemcpyHostToDevice, stream));
+        unsigned long long init = ~0ull;
+        CK(cudaMemcpyAsync(d_bad.p, &init, 8, cudaMemcpyHostToDevice, stream));
+        // have_mask was left in d_keys by build_csr
+        if (n)
+            mask_check_kernel<<<1184, 256, 0, stream>>>(
+                reinterpret_cast<unsigned long long*>(d_keys.p), d_mask.p, n, d_bad.p);
+        CK(cudaGetLastError());
+        unsigned long long bad = 0;
+        CK(cudaMemcpyAsync(&bad, d_bad.p, 8, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (bad != ~0ull) {
+            unsigned long long have = 0;
+            CK(cudaMemcpy(&have, reinterpret_cast<unsigned long long*>(d_keys.p) + bad, 8,
+                          cudaMemcpyDeviceToHost));
+            const uint32_t s = (uint32_t)(std::upper_bound(wbase.begin(), wbase.end(),
+                                                           (uint32_t)bad) - wbase.begin()) - 1;
+            const uint64_t diff = have ^ h_mask[bad];
+            int d = 0;
+            while (!((diff >> d) & 1ull)) ++d;
+            throw SimError(fmt("destination mask inconsistent with tables (worker %u neuron %u "
+                               "-> worker %d)",
+                               s, (unsigned)(bad - wbase[s]), d));
+        }
+        d_keys.release();
+    }
+
+    const size_t pend_bytes = (packed ? 16ull : 32ull) * n;
+    d_pend0.alloc(pend_bytes);
+    d_pend1.alloc(pend_bytes);
+    d_pend0.zero(stream);
+    d_pend1.zero(stream);
+    d_ctl.alloc(1);
+
+    // probes and forced spikes (engine.cpp:276-290)
+    for (uint32_t s = 0; s < opt->n_probes; ++s) {
+        uint32_t uid;
+        const vxb_unit& u = unit_of_gid(opt->probe_gids[s], &uid);
+        const uint32_t loc = wbase[unit_worker[uid]] + unit_local_base[uid] +
+                             (uint32_t)(opt->probe_gids[s] - u.gid_base);
+        probes.push_back({opt->probe_gids[s], loc});
+    }
+    for (uint32_t f = 0; f < opt->n_forced; ++f) {
+        uint32_t uid;
+        const vxb_unit& u = unit_of_gid(opt->forced_spikes[f].gid, &uid);
+        const uint32_t loc = wbase[unit_worker[uid]] + unit_local_base[uid] +
+                             (uint32_t)(opt->forced_spikes[f].gid - u.gid_base);
+        forced.push_back({opt->forced_spikes[f].step, loc});
+    }
+    std::sort(forced.begin(), forced.end());
+    forced.erase(std::unique(forced.begin(), forced.end()), forced.end());
+    if (!probes.empty()) {
+        std::vector<std::pair<uint32_t, uint32_t>> ps;
+        for (uint32_t s = 0; s < probes.size(); ++s) ps.push_back({probes[s].local, s});
+        std::sort(ps.begin(), ps.end());
+        std::vector<uint32_t> pl, pslot;
+        for (auto& x : ps) {
+            pl.push_back(x.first);
+            pslot.push_back(x.second);
+        }
+        d_probe_local.alloc(pl.size());
+        d_probe_slot.alloc(pslot.size());
+        CK(cudaMemcpyAsync(d_probe_local.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice,
+                           stream));
+        CK(cudaMemcpyAsync(d_probe_slot.p, pslot.data(), 4 * pslot.size(),
+                           cudaMemcpyHostToDevice, stream));
+    }
+
+    // transport (engine.cpp:292, transport.cpp:124-128)
+    const std::string tr = opt->transport ? opt->transport : "queue";
+    if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
+
+    // cooperative grid
+    int sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (packed)
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0));
+    else
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0));
+    if (per_sm < 1) throw SimError("step kernel cannot be resident on this device");
+    grid = sms * per_sm;
+    CK(cudaStreamSynchronize(stream));
+}
+
+void Engine::build_csr(const vxb_network* net) {
+    DevBuf<unsigned long long> cnt;  // counts, then cursors
+    cnt.alloc((size_t)n + 1);
+    cnt.zero(stream);
+    DevBuf<uint32_t> d_wbase, d_wn;
+    d_wbase.alloc(workers);
+    d_wn.alloc(workers);
+    std::vector<uint32_t> wn(workers);
+    for (uint16_t w = 0; w < workers; ++w) wn[w] = net->workers[w].n_neurons;
+    CK(cudaMemcpyAsync(d_wbase.p, wbase.data(), 4ull * workers, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_wn.p, wn.data(), 4ull * workers, cudaMemcpyHostToDevice, stream));
+    DevBuf<unsigned int> flags;  // [0] bad source, [1] needs wide accumulators
+    flags.alloc(2);
+    flags.zero(stream);
+
+    n_syn = 0;
+    for (uint16_t w = 0; w < workers; ++w) n_syn += net->workers[w].n_synapses;
+    // stage all in-rows once (16 B / synapse), then count and scatter
+    std::vector<std::unique_ptr<DevBuf<SynIn>>> stage(workers);
+    std::vector<std::unique_ptr<DevBuf<uint64_t>>> rb(workers);
+    for (uint16_t w = 0; w < workers; ++w) {
+        const vxb_worker_table& t = net->workers[w];
+        stage[w] = std::make_unique<DevBuf<SynIn>>();
+        rb[w] = std::make_unique<DevBuf<uint64_t>>();
+        stage[w]->alloc(t.n_synapses);
+        rb[w]->alloc((size_t)t.n_neurons + 1);
+        if (t.n_synapses)
+            CK(cudaMemcpyAsync(stage[w]->p, t.synapses, 16ull * t.n_synapses,
+                               cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(rb[w]->p, t.row_base, 8ull * (t.n_neurons + 1),
+                           cudaMemcpyHostToDevice, stream));
+        if (t.n_synapses)
+            csr_count_kernel<<<2368, 256, 0, stream>>>(stage[w]->p, t.n_synapses, d_wbase.p,
+                                                       d_wn.p, workers, cnt.p + 1, flags.p);
+        CK(cudaGetLastError());
+    }
+    unsigned int bad = 0;
+    CK(cudaMemcpyAsync(&bad, flags.p, 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (bad) throw SimError("synapse entry references a nonexistent source");
+
+    // exclusive offsets: off[0] = 0, off[i+1] = sum(cnt[0..i])
+    d_off.alloc((size_t)n + 1);
+    {
+        size_t tmp = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.p + 1,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         stream));
+        DevBuf<unsigned char> t;
+        t.alloc(tmp ? tmp : 1);
+        CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cnt.p + 1,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         stream));
+        CK(cudaMemsetAsync(d_off.p, 0, 8, stream));
+    }
+    CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n, cudaMemcpyDeviceToDevice, stream));
+    d_tgt.alloc(n_syn);
+    d_w.alloc(n_syn);
+    d_inner.alloc(n);
+    d_inner.zero(stream);
+    d_keys.alloc(n);  // reused as have_mask for the consistency check
+    d_keys.zero(stream);
+    for (uint16_t w = 0; w < workers; ++w) {
+        const vxb_worker_table& t = net->workers[w];
+        if (t.n_neurons)
+            csr_scatter_kernel<<<2368, 256, 0, stream>>>(
+                stage[w]->p, rb[w]->p, t.n_neurons, w, wbase[w], d_wbase.p, cnt.p, d_tgt.p,
+                d_w.p, reinterpret_cast<unsigned long long*>(d_keys.p), d_inner.p, flags.p + 1);
+        CK(cudaGetLastError());
+    }
+    unsigned int wide = 0;
+    CK(cudaMemcpyAsync(&wide, flags.p + 1, 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    packed = wide == 0;
+}
+
+struct Chunk {
+    uint32_t t0, rel0, steps;
+};
+
+void Engine::advance(uint32_t steps) {
+    if (failed) throw SimError("instance is in a failed state");
+    res_steps = steps;
+    res_start = step_done;
+    raster_keys.clear();
+    rates.assign((size_t)n_units * steps, 0);
+    probe_v.assign(probes.size() * (size_t)steps, 0.0f);
+    probe_i.assign(probes.size() * (size_t)steps, 0.0f);
+    flops = vxb_flops{};
+    total_spikes = 0;
+    timings.clear();
+    device_ms = 0;
+    h2d = d2h = launches = 0;
+    if (steps == 0) return;
+    CK(cudaSetDevice(device));
+
+    // per-advance tables: forced spikes and injection epochs by relative step
+    std::vector<uint32_t> f_off(steps + 1, 0), f_loc;
+    {
+        size_t k = 0;
+        while (k < forced.size() && forced[k].first < step_done) ++k;
+        for (uint32_t rel = 0; rel < steps; ++rel) {
+            f_off[rel] = (uint32_t)f_loc.size();
+            while (k < forced.size() && forced[k].first == step_done + rel)
+                f_loc.push_back(forced[k++].second);
+        }
+        f_off[steps] = (uint32_t)f_loc.size();
+    }
+    std::vector<uint32_t> inj_ep(steps, 0);
+    std::vector<float> inj_tab;
+    if (!injections.empty()) {
+        std::map<std::vector<uint32_t>, uint32_t> seen;  // active set -> epoch
+        for (uint32_t rel = 0; rel < steps; ++rel) {
+            const uint32_t t = step_done + rel;
+            std::vector<uint32_t> act;
+            for (uint32_t k = 0; k < injections.size(); ++k)
+                if (injections[k].from_step <= t && t < injections[k].to_step) act.push_back(k);
+            if (act.empty()) continue;
+            auto it = seen.find(act);
+            if (it == seen.end()) {
+                std::vector<float> vox(n_voxels, 0.0f);  // engine.cpp:355-361, list order
+                for (uint32_t k : act) vox[injections[k].voxel] += injections[k].current_pa;
+                inj_tab.insert(inj_tab.end(), vox.begin(), vox.end());
+                it = seen.emplace(act, (uint32_t)seen.size() + 1).first;
+            }
+            inj_ep[rel] = it->second;
+        }
+    }
+    const bool has_forced = !f_loc.empty(), has_inj = !inj_tab.empty();
+    if (has_forced) {
+        d_forced_off.alloc(f_off.size());
+        d_forced_local.alloc(f_loc.size());
+        CK(cudaMemcpyAsync(d_forced_off.p, f_off.data(), 4 * f_off.size(),
+                           cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_forced_local.p, f_loc.data(), 4 * f_loc.size(),
+                           cudaMemcpyHostToDevice, stream));
+        h2d += 4 * (f_off.size() + f_loc.size());
+    }
+    if (has_inj) {
+        d_inj_epoch.alloc(steps);
+        d_inj_table.alloc(inj_tab.size());
+        CK(cudaMemcpyAsync(d_inj_epoch.p, inj_ep.data(), 4ull * steps, cudaMemcpyHostToDevice,
+                           stream));
+        CK(cudaMemcpyAsync(d_inj_table.p, inj_tab.data(), 4 * inj_tab.size(),
+                           cudaMemcpyHostToDevice, stream));
+        h2d += 4ull * steps + 4 * inj_tab.size();
+    }
+    if (!probes.empty()) {
+        d_probe_v.alloc(probes.size() * (size_t)steps);
+        d_probe_i.alloc(probes.size() * (size_t)steps);
+        d_probe_v.zero(stream);
+        d_probe_i.zero(stream);
+    }
+
+    // chunking: the linear spike log holds n entries per step of a chunk
+    uint32_t chunk = steps;
+    if (record_raster) {
+        const uint64_t cap = 1ull << 29;  // 2 GiB of spike ids per chunk
+        chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(steps, cap / std::max(1u, n)));
+    }
+    const uint32_t cap_entries = record_raster ? n * chunk : 2 * n;
+    if (d_spk.n < std::max<size_t>(1, cap_entries)) d_spk.alloc(std::max<size_t>(1, cap_entries));
+    d_seg_end.alloc(chunk + 2);
+    d_rates.alloc((size_t)n_units * chunk);
+    d_phase_ns.alloc(chunk + 2);
+
+    std::vector<unsigned long long> phase_ns_all;
+    phase_ns_all.reserve(steps + 2);
+    for (uint32_t rel0 = 0; rel0 < steps; rel0 += chunk) {
+        const uint32_t cs = std::min(chunk, steps - rel0);
+        run_chunk(step_done + rel0, rel0, cs, steps);
+        // phase end times of this chunk
+        std::vector<unsigned long long> ph(cs + 2);
+        CK(cudaMemcpyAsync(ph.data(), d_phase_ns.p, 8ull * (cs + 2), cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaStreamSynchronize(stream));
+        d2h += 8ull * (cs + 2);
+        if (phase_ns_all.empty()) phase_ns_all.push_back(ph[0]);
+        for (uint32_t p = 1; p <= cs + 1; ++p) phase_ns_all.push_back(ph[p]);
+        // the next chunk re-runs no phase: its A-only prologue follows this
+        // chunk's E-only epilogue; stitch their times together.
+    }
+
+    // probes
+    if (!probes.empty()) {
+        CK(cudaMemcpyAsync(probe_v.data(), d_probe_v.p, 4 * probe_v.size(),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(probe_i.data(), d_probe_i.p, 4 * probe_i.size(),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        d2h += 8 * probe_v.size();
+    }
+    for (uint32_t x : rates) total_spikes += x;
+    const uint64_t nn = n;
+    flops.membrane += 6ull * nn * steps;       // engine.cpp:387
+    flops.gating_decay += 12ull * nn * steps;  // engine.cpp:560
+    flops.current += 16ull * nn * steps;       // engine.cpp:561
+
+    if (record_timings) {
+        // One row per (step, worker).  The cuda scheduler has no per-worker
+        // threads: t1 = the phase holding A(t), t3 adds the phase holding E(t).
+        timings.resize((size_t)steps * workers);
+        std::vector<uint32_t> unit_of_worker_spikes((size_t)steps * workers, 0);
+        for (uint32_t u = 0; u < n_units; ++u)
+            for (uint32_t s = 0; s < steps; ++s)
+                unit_of_worker_spikes[(size_t)s * workers + unit_worker[u]] +=
+                    rates[(size_t)u * steps + s];
+        for (uint32_t s = 0; s < steps; ++s) {
+            // phase_ns_all[k] = end of global phase k-1; phase of A(s) is s
+            const int64_t a = (int64_t)(phase_ns_all[s + 1] - phase_ns_all[s]);
+            const int64_t e = (int64_t)(phase_ns_all[s + 2] - phase_ns_all[s + 1]);
+            for (uint16_t w = 0; w < workers; ++w) {
+                vxb_step_timings& r = timings[(size_t)s * workers + w];
+                std::memset(&r, 0, sizeof r);
+                r.step = step_done + s;
+                r.worker = w;
+                r.spikes = unit_of_worker_spikes[(size_t)s * workers + w];
+                r.t[0] = a;      // t1
+                r.t[1] = a;      // t2: no inbound wait on one device
+                r.t[2] = a + e;  // t3
+                r.t[3] = r.t[4] = r.t[0];
+                r.t[5] = r.t[6] = r.t[1];
+            }
+        }
+    }
+    step_done += steps;
+}
+
+void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
+    Control c0;
+    std::memset(&c0, 0, sizeof c0);
+    c0.err = ~0ull;
+    CK(cudaMemcpyAsync(d_ctl.p, &c0, sizeof c0, cudaMemcpyHostToDevice, stream));
+    d_rates.zero(stream);
+    CK(cudaMemsetAsync(d_seg_end.p, 0, 4 * d_seg_end.n, stream));
+
+    StepArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.n = n;
+    a.nseg = (uint32_t)segs.size();
+    a.n_units = n_units;
+    a.steps = steps;
+    a.t0 = t0;
+    a.rel0 = rel0;
+    a.adv_steps = adv_steps;
+    a.spk_cap = (uint32_t)d_spk.n;
+    a.ring = record_raster ? 0u : 1u;
+    a.use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg ? 1u : 0u;
+    a.dtf = dtf;
+    a.ou_root = mix_key(seed, 1);  // rngstream::ou_noise (rng.hpp:18)
+    a.seg = d_seg.p;
+    a.seg_start = d_seg_start.p;
+    a.v = d_v.p;
+    a.j = d_j.p;
+    a.i_ou = d_iou.p;
+    a.i_syn = d_isyn.p;
+    a.g = d_g.p;
+    a.pend0 = d_pend0.p;
+    a.pend1 = d_pend1.p;
+    a.off = d_off.p;
+    a.inner = d_inner.p;
+    a.tgt = d_tgt.p;
+    a.w = d_w.p;
+    a.spk = d_spk.p;
+    a.seg_end = d_seg_end.p;
+    a.rates = d_rates.p;
+    a.n_probes = (uint32_t)probes.size();
+    a.probe_local = d_probe_local.p;
+    a.probe_slot = d_probe_slot.p;
+    a.probe_v = d_probe_v.p;
+    a.probe_i = d_probe_i.p;
+    a.has_forced = d_forced_off.n ? 1u : 0u;
+    a.forced_off = a.has_forced ? d_forced_off.p + rel0 : nullptr;
+    a.forced_local = d_forced_local.p;
+    a.has_inj = d_inj_epoch.n ? 1u : 0u;
+    a.inj_epoch = a.has_inj ? d_inj_epoch.p + rel0 : nullptr;
+    a.inj_table = d_inj_table.p;
+    a.n_voxels = n_voxels;
+    a.phase_ns = d_phase_ns.p;
+    a.ctl = d_ctl.p;
+
+    void* args[] = {&a};
+    CK(cudaEventRecord(ev0, stream));
+    if (packed)
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args, 0,
+                                       stream));
+    else
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<false>, grid, kThreads, args, 0,
+                                       stream));
+    CK(cudaEventRecord(ev1, stream));
+    launches += 1;
+
+    Control c;
+    CK(cudaMemcpyAsync(&c, d_ctl.p, sizeof c, cudaMemcpyDeviceToHost, stream));
+    std::vector<uint32_t> rr((size_t)n_units * steps);
+    if (!rr.empty())
+        CK(cudaMemcpyAsync(rr.data(), d_rates.p, 4 * rr.size(), cudaMemcpyDeviceToHost, stream));
+    std::vector<uint32_t> seg_end(steps + 1);
+    CK(cudaMemcpyAsync(seg_end.data(), d_seg_end.p, 4ull * (steps + 1), cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    device_ms += ms;
+    d2h += sizeof c + 4 * rr.size() + 4ull * (steps + 1);
+    if (c.err != ~0ull) {
+        failed = true;
+        const uint32_t step = (uint32_t)(c.err >> 32), loc = (uint32_t)(c.err & 0xffffffffu);
+        const SegParams& s = segs[seg_of(loc)];
+        throw SimError(fmt("membrane potential diverged (neuron %llu, step %u)",
+                           (unsigned long long)((int64_t)loc + s.gid_off), step));
+    }
+    for (uint32_t u = 0; u < n_units; ++u)
+        for (uint32_t s = 0; s < steps; ++s)
+            rates[(size_t)u * adv_steps + rel0 + s] += rr[(size_t)u * steps + s];
+    flops.gating_inner += c.flops_inner;
+    flops.gating_outer += c.flops_outer;
+
+    if (record_raster) {
+        const uint32_t total = seg_end[steps - 1];
+        if (total) {
+            if (d_keys.n < total) d_keys.alloc(total);
+            if (d_keys_sorted.n < total) d_keys_sorted.alloc(total);
+            raster_keys_kernel<<<std::min<uint32_t>(steps, 4096), 256, 0, stream>>>(
+                d_spk.p, d_seg_end.p, steps, d_keys.p);
+            CK(cudaGetLastError());
+            launches += 1;
+            int end_bit = 32;
+            while ((1ull << (end_bit - 32)) < steps) ++end_bit;
+            size_t tmp = 0;
+            CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp,
+                                              reinterpret_cast<unsigned long long*>(d_keys.p),
+                                              reinterpret_cast<unsigned long long*>(d_keys_sorted.p),
+                                              total, 0, end_bit, stream));
+            if (d_cub_tmp.n < tmp) d_cub_tmp.alloc(tmp);
+            CK(cub::DeviceRadixSort::SortKeys(d_cub_tmp.p, tmp,
+                                              reinterpret_cast<unsigned long long*>(d_keys.p),
+                                              reinterpret_cast<unsigned long long*>(d_keys_sorted.p),
+                                              total, 0, end_bit, stream));
+            launches += 1;
+            const size_t base = raster_keys.size();
+            raster_keys.resize(base + total);
+            CK(cudaMemcpyAsync(raster_keys.data() + base, d_keys_sorted.p, 8ull * total,
+                               cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            d2h += 8ull * total;
+            const uint64_t add = (uint64_t)rel0 << 32;
+            for (size_t k = base; k < raster_keys.size(); ++k) raster_keys[k] += add;
+        }
+    }
+}
+
+int fail_code(const std::exception& e) {
+    return dynamic_cast<const ConfigError*>(&e) ? VXB_ECONFIG : VXB_ESIM;
+}
+
+}  // namespace
+
+struct vxb_engine {
+    Engine eng;
+};
+
+extern "C" {
+
+int vxb_abi_version(void) { return VXB_ABI_VERSION; }
+
+const char* vxb_last_error(const vxb_engine* e) {
+    return e ? e->eng.err.c_str() : g_create_error.c_str();
+}
+
+int vxb_create(const vxb_network* net, const vxb_options* opt, vxb_engine** out) {
+    *out = nullptr;
+    auto* e = new vxb_engine();
+    try {
+        e->eng.load(net, opt);
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        int rc = fail_code(x);
+        delete e;
+        return rc;
+    }
+    *out = e;
+    return VXB_OK;
+}
+
+void vxb_destroy(vxb_engine* e) { delete e; }
+
+int vxb_advance(vxb_engine* e, uint32_t steps) {
+    try {
+        e->eng.advance(steps);
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        e->eng.err = x.what();
+        e->eng.failed = true;
+        return fail_code(x);
+    }
+}
+
+uint32_t vxb_current_step(const vxb_engine* e) { return e->eng.step_done; }
+uint32_t vxb_result_steps_done(const vxb_engine* e) { return e->eng.res_steps; }
+uint64_t vxb_result_total_spikes(const vxb_engine* e) { return e->eng.total_spikes; }
+uint64_t vxb_result_raster_size(const vxb_engine* e) { return e->eng.raster_keys.size(); }
+
+int vxb_result_raster(const vxb_engine* e, vxb_raster_event* out, uint64_t cap) {
+    const Engine& g = e->eng;
+    if (cap < g.raster_keys.size()) return VXB_ECONFIG;
+    for (size_t k = 0; k < g.raster_keys.size(); ++k) {
+        const uint64_t key = g.raster_keys[k];
+        const uint32_t loc = (uint32_t)(key & 0xffffffffu);
+        const SegParams& s = g.segs[g.seg_of(loc)];
+        vxb_raster_event r;
+        std::memset(&r, 0, sizeof r);
+        r.step = g.res_start + (uint32_t)(key >> 32);
+        r.worker = (uint16_t)s.worker;
+        r.local = loc - g.wbase[s.worker];
+        r.gid = (uint64_t)((int64_t)loc + s.gid_off);
+        out[k] = r;
+    }
+    return VXB_OK;
+}
+
+int vxb_result_rates(const vxb_engine* e, uint32_t* counts, uint64_t cap) {
+    if (cap < e->eng.rates.size()) return VXB_ECONFIG;
+    std::memcpy(counts, e->eng.rates.data(), 4 * e->eng.rates.size());
+    return VXB_OK;
+}
+
+int vxb_result_probes(const vxb_engine* e, float* v, float* i_syn, uint64_t cap) {
+    if (cap < e->eng.probe_v.size()) return VXB_ECONFIG;
+    std::memcpy(v, e->eng.probe_v.data(), 4 * e->eng.probe_v.size());
+    std::memcpy(i_syn, e->eng.probe_i.data(), 4 * e->eng.probe_i.size());
+    return VXB_OK;
+}
+
+int vxb_result_flops(const vxb_engine* e, vxb_flops* out) {
+    *out = e->eng.flops;
+    return VXB_OK;
+}
+
+uint64_t vxb_result_timings_size(const vxb_engine* e) { return e->eng.timings.size(); }
+
+int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap) {
+    if (cap < e->eng.timings.size()) return VXB_ECONFIG;
+    std::memcpy(out, e->eng.timings.data(), sizeof(vxb_step_timings) * e->eng.timings.size());
+    return VXB_OK;
+}
+
+double vxb_result_device_ms(const vxb_engine* e) { return e->eng.device_ms; }
+uint64_t vxb_result_h2d_bytes(const vxb_engine* e) { return e->eng.h2d; }
+uint64_t vxb_result_d2h_bytes(const vxb_engine* e) { return e->eng.d2h; }
+uint64_t vxb_result_launches(const vxb_engine* e) { return e->eng.launches; }
+
+int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float* values,
+                         uint32_t n) {
+    Engine& g = e->eng;
+    try {
+        if (unit >= g.n_units) throw ConfigError("unit out of range");
+        if (receptor < 0 || receptor >= 4) throw ConfigError("receptor out of range");
+        if (n != g.units[unit].neurons)
+            throw ConfigError("conductance vector size does not match unit");
+        for (uint32_t i = 0; i < n; ++i)
+            if (!(values[i] >= 0.0f) || !std::isfinite(values[i]))
+                throw ConfigError("conductance values must be finite and >= 0");
+        if (n == 0) return VXB_OK;
+        CK(cudaSetDevice(g.device));
+        const uint32_t base = g.wbase[g.unit_worker[unit]] + g.unit_local_base[unit];
+        std::vector<float4> buf(n);
+        CK(cudaMemcpy(buf.data(), g.d_g.p + base, 16ull * n, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < n; ++i) (&buf[i].x)[receptor] = values[i];
+        CK(cudaMemcpy(g.d_g.p + base, buf.data(), 16ull * n, cudaMemcpyHostToDevice));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
+}
+
+int vxb_membrane_snapshot(const vxb_engine* e, uint16_t worker, float* out, uint32_t cap) {
+    Engine& g = const_cast<Engine&>(e->eng);
+    try {
+        if (worker >= g.workers) throw ConfigError("worker out of range");
+        const uint32_t b = g.wbase[worker], n = g.wbase[worker + 1] - b;
+        if (cap < n) throw ConfigError("snapshot buffer too small");
+        if (n == 0) return VXB_OK;
+        CK(cudaSetDevice(g.device));
+        std::vector<uint32_t> bits(n);
+        CK(cudaMemcpy(bits.data(), g.d_v.p + b, 4ull * n, cudaMemcpyDeviceToHost));
+        for (uint32_t i = 0; i < n; ++i) {
+            if (is_refrac(bits[i])) {
+                out[i] = g.segs[g.seg_of(b + i)].v_reset;
+            } else {
+                std::memcpy(out + i, &bits[i], 4);
+            }
+        }
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
+}
+
+uint32_t vxb_worker_neurons(const vxb_engine* e, uint16_t worker) {
+    if (worker >= e->eng.workers) return 0;
+    return e->eng.wbase[worker + 1] - e->eng.wbase[worker];
+}
+uint16_t vxb_workers(const vxb_engine* e) { return e->eng.workers; }
+uint32_t vxb_units(const vxb_engine* e) { return e->eng.n_units; }
+uint32_t vxb_probes(const vxb_engine* e) { return (uint32_t)e->eng.probes.size(); }
+
+int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
+                            double* out) {
+    try {
+        CK(cudaSetDevice(device));
+        DevBuf<uint64_t> b, kk;
+        DevBuf<double> o;
+        b.alloc(n);
+        kk.alloc(n);
+        o.alloc(n);
+        CK(cudaMemcpy(b.p, base, 8 * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(kk.p, k, 8 * n, cudaMemcpyHostToDevice));
+        debug_normal_kernel<<<1184, 256>>>(b.p, kk.p, n, o.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, o.p, 8 * n, cudaMemcpyDeviceToHost));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return fail_code(x);
+    }
+}
+
+int vxb_run_simulation(const vxb_network* net, const vxb_options* opt, uint32_t steps,
+                       vxb_engine** out) {
+    int rc = vxb_create(net, opt, out);
+    if (rc != VXB_OK) return rc;
+    return vxb_advance(*out, steps);
+}
+
+}  // extern "C"

@@ -1,0 +1,530 @@
+// vxb_kernels.cuh — sm_100a kernels of the voxel-network simulation step.
+//
+// One persistent cooperative kernel runs a whole chunk of steps.  Each grid
+// phase ph does, for absolute steps tA = t0 + ph and tE = tA - 1:
+//
+//   F: for every neuron (static partition, thread-owned state)
+//        E(tE)  gating with the pending buffer of S(tE-1), current, OU noise
+//               (engine.cpp:539-559)
+//        A(tA)  membrane / threshold / refractory / injection / forced spike
+//               (engine.cpp:363-398), spiking neurons appended to the log
+//   D: deliver S(tE) — the spikes A(tE) produced in the previous phase — into
+//      the other pending buffer with integer atomics (engine.cpp:444-464)
+//   grid barrier
+//
+// F and D of one phase touch disjoint pending buffers, so the delivery of a
+// step overlaps the neuron update of the next: the one-step synaptic delay
+// of the reference (test_engine.cpp:203-246) is the slack that makes the
+// fusion legal.  Phase 0 of a chunk is A only, the last phase is E only, so
+// the state between chunks (and between advance() calls) is exactly the
+// reference's post-phase-E state.
+#pragma once
+
+#include <cstdint>
+
+#include "vxb_device.cuh"
+
+namespace vxb {
+
+// Per-segment parameters: a segment is a run of shard-local neurons with
+// identical NeuronRecord parameters, unit, voxel, worker and consecutive gids.
+// Reference populations give one segment per unit.
+struct SegParams {
+    int64_t gid_off;      // gid = local + gid_off
+    uint32_t start;       // first shard-local index
+    uint32_t unit;
+    uint32_t voxel;
+    uint32_t worker;
+    uint32_t tref;        // refractory_steps
+    float dt_over_c;      // dtf / C (engine.cpp:242)
+    float g_leak, e_leak, v_th, v_reset;
+    float decay[4];       // 1 - dtf / tau_u   (gating_kernel, model.hpp:69-71)
+    float omega[4];
+    float e_rev[4];
+    float ou_mu;
+    float ou_a;           // dtf / tau_ou
+    float ou_b;           // sigma * sqrtf(2 dtf / tau_ou)  (ou_kernel, model.hpp:88-90)
+    uint32_t sigma_pos;   // sigma > 0
+    uint32_t pad[4];
+};
+static_assert(sizeof(SegParams) == 128, "SegParams layout");
+
+// Refractory neurons hold V = V_reset (engine.cpp:364-367); the counter is
+// kept in the V word as a negative NaN payload so the state is one word.
+__host__ __device__ __forceinline__ bool is_refrac(uint32_t bits) {
+    return (bits & 0xff800000u) == 0xff800000u && (bits & 0x007fffffu) != 0u;
+}
+__host__ __device__ __forceinline__ uint32_t refrac_bits(uint32_t r) { return 0xff800000u | r; }
+
+struct Control {
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    unsigned int work;         // dynamic delivery work counter of the phase
+    unsigned int spk_cursor;   // append cursor of the spike log
+    unsigned long long err;    // min (step << 32 | local) of a divergence, ~0 = none
+    unsigned long long flops_inner, flops_outer;
+    unsigned int pad[6];
+};
+
+struct StepArgs {
+    // sizes
+    uint32_t n;             // shard neurons
+    uint32_t nseg;
+    uint32_t n_units;
+    uint32_t steps;         // A steps in this chunk (phases = steps + 1)
+    uint32_t t0;            // absolute step of the chunk's first A
+    uint32_t rel0;          // index of t0 within the current advance()
+    uint32_t adv_steps;     // steps of the whole advance() (trace stride)
+    uint32_t spk_cap;       // spike log capacity
+    uint32_t ring;          // spike log in ring mode (raster not recorded)
+    uint32_t use_smem_seg;
+    float dtf;
+    uint64_t ou_root;       // mix_key(seed, rngstream::ou_noise)
+    // parameters
+    const SegParams* seg;
+    const uint32_t* seg_start;
+    // state
+    uint32_t* v;            // float bits or refractory code
+    float4* j;
+    float* i_ou;
+    float* i_syn;
+    const float4* g;
+    void* pend0;            // pending buffers, parity of the step they hold
+    void* pend1;
+    // out-CSR
+    const uint64_t* off;    // n + 1
+    const uint32_t* inner;  // per source: entries whose target is on its worker
+    const uint32_t* tgt;    // target | cls << 31
+    const uint64_t* w;      // (u32)wq_fast | (u64)(u32)wq_slow << 32
+    // spike log
+    uint32_t* spk;
+    uint32_t* seg_end;      // per phase: log end after that phase's A
+    // readout
+    uint32_t* rates;        // [unit][chunk step]
+    uint32_t n_probes;
+    const uint32_t* probe_local;  // sorted
+    const uint32_t* probe_slot;
+    float* probe_v;         // [slot][adv_steps]
+    float* probe_i;
+    const uint32_t* forced_off;   // [steps + 1]
+    const uint32_t* forced_local; // sorted per step
+    uint32_t has_forced;
+    const uint32_t* inj_epoch;    // [steps], 0 = no injection active
+    const float* inj_table;       // [(epoch-1) * n_voxels + voxel]
+    uint32_t n_voxels;
+    uint32_t has_inj;
+    unsigned long long* phase_ns; // [steps + 2] globaltimer at phase ends
+    Control* ctl;
+};
+
+__device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {
+    return (uint64_t)__ldg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Sense-counting grid barrier for a cooperative launch.  The last CTA to
+// arrive runs `hook` (bookkeeping for the next phase) before releasing.
+template <typename Hook>
+__device__ __forceinline__ void grid_barrier(Control* ctl, Hook hook) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = ld_acquire(&ctl->bar_gen);
+        __threadfence();
+        const unsigned int arrived = atomicAdd(&ctl->bar_count, 1u);
+        if (arrived == gridDim.x - 1) {
+            ctl->bar_count = 0;
+            hook();
+            __threadfence();
+            st_release(&ctl->bar_gen, gen + 1);
+        } else {
+            while (ld_acquire(&ctl->bar_gen) == gen) __nanosleep(40);
+        }
+    }
+    __syncthreads();
+}
+
+// Index of the segment holding shard-local neuron i (largest start <= i).
+__device__ __forceinline__ uint32_t find_seg(const uint32_t* starts, uint32_t nseg, uint32_t i) {
+    uint32_t lo = 0, hi = nseg;  // invariant: starts[lo] <= i < starts[hi]
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (starts[mid] <= i)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// First index in sorted a[0..n) with a[k] >= x.
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+template <bool PACKED>
+struct Pend;
+template <>
+struct Pend<true> {  // (AMPA|NMDA<<32, GABAA|GABAB<<32), carry-free by construction
+    using T = ulonglong2;
+};
+template <>
+struct Pend<false> {  // four signed int64 buckets, the reference's layout
+    struct T {
+        longlong2 lo, hi;
+    };
+};
+
+constexpr int kMaxSmemSeg = 256;
+constexpr int kThreads = 512;
+
+template <bool PACKED>
+__global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
+    using PT = typename Pend<PACKED>::T;
+    __shared__ SegParams s_seg[kMaxSmemSeg];
+    __shared__ uint32_t s_start[kMaxSmemSeg + 1];
+
+    const SegParams* segp = a.seg;
+    const uint32_t* startp = a.seg_start;
+    if (a.use_smem_seg) {
+        for (uint32_t k = threadIdx.x; k < a.nseg; k += blockDim.x) {
+            s_seg[k] = a.seg[k];
+            s_start[k] = a.seg_start[k];
+        }
+        if (threadIdx.x == 0) s_start[a.nseg] = a.n;
+        __syncthreads();
+        segp = s_seg;
+        startp = s_start;
+    }
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t gthreads = gridDim.x * blockDim.x;
+    const uint32_t gwarps = gthreads >> 5;
+    (void)gwarps;
+    Control* ctl = a.ctl;
+    unsigned long long my_inner = 0, my_outer = 0;
+
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
+    const uint32_t nph = a.steps + 1;
+    for (uint32_t ph = 0; ph < nph; ++ph) {
+        const bool doA = ph < a.steps;
+        const bool doE = ph >= 1;
+        const uint32_t tA = a.t0 + ph;
+        const uint32_t tE = tA - 1;
+        // pending buffer consumed by E(tE) holds S(tE-1): parity (tE-1)&1 == tA&1
+        PT* pend_rd = reinterpret_cast<PT*>((tA & 1u) ? a.pend1 : a.pend0);
+        // deliveries of S(tE) go to parity tE&1
+        PT* pend_wr = reinterpret_cast<PT*>((tE & 1u) ? a.pend1 : a.pend0);
+        const uint32_t inj_ep = (doA && a.has_inj) ? a.inj_epoch[ph] : 0u;
+        uint32_t f_lo = 0, f_hi = 0;
+        if (doA && a.has_forced) {
+            f_lo = a.forced_off[ph];
+            f_hi = a.forced_off[ph + 1];
+        }
+        uint32_t log_base;  // where this phase's spikes go
+        if (a.ring)
+            log_base = (ph & 1u) * a.n;
+        else
+            log_base = 0;
+
+        // ------------------------------------------------------------ F
+        const uint32_t n_round = (a.n + 31u) & ~31u;
+        for (uint32_t i0 = gtid; i0 < n_round; i0 += gthreads) {
+            const uint32_t i = i0;
+            const bool live = i < a.n;
+            bool spiked = false;
+            if (live) {
+                const SegParams& P = segp[find_seg(startp, a.nseg, i)];
+                uint32_t vb = a.v[i];
+                float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                float4 j = a.j[i];
+                float iou = a.i_ou[i];
+                float isyn;
+                if (doE) {
+                    // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
+                    float p0, p1, p2, p3;
+                    if constexpr (PACKED) {
+                        const ulonglong2 pv = __ldcg(pend_rd + i);
+                        p0 = dequantize((int64_t)(uint32_t)(pv.x & 0xffffffffull));
+                        p1 = dequantize((int64_t)(uint32_t)(pv.x >> 32));
+                        p2 = dequantize((int64_t)(uint32_t)(pv.y & 0xffffffffull));
+                        p3 = dequantize((int64_t)(uint32_t)(pv.y >> 32));
+                        __stcg(pend_rd + i, make_ulonglong2(0ull, 0ull));
+                    } else {
+                        longlong2* q = reinterpret_cast<longlong2*>(pend_rd + i);
+                        const longlong2 lo = __ldcg(q), hi = __ldcg(q + 1);
+                        p0 = dequantize(lo.x);
+                        p1 = dequantize(lo.y);
+                        p2 = dequantize(hi.x);
+                        p3 = dequantize(hi.y);
+                        __stcg(q, make_longlong2(0, 0));
+                        __stcg(q + 1, make_longlong2(0, 0));
+                    }
+                    j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
+                    j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
+                    j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
+                    j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
+                    // current_kernel (model.hpp:73-81), u order, from 0.0f
+                    const float4 g = a.g[i];
+                    float c = 0.0f;
+                    c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
+                    c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
+                    c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
+                    c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
+                    isyn = c;
+                    // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
+                    float xi = 0.0f;
+                    if (P.sigma_pos) {
+                        const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
+                        xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
+                    }
+                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                    if (!doA) a.i_syn[i] = isyn;
+                } else {
+                    isyn = a.i_syn[i];
+                }
+                if (doA) {
+                    // membrane_kernel + threshold (engine.cpp:363-385)
+                    if (is_refrac(vb)) {
+                        const uint32_t r = (vb & 0x007fffffu) - 1u;
+                        vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
+                    } else {
+                        float inoise = iou;
+                        if (inj_ep) {
+                            const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
+                            if (x != 0.0f) inoise = fadd(iou, x);
+                        }
+                        const float nv = fadd(v, fmul(P.dt_over_c,
+                                                      fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                        if (!isfinite(nv)) {
+                            atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
+                            vb = __float_as_uint(nv);
+                        } else if (nv >= P.v_th) {
+                            spiked = true;
+                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                        } else {
+                            vb = __float_as_uint(nv);
+                        }
+                    }
+                }
+                if (doE) {
+                    a.j[i] = j;
+                    a.i_ou[i] = iou;
+                }
+                if (doA) a.v[i] = vb;
+                // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
+                if (a.n_probes) {
+                    uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                    while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                        const uint32_t slot = __ldg(a.probe_slot + k);
+                        if (doE) a.probe_i[(size_t)slot * a.adv_steps + a.rel0 + ph - 1] = isyn;
+                        ++k;
+                    }
+                }
+            }
+            // forced spikes (engine.cpp:389-398): join unless already fired
+            if (doA && f_hi > f_lo && live) {
+                const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                if (k < f_hi && __ldg(a.forced_local + k) == i && !spiked) {
+                    const SegParams& P = segp[find_seg(startp, a.nseg, i)];
+                    spiked = true;
+                    a.v[i] = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                }
+            }
+            if (doA && live && a.n_probes) {
+                uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                    const uint32_t slot = __ldg(a.probe_slot + k);
+                    const uint32_t vb = a.v[i];
+                    const SegParams& P = segp[find_seg(startp, a.nseg, i)];
+                    a.probe_v[(size_t)slot * a.adv_steps + a.rel0 + ph] =
+                        is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                    ++k;
+                }
+            }
+            // spike log append + rates (engine.cpp:400-404), warp aggregated
+            const unsigned ball = __ballot_sync(0xffffffffu, spiked);
+            if (ball) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(&ctl->spk_cursor, (unsigned)__popc(ball));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (spiked) {
+                    const unsigned rank = __popc(ball & ((1u << lane) - 1u));
+                    a.spk[log_base + base + rank] = i;
+                    const uint32_t unit = segp[find_seg(startp, a.nseg, i)].unit;
+                    const unsigned peers = __match_any_sync(ball, unit);
+                    if ((unsigned)__ffs(peers) - 1u == lane)
+                        atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
+                }
+            }
+        }
+
+        // ------------------------------------------------------------ D
+        if (doE) {
+            const uint32_t lo = (ph >= 2 && !a.ring) ? __ldcg(a.seg_end + ph - 2) : 0u;
+            const uint32_t hi = __ldcg(a.seg_end + ph - 1);
+            const uint32_t prev_base = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
+            const uint32_t cnt = hi - lo;
+            for (;;) {
+                unsigned k = 0;
+                if (lane == 0) k = atomicAdd(&ctl->work, 1u);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k >= cnt) break;
+                const uint32_t s = __ldcg(a.spk + prev_base + lo + k);
+                const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
+                for (uint64_t e = e0 + lane; e < e1; e += 32) {
+                    const uint32_t t = __ldg(a.tgt + e);
+                    const uint64_t wq = ldg64(a.w + e);
+                    const uint32_t tid = t & 0x7fffffffu;
+                    const uint32_t cls = t >> 31;
+                    if constexpr (PACKED) {
+                        unsigned long long* dst =
+                            reinterpret_cast<unsigned long long*>(pend_wr + tid) + cls;
+                        atomicAdd(dst, (unsigned long long)wq);
+                    } else {
+                        unsigned long long* dst =
+                            reinterpret_cast<unsigned long long*>(pend_wr + tid) + 2 * cls;
+                        atomicAdd(dst, (unsigned long long)(long long)(int32_t)(uint32_t)wq);
+                        atomicAdd(dst + 1, (unsigned long long)(long long)(int32_t)(uint32_t)(wq >> 32));
+                    }
+                }
+                if (lane == 0) {
+                    const uint32_t in = __ldg(a.inner + s);
+                    my_inner += 2ull * in;
+                    my_outer += 2ull * ((e1 - e0) - in);
+                }
+            }
+        }
+
+        grid_barrier(ctl, [&] {
+            if (doA) a.seg_end[ph] = ctl->spk_cursor;
+            if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
+            ctl->work = 0;
+            a.phase_ns[ph + 1] = globaltimer();
+        });
+        if (*((volatile unsigned long long*)&ctl->err) != ~0ull) break;
+    }
+    if (lane == 0 && (my_inner | my_outer)) {
+        atomicAdd(&ctl->flops_inner, my_inner);
+        atomicAdd(&ctl->flops_outer, my_outer);
+    }
+}
+
+// ------------------------------------------------------- out-CSR build
+// Inverts the in-rows of the worker tables (engine.cpp:295-327) on the
+// device: count per source, scan, scatter.
+
+struct SynIn {  // == vxb_syn_entry
+    uint32_t src_local;
+    uint16_t src_worker;
+    uint8_t cls;
+    uint8_t pad;
+    int32_t wq_fast;
+    int32_t wq_slow;
+};
+
+__global__ void csr_count_kernel(const SynIn* __restrict__ e, uint64_t ne,
+                                 const uint32_t* __restrict__ wbase,
+                                 const uint32_t* __restrict__ wn, uint32_t nw,
+                                 unsigned long long* __restrict__ cnt,
+                                 unsigned int* __restrict__ bad) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < ne;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const SynIn x = e[k];
+        if (x.src_worker >= nw || x.src_local >= wn[x.src_worker]) {
+            atomicExch(bad, 1u);
+            continue;
+        }
+        atomicAdd(cnt + wbase[x.src_worker] + x.src_local, 1ull);
+    }
+}
+
+// One warp per target row.
+__global__ void csr_scatter_kernel(const SynIn* __restrict__ e,
+                                   const uint64_t* __restrict__ row_base, uint32_t rows,
+                                   uint32_t dst_worker, uint32_t dst_base,
+                                   const uint32_t* __restrict__ wbase,
+                                   unsigned long long* __restrict__ cursor,
+                                   uint32_t* __restrict__ tgt, uint64_t* __restrict__ w,
+                                   unsigned long long* __restrict__ have_mask,
+                                   uint32_t* __restrict__ inner,
+                                   unsigned int* __restrict__ wide) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t base0 = row_base[0];
+    for (uint64_t r = warp; r < rows; r += nwarps) {
+        const uint64_t b = row_base[r] - base0, en = row_base[r + 1] - base0;
+        long long sf = 0, ss = 0;
+        bool neg = false;
+        for (uint64_t k = b + lane; k < en; k += 32) {
+            const SynIn x = e[k];
+            const uint32_t src = wbase[x.src_worker] + x.src_local;
+            const unsigned long long pos = atomicAdd(cursor + src, 1ull);
+            tgt[pos] = (dst_base + (uint32_t)r) | (x.cls ? 0x80000000u : 0u);
+            w[pos] = (uint64_t)(uint32_t)x.wq_fast | ((uint64_t)(uint32_t)x.wq_slow << 32);
+            atomicOr(have_mask + src, 1ull << dst_worker);
+            if (x.src_worker == dst_worker) atomicAdd(inner + src, 1u);
+            sf += x.wq_fast;
+            ss += x.wq_slow;
+            neg |= (x.wq_fast < 0) || (x.wq_slow < 0);
+        }
+        for (int o = 16; o; o >>= 1) {
+            sf += __shfl_xor_sync(0xffffffffu, sf, o);
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        }
+        neg = __any_sync(0xffffffffu, neg);
+        if (lane == 0 && (neg || sf >= (1ll << 32) || ss >= (1ll << 32))) atomicExch(wide, 1u);
+    }
+}
+
+__global__ void mask_check_kernel(const unsigned long long* __restrict__ have,
+                                  const unsigned long long* __restrict__ mask, uint32_t n,
+                                  unsigned long long* __restrict__ first_bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (have[i] != mask[i]) atomicMin(first_bad, (unsigned long long)i);
+}
+
+// Pack (step << 32 | local) keys of the spike log for the raster sort.
+__global__ void raster_keys_kernel(const uint32_t* __restrict__ spk,
+                                   const uint32_t* __restrict__ seg_end, uint32_t steps,
+                                   uint64_t* __restrict__ keys) {
+    for (uint32_t s = blockIdx.x; s < steps; s += gridDim.x) {
+        const uint32_t lo = s ? seg_end[s - 1] : 0u, hi = seg_end[s];
+        for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
+            keys[k] = ((uint64_t)s << 32) | spk[k];
+    }
+}
+
+__global__ void debug_normal_kernel(const uint64_t* __restrict__ base,
+                                    const uint64_t* __restrict__ k, uint64_t n,
+                                    double* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = stream_normal(base[i], k[i]);
+}
+
+}  // namespace vxb

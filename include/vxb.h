@@ -235,6 +235,73 @@ uint16_t vxb_workers(const vxb_engine* e);
 uint32_t vxb_units(const vxb_engine* e);
 uint32_t vxb_probes(const vxb_engine* e);
 
+/* ---- on-device network generation ----------------------------------------
+ * Replaces sample_synapses + emit_tables (netgen.hpp:84-92, netgen.cpp:51-316)
+ * for networks too large to build on the host: the per-neuron records are
+ * drawn on the host (O(neurons)), the K in-picks of every neuron are drawn on
+ * the device and written straight into the engine's delivery tables.  Draws
+ * are keyed by (seed, gid, slot) exactly as the reference, so the tables are
+ * those emit_tables would produce for the same layout/connectome/partition.
+ */
+
+/* PopulationSpec (layout.hpp:17-38) + NeuronParams/OuParams of one unit. */
+typedef struct vxb_gen_population {
+    double g_location[VXB_RECEPTORS];
+    double g_scale[VXB_RECEPTORS];
+    double weight_mean[VXB_RECEPTORS];
+    double weight_spread[VXB_RECEPTORS];
+    double split_ratio;
+    float capacitance, g_leak, e_leak, v_threshold, v_reset;
+    uint32_t refractory_steps;
+    float e_rev[VXB_RECEPTORS];
+    float tau[VXB_RECEPTORS];
+    float omega[VXB_RECEPTORS];
+    float ou_mean, ou_sigma, ou_tau;
+    uint8_t excitatory;
+    uint8_t dual_receptor;
+    uint8_t pad0[2];
+} vxb_gen_population;
+
+/* VoxelSpec (layout.hpp:40-49) after NetworkLayout::build. */
+typedef struct vxb_gen_voxel {
+    uint32_t k_in;
+    uint32_t region;     /* Region enum (layout.hpp:12) */
+    double rho;
+    uint32_t unit_begin; /* NetworkLayout::voxel_unit_base[v] */
+    uint32_t unit_end;
+} vxb_gen_voxel;
+
+/* ConnectomeEdge (connectome.hpp:14-18). */
+typedef struct vxb_gen_edge {
+    uint32_t src;
+    uint32_t dst;
+    double weight;
+} vxb_gen_edge;
+
+typedef struct vxb_netspec {
+    uint64_t seed;
+    uint32_t n_voxels;
+    uint32_t n_units;
+    uint32_t n_edges;
+    uint32_t n_workers;
+    const vxb_gen_voxel* voxels;
+    const vxb_unit* units;                /* NetworkLayout::units */
+    const vxb_gen_population* unit_pops;  /* population spec of each unit */
+    const vxb_gen_edge* edges;            /* sorted by (dst, src) */
+    const double* intra[4];               /* IntraMatrices per region, [tgt][src] */
+    uint32_t intra_pops[4];
+    const uint16_t* unit_worker;          /* PartitionMap::unit_worker */
+} vxb_netspec;
+
+int vxb_create_generated(const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out);
+
+/* Export worker `worker`'s WorkerTable as emit_tables would build it (for
+ * parity checks on small networks).  Sizes: n_neurons = sum of the worker's
+ * unit sizes, n_synapses = sum of neurons * k_in of their voxels. */
+int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t worker,
+                              vxb_neuron* neurons, uint32_t n_cap, vxb_syn_entry* synapses,
+                              uint64_t syn_cap, uint64_t* row_base);
+
 /* ---- diagnostics --------------------------------------------------------- */
 /* Device evaluation of stream_normal(base[i], k[i]) (rng.hpp:63-67) exactly as
  * the step kernel computes it, for noise-parity checks against the host. */

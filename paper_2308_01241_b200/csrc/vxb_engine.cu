@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -30,6 +31,7 @@
 
 #include "vxb.h"
 #include "vxb_kernels.cuh"
+#include "vxb_netgen.cuh"
 
 namespace {
 
@@ -154,8 +156,10 @@ struct Engine {
         if (stream) cudaStreamDestroy(stream);
     }
 
-    void load(const vxb_network* net, const vxb_options* opt);
+    void load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen = nullptr);
     void build_csr(const vxb_network* net);
+    void generate_csr(const vxb_netspec& spec);
+    std::vector<unsigned long long> gen_have_mask;  // dst masks of generated tables
     void advance(uint32_t steps);
     void run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps);
     uint32_t seg_of(uint32_t local) const {
@@ -254,7 +258,7 @@ bool same_params(const SegParams& s, const vxb_neuron& r, uint32_t local, uint32
     return std::memcmp(&s, &t, sizeof s) == 0;
 }
 
-void Engine::load(const vxb_network* net, const vxb_options* opt) {
+void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen) {
     if (!net || !opt) throw ConfigError("null network or options");
     if (net->n_workers == 0) throw ConfigError("no worker tables");
     if (net->n_workers > 64) throw ConfigError("worker counts above 64 are unsupported");
@@ -358,13 +362,15 @@ void Engine::load(const vxb_network* net, const vxb_options* opt) {
     d_isyn.zero(stream);
 
     // out-CSR + mask consistency
-    build_csr(net);
-    {
+    if (gen) {
+        generate_csr(*gen);  // consistent by construction
+    } else {
+        build_csr(net);
         DevBuf<unsigned long long> d_mask, d_bad;
         d_mask.alloc(n);
         d_bad.alloc(1);
         CK(cudaMemcpyAsync(d_mask.p, h_mask.data(), 8ull * n, cudaMemcpyHostToDevice, stream));
-        unsigned long long init = ~0ull;
+        const unsigned long long init = ~0ull;
         CK(cudaMemcpyAsync(d_bad.p, &init, 8, cudaMemcpyHostToDevice, stream));
         // have_mask was left in d_keys by build_csr
         if (n)
@@ -387,8 +393,8 @@ void Engine::load(const vxb_network* net, const vxb_options* opt) {
                                "-> worker %d)",
                                s, (unsigned)(bad - wbase[s]), d));
         }
-        d_keys.release();
     }
+    d_keys.release();
 
     const size_t pend_bytes = (packed ? 16ull : 32ull) * n;
     d_pend0.alloc(pend_bytes);
@@ -520,6 +526,306 @@ void Engine::build_csr(const vxb_network* net) {
     unsigned int wide = 0;
     CK(cudaMemcpyAsync(&wide, flags.p + 1, 4, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    packed = wide == 0;
+}
+
+// ------------------------------------------------------------ generation
+// Host half of on-device generation: the per-neuron records of emit_tables
+// (netgen.cpp:242-298) with the reference's own libm calls, and the sampling
+// tables the device draws from (netgen.cpp:60-100).
+
+double h_stream_u01(uint64_t base, uint64_t k) {
+    return (double)(stream_word(base, k) >> 11) * 0x1.0p-53;
+}
+double h_stream_normal(uint64_t base, uint64_t k) {  // rng.hpp:63-67, glibc
+    const double u1 = 1.0 - h_stream_u01(base, 2 * k);
+    const double u2 = h_stream_u01(base, 2 * k + 1);
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+}
+
+struct GenHost {
+    std::vector<uint32_t> unit_local_base;
+    std::vector<std::vector<vxb_neuron>> recs;  // per worker
+    std::vector<uint64_t> nsyn;                 // per worker
+    std::vector<vxb_worker_table> tables;
+    std::vector<GenUnit> gunits;
+    std::vector<GenVoxel> gvox;
+    std::vector<double> e_cdf, pc;
+    std::vector<uint32_t> e_src;
+    std::vector<uint64_t> e_nexc;
+    vxb_network net{};
+    uint64_t total_neurons = 0;
+};
+
+void build_gen_host(const vxb_netspec& s, GenHost& h) {
+    if (s.n_workers == 0) throw ConfigError("partition with zero workers");
+    if (s.n_workers > 64)
+        throw ConfigError("worker count exceeds the routing mask limit of 64");
+    if (s.n_voxels == 0) throw ConfigError("layout with zero voxels");
+    const uint32_t U = s.n_units;
+    std::vector<uint32_t> fill(s.n_workers, 0), nunits(s.n_workers, 0);
+    h.unit_local_base.assign(U, 0);
+    for (uint32_t u = 0; u < U; ++u) {
+        const uint16_t w = s.unit_worker[u];
+        if (w >= s.n_workers) throw ConfigError("partition worker id out of range");
+        h.unit_local_base[u] = fill[w];
+        fill[w] += s.units[u].neurons;
+        nunits[w] += 1;
+    }
+    for (uint32_t w = 0; w < s.n_workers; ++w)
+        if (nunits[w] == 0)
+            throw ConfigError("worker " + std::to_string(w) + " has no units assigned");
+    for (uint32_t u = 0; u < U; ++u) h.total_neurons += s.units[u].neurons;
+    if (h.total_neurons > 0xffffffffull)
+        throw ConfigError("global neuron ids exceed 32-bit source addressing");
+    for (uint32_t e = 0; e < s.n_edges; ++e) {
+        const vxb_gen_edge& x = s.edges[e];
+        if (x.src >= s.n_voxels || x.dst >= s.n_voxels)
+            throw ConfigError("edge endpoint out of range");
+        if (e && (x.dst < s.edges[e - 1].dst ||
+                  (x.dst == s.edges[e - 1].dst && x.src <= s.edges[e - 1].src)))
+            throw ConfigError("edges must be sorted by (dst, src), unique");
+    }
+
+    // sampling tables
+    std::vector<uint64_t> exc_count(s.n_voxels, 0);  // layout.cpp:130-135
+    for (uint32_t v = 0; v < s.n_voxels; ++v)
+        for (uint32_t u = s.voxels[v].unit_begin; u < s.voxels[v].unit_end; ++u)
+            if (s.units[u].excitatory) exc_count[v] += s.units[u].neurons;
+    h.gunits.resize(U);
+    for (uint32_t u = 0; u < U; ++u) {
+        const vxb_unit& x = s.units[u];
+        const vxb_gen_population& p = s.unit_pops[u];
+        GenUnit& g = h.gunits[u];
+        std::memset(&g, 0, sizeof g);
+        g.gid_base = x.gid_base;
+        g.neurons = x.neurons;
+        g.voxel = x.voxel;
+        g.worker = s.unit_worker[u];
+        g.local_base = h.unit_local_base[u];
+        g.exc = x.excitatory ? 1u : 0u;
+        g.dual = p.dual_receptor ? 1u : 0u;
+        g.split_ratio = p.split_ratio;
+        for (int r = 0; r < 4; ++r) {
+            g.w_mean[r] = p.weight_mean[r];
+            g.w_spread[r] = p.weight_spread[r];
+        }
+    }
+    h.gvox.resize(s.n_voxels);
+    uint32_t e = 0;
+    for (uint32_t v = 0; v < s.n_voxels; ++v) {
+        const vxb_gen_voxel& x = s.voxels[v];
+        GenVoxel& g = h.gvox[v];
+        std::memset(&g, 0, sizeof g);
+        g.k_in = x.k_in;
+        g.m = (uint32_t)std::ceil(x.rho * x.k_in - 1e-9);
+        g.unit_begin = x.unit_begin;
+        g.unit_end = x.unit_end;
+        g.e0 = (uint32_t)h.e_cdf.size();
+        double acc = 0.0;
+        for (; e < s.n_edges && s.edges[e].dst == v; ++e) {
+            const double wgt = s.edges[e].weight;
+            if (!(wgt >= 0.0)) throw ConfigError("negative categorical weight");
+            acc += wgt;
+            h.e_cdf.push_back(acc);
+            h.e_src.push_back(s.edges[e].src);
+            h.e_nexc.push_back(exc_count[s.edges[e].src]);
+            if (g.m > 0 && wgt > 0 && exc_count[s.edges[e].src] == 0)
+                throw ConfigError("voxel " + std::to_string(s.edges[e].src) +
+                                  " has no excitatory neurons but is an in-edge source");
+        }
+        g.e1 = (uint32_t)h.e_cdf.size();
+        g.in_total = acc;
+        if (g.m > 0 && !(acc > 0.0))
+            throw ConfigError("voxel " + std::to_string(v) +
+                              ": rho > 0 but no weighted inter-voxel in-edges");
+        const uint32_t pops = x.unit_end - x.unit_begin;
+        const uint32_t reg = x.region;
+        if (reg >= 4 || s.intra_pops[reg] != pops)
+            throw ConfigError("population matrix size does not match region layout");
+        g.pc_off = (uint32_t)h.pc.size();
+        std::vector<double> totals(pops);
+        for (uint32_t tp = 0; tp < pops; ++tp) {
+            double a = 0.0;
+            for (uint32_t sp = 0; sp < pops; ++sp) {
+                const double wgt = s.intra[reg][tp * pops + sp] *
+                                   (double)s.units[x.unit_begin + sp].neurons;
+                if (!(wgt >= 0.0)) throw ConfigError("negative categorical weight");
+                a += wgt;
+                h.pc.push_back(a);
+            }
+            totals[tp] = a;
+            if (g.m < g.k_in && !(a > 0.0))
+                throw ConfigError("voxel " + std::to_string(v) + " population " +
+                                  std::to_string(tp) +
+                                  ": intra picks required but matrix row is empty");
+        }
+        g.pt_off = (uint32_t)h.pc.size();
+        h.pc.insert(h.pc.end(), totals.begin(), totals.end());
+    }
+
+    // per-neuron records (emit_tables, netgen.cpp:251-298)
+    h.recs.assign(s.n_workers, {});
+    h.nsyn.assign(s.n_workers, 0);
+    for (uint32_t w = 0; w < s.n_workers; ++w) h.recs[w].reserve(fill[w]);
+    const uint64_t init_key = mix_key(mix_key(s.seed, 2), 0);  // rngstream::init_state
+    for (uint32_t u = 0; u < U; ++u) {
+        const vxb_unit& x = s.units[u];
+        const vxb_gen_population& p = s.unit_pops[u];
+        const uint16_t w = s.unit_worker[u];
+        const uint32_t k_in = s.voxels[x.voxel].k_in;
+        std::array<uint64_t, 4> gbase;
+        for (int r = 0; r < 4; ++r)  // sample_conductances (netgen.cpp:318-329), salt 0
+            gbase[r] = mix_key(mix_key(mix_key(mix_key(s.seed, 7), 0), u), (uint64_t)r);
+        for (uint32_t j = 0; j < x.neurons; ++j) {
+            vxb_neuron r;
+            std::memset(&r, 0, sizeof r);
+            r.gid = x.gid_base + j;
+            r.voxel = x.voxel;
+            r.unit = u;
+            r.pop = x.pop;
+            r.excitatory = x.excitatory;
+            r.row_len = k_in;
+            r.capacitance = p.capacitance;
+            r.g_leak = p.g_leak;
+            r.e_leak = p.e_leak;
+            r.v_threshold = p.v_threshold;
+            r.v_reset = p.v_reset;
+            r.refractory_steps = p.refractory_steps;
+            for (int q = 0; q < 4; ++q) {
+                r.e_rev[q] = p.e_rev[q];
+                r.tau[q] = p.tau[q];
+                r.omega[q] = p.omega[q];
+                r.g[q] = (float)std::exp(p.g_location[q] +
+                                         p.g_scale[q] * h_stream_normal(gbase[q], j));
+            }
+            r.ou_mean = p.ou_mean;
+            r.ou_sigma = p.ou_sigma;
+            r.ou_tau = p.ou_tau;
+            const double u01 = h_stream_u01(init_key, r.gid);
+            const float span = p.v_threshold - p.v_reset;  // float subtraction, as the reference
+            r.v_init = (float)((double)p.v_reset + u01 * (double)span);
+            h.recs[w].push_back(r);
+        }
+        h.nsyn[w] += (uint64_t)x.neurons * k_in;
+    }
+    h.tables.resize(s.n_workers);
+    for (uint32_t w = 0; w < s.n_workers; ++w) {
+        vxb_worker_table& t = h.tables[w];
+        std::memset(&t, 0, sizeof t);
+        t.worker = (uint16_t)w;
+        t.worker_count = (uint16_t)s.n_workers;
+        t.n_neurons = (uint32_t)h.recs[w].size();
+        t.seed = s.seed;
+        t.n_synapses = h.nsyn[w];
+        t.neurons = h.recs[w].data();
+    }
+    h.net.n_workers = s.n_workers;
+    h.net.n_units = U;
+    h.net.n_voxels = s.n_voxels;
+    h.net.workers = h.tables.data();
+    h.net.unit_worker = s.unit_worker;
+    h.net.unit_local_base = h.unit_local_base.data();
+    h.net.units = s.units;
+}
+
+struct GenDevTables {
+    DevBuf<GenUnit> units;
+    DevBuf<GenVoxel> vox;
+    DevBuf<double> e_cdf, pc;
+    DevBuf<uint32_t> e_src, wbase;
+    DevBuf<uint64_t> e_nexc;
+    DevBuf<unsigned int> flags;  // [0] err, [1] wide
+    GenDev G{};
+
+    void upload(const GenHost& h, const vxb_netspec& s, const std::vector<uint32_t>& wb,
+                cudaStream_t st) {
+        auto up = [&](auto& buf, const auto& vec) {
+            buf.alloc(std::max<size_t>(1, vec.size()));
+            if (!vec.empty())
+                CK(cudaMemcpyAsync(buf.p, vec.data(), vec.size() * sizeof(vec[0]),
+                                   cudaMemcpyHostToDevice, st));
+        };
+        up(units, h.gunits);
+        up(vox, h.gvox);
+        up(e_cdf, h.e_cdf);
+        up(pc, h.pc);
+        up(e_src, h.e_src);
+        up(e_nexc, h.e_nexc);
+        up(wbase, wb);
+        flags.alloc(2);
+        flags.zero(st);
+        G.kv_root = mix_key(s.seed, 3);  // rngstream::pick_voxel
+        G.kn_root = mix_key(s.seed, 4);  // rngstream::pick_neuron
+        G.kp_root = mix_key(s.seed, 5);  // rngstream::pick_pop
+        G.kw_root = mix_key(s.seed, 6);  // rngstream::weight
+        G.n_units = s.n_units;
+        G.units = units.p;
+        G.voxels = vox.p;
+        G.e_cdf = e_cdf.p;
+        G.e_src = e_src.p;
+        G.e_nexc = e_nexc.p;
+        G.pc = pc.p;
+        G.wbase = wbase.p;
+        G.err = flags.p;
+        G.wide = flags.p + 1;
+    }
+    void check(cudaStream_t st, unsigned int* wide_out) {
+        unsigned int f[2] = {0, 0};
+        CK(cudaMemcpyAsync(f, flags.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (f[0])
+            throw ConfigError("cannot draw a non-self intra-voxel source (population too small)");
+        if (wide_out) *wide_out = f[1];
+    }
+};
+
+thread_local GenHost* g_gen_host = nullptr;
+
+void Engine::generate_csr(const vxb_netspec& spec) {
+    GenHost& h = *g_gen_host;
+    GenDevTables T;
+    std::vector<uint32_t> wb(wbase.begin(), wbase.end() - 1);
+    T.upload(h, spec, wb, stream);
+    n_syn = 0;
+    for (uint64_t x : h.nsyn) n_syn += x;
+    DevBuf<unsigned long long> cnt;
+    cnt.alloc((size_t)n + 1);
+    cnt.zero(stream);
+    const int blocks = 148 * 8, threads = 256;
+    if (h.total_neurons)
+        gen_kernel<0><<<blocks, threads, 0, stream>>>(T.G, 0, h.total_neurons, cnt.p + 1,
+                                                      nullptr, nullptr, nullptr, nullptr, 0,
+                                                      nullptr, nullptr);
+    CK(cudaGetLastError());
+    T.check(stream, nullptr);
+    d_off.alloc((size_t)n + 1);
+    {
+        size_t tmp = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.p + 1,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         stream));
+        DevBuf<unsigned char> t;
+        t.alloc(tmp ? tmp : 1);
+        CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cnt.p + 1,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         stream));
+        CK(cudaMemsetAsync(d_off.p, 0, 8, stream));
+    }
+    CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n, cudaMemcpyDeviceToDevice, stream));
+    d_tgt.alloc(n_syn);
+    d_w.alloc(n_syn);
+    d_inner.alloc(n);
+    d_inner.zero(stream);
+    d_keys.alloc(n);  // have_mask
+    d_keys.zero(stream);
+    if (h.total_neurons)
+        gen_kernel<1><<<blocks, threads, 0, stream>>>(
+            T.G, 0, h.total_neurons, cnt.p, d_tgt.p, d_w.p,
+            reinterpret_cast<unsigned long long*>(d_keys.p), d_inner.p, 0, nullptr, nullptr);
+    CK(cudaGetLastError());
+    unsigned int wide = 0;
+    T.check(stream, &wide);
     packed = wide == 0;
 }
 
@@ -955,6 +1261,80 @@ uint32_t vxb_worker_neurons(const vxb_engine* e, uint16_t worker) {
 uint16_t vxb_workers(const vxb_engine* e) { return e->eng.workers; }
 uint32_t vxb_units(const vxb_engine* e) { return e->eng.n_units; }
 uint32_t vxb_probes(const vxb_engine* e) { return (uint32_t)e->eng.probes.size(); }
+
+int vxb_create_generated(const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out) {
+    *out = nullptr;
+    auto* e = new vxb_engine();
+    try {
+        if (!spec) throw ConfigError("null network spec");
+        GenHost h;
+        build_gen_host(*spec, h);
+        g_gen_host = &h;
+        e->eng.load(&h.net, opt, spec);
+        g_gen_host = nullptr;
+    } catch (const std::exception& x) {
+        g_gen_host = nullptr;
+        g_create_error = x.what();
+        int rc = fail_code(x);
+        delete e;
+        return rc;
+    }
+    *out = e;
+    return VXB_OK;
+}
+
+int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t worker,
+                              vxb_neuron* neurons, uint32_t n_cap, vxb_syn_entry* synapses,
+                              uint64_t syn_cap, uint64_t* row_base) {
+    try {
+        if (!spec) throw ConfigError("null network spec");
+        GenHost h;
+        build_gen_host(*spec, h);
+        if (worker >= spec->n_workers) throw ConfigError("worker out of range");
+        const auto& recs = h.recs[worker];
+        if (n_cap < recs.size() || syn_cap < h.nsyn[worker])
+            throw ConfigError("output buffers too small");
+        std::vector<uint64_t> rb(recs.size() + 1, 0);
+        for (size_t i = 0; i < recs.size(); ++i) rb[i + 1] = rb[i] + recs[i].row_len;
+        std::vector<uint32_t> wb(spec->n_workers, 0);
+        for (uint32_t w = 1; w < spec->n_workers; ++w)
+            wb[w] = wb[w - 1] + (uint32_t)h.recs[w - 1].size();
+        const uint64_t nall = wb.back() + h.recs.back().size();
+        CK(cudaSetDevice(device));
+        cudaStream_t st = nullptr;
+        CK(cudaStreamCreate(&st));
+        GenDevTables T;
+        T.upload(h, *spec, wb, st);
+        DevBuf<uint64_t> d_rb;
+        DevBuf<uint4> d_rows;
+        DevBuf<unsigned long long> have;
+        d_rb.alloc(rb.size());
+        d_rows.alloc(std::max<uint64_t>(1, h.nsyn[worker]));
+        have.alloc(std::max<uint64_t>(1, nall));
+        have.zero(st);
+        CK(cudaMemcpyAsync(d_rb.p, rb.data(), 8 * rb.size(), cudaMemcpyHostToDevice, st));
+        if (h.total_neurons)
+            gen_kernel<2><<<148 * 8, 256, 0, st>>>(T.G, 0, h.total_neurons, nullptr, nullptr,
+                                                   nullptr, have.p, nullptr, worker, d_rb.p,
+                                                   d_rows.p);
+        CK(cudaGetLastError());
+        T.check(st, nullptr);
+        std::vector<unsigned long long> hv(nall);
+        if (nall) CK(cudaMemcpy(hv.data(), have.p, 8 * nall, cudaMemcpyDeviceToHost));
+        if (h.nsyn[worker])
+            CK(cudaMemcpy(synapses, d_rows.p, 16 * h.nsyn[worker], cudaMemcpyDeviceToHost));
+        cudaStreamDestroy(st);
+        for (size_t i = 0; i < recs.size(); ++i) {
+            neurons[i] = recs[i];
+            neurons[i].dst_mask = hv[wb[worker] + i];
+        }
+        std::memcpy(row_base, rb.data(), 8 * rb.size());
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return fail_code(x);
+    }
+}
 
 int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
                             double* out) {

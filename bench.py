@@ -1,0 +1,318 @@
+"""Benchmark of the B200 simulation step on BASELINE.json's config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): 1M conductance-LIF neurons (ring of 100
+voxels x 10 000, subcortex, 80% E / 20% I), in-degree K = 1000 (1e9 synapses,
+4 receptor types), dt = 1 ms, seed 2, ~10 Hz mean rate (g_location[AMPA] and
+ou_mean calibrated with tools/calibrate_rate.py; the reference defaults are
+bistable at K = 1000).  Synthetic network drawn by the
+reference's own sampler, on the device.
+
+One bench step = one SimInstance::advance of `--bio-ms` milliseconds of
+biological time (default 100 ms = 100 dt-steps).  Metric: synaptic events per
+second (events = delivered table entries, (gating_inner + gating_outer) / 2,
+engine.cpp:459-463); wall seconds per biological second is reported beside it.
+
+`value` uses the device time of the step kernel (CUDA events on the engine's
+launching stream), inputs resident in HBM.  `e2e` times the same advance
+through the C ABI as a caller sees it: synchronous call, results (rates,
+FLOP tallies, timing rows) copied back to host memory every step.  The
+synapse tables (12 GB) exceed L2 (126 MB), so no flush is needed.
+
+--impl reference runs the reference CPU engine (oracle/_ref/libvoxsim_ref.so,
+built from /root/reference/proj/src) on a bounded, down-scaled sample of the
+same workload (same K, parameters, dt and operating point; fewer voxels) with
+scheduler "threads" on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+G_LOC_10HZ = [-2.3, -4.1997, -0.2231, -2.9957]
+OU_MEAN_10HZ = 275.0
+SEED = 2
+
+
+def workload_cfg(voxels=100, npv=10000, k_in=1000, dt_ms=1.0, workers=1):
+    return {"seed": SEED, "dt_ms": dt_ms, "steps": 1000, "workers": workers,
+            "connectome": {"kind": "ring", "voxels": voxels, "neurons_per_voxel": npv},
+            "partition": {"method": "sequential" if workers == 1 else "greedy"},
+            "regions": {"subcortex": {"k_in": k_in, "g_location": G_LOC_10HZ,
+                                      "ou_mean": OU_MEAN_10HZ}}}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """DRAM bytes per step-kernel launch from the committed ncu capture of
+    this command (profiles/), or None."""
+    p = ROOT / "profiles" / "step_kernel_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class CpuReference:
+    """The reference engine on a down-scaled sample of the workload: same K,
+    parameters, dt and operating point, fewer voxels."""
+
+    def __init__(self, sample_voxels: int, threads: int):
+        sys.path.insert(0, str(ROOT / "tests"))
+        from refnet import RefNet, RefSim
+        from paper_2308_01241_b200.engine import SimOptions
+        self.workers = max(1, min(threads, 2 * sample_voxels))
+        cfg = workload_cfg(voxels=sample_voxels, workers=self.workers)
+        cfg["scheduler"] = "threads"
+        self.net = RefNet(cfg)
+        self.sim = RefSim(self.net, SimOptions(dt_ms=cfg["dt_ms"], record_raster=False,
+                                               record_timings=False),
+                          scheduler="threads" if self.workers > 1 else "loopback")
+        self.neurons = self.net.total_neurons
+        self.threads = 3 * self.workers if self.workers > 1 else 1
+
+    def step(self, steps: int):
+        r = self.sim.advance(steps)
+        events = (r.flops["gating_inner"] + r.flops["gating_outer"]) // 2
+        return events, r.seconds, r.total_spikes
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
+    for _ in range(args.warmup):
+        ref.step(args.cpu_steps)
+    ev = sec = spk = 0
+    for _ in range(args.steps):
+        e, s, k = ref.step(args.cpu_steps)
+        ev, sec, spk = ev + e, sec + s, spk + k
+    value = ev / sec
+    rate = spk / (ref.neurons * args.steps * args.cpu_steps * 1e-3)
+    sample = (f"ring {args.cpu_voxels} voxels x 10000 neurons, K=1000, dt=1 ms, "
+              f"{args.cpu_steps} steps per bench step, {ref.workers} workers "
+              f"(scheduler threads), {rate:.1f} Hz")
+    line = {"metric": "synaptic_events_per_s", "value": value, "unit": "events/s",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 state / i64 Q16 / f64 noise",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "config2-sample", "neurons": ref.neurons, "k_in": 1000,
+                       "dt_ms": 1.0, "parallelism": f"cpu threads x{ref.threads}"},
+            "wall_s_per_bio_s_extrapolated_1M": (sec / args.steps) / (args.cpu_steps * 1e-3)
+            * (1e6 / ref.neurons),
+            "cpu_baseline": {"value": value, "unit": "events/s", "cores": ref.threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("gloo")
+        dist = tdist
+    from paper_2308_01241_b200 import netgen
+    from paper_2308_01241_b200.engine import SimOptions
+
+    dev = local if ws > 1 else args.device
+    bio_steps = int(round(args.bio_ms / args.dt))
+    cfg = workload_cfg(dt_ms=args.dt)
+    net = netgen.build_network(cfg)
+    opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=True,
+                     device=dev)
+    sim = netgen.GeneratedSimInstance(net, opt)
+    for _ in range(args.warmup):
+        sim.advance(bio_steps)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    dev_ms, wall, events, spikes, h2d, d2h, launches, results = [], [], 0, 0, 0, 0, 0, []
+    with ClockSampler(dev) as clk:
+        barrier()
+        t_all = time.perf_counter()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = sim.advance(bio_steps)  # synchronous C-ABI call, results on host
+            wall.append(time.perf_counter() - t0)
+            dev_ms.append(r.device_ms)
+            events += r.events
+            spikes += r.total_spikes
+            h2d += r.h2d_bytes
+            d2h += r.d2h_bytes
+            launches += r.launches
+        barrier()
+        t_all = time.perf_counter() - t_all
+    sim.close()
+    dev_s = sum(dev_ms) / 1e3
+    wall_s = sum(wall)
+    # max over ranks of time, sum of work
+    if dist:
+        import torch
+        t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, wall_s = float(t[0]), float(t[1])
+        e = torch.tensor([events, spikes], dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        events, spikes = int(e[0]), int(e[1])
+    if rank != 0:
+        return
+    n = net.total_neurons * ws
+    bio_s = args.steps * bio_steps * args.dt * 1e-3
+    value = events / dev_s
+    rate = spikes / (n * bio_s)
+    # roofline of the step kernel: algorithmic bytes
+    neuron_steps = n * args.steps * bio_steps
+    alg_bytes = 98 * neuron_steps + 12 * events + 20 * spikes
+    peak, peak_kind = measured_peak_hbm()
+    achieved = alg_bytes / dev_s / 1e9
+    launches_per = max(1, launches // max(1, args.steps * ws))
+    traffic = ncu_traffic()
+    line = {
+        "metric": "synaptic_events_per_s", "value": value, "unit": "events/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 state / i64 Q16 / f64 noise", "data": "synthetic",
+        "config": {"workload": "config2", "neurons_per_gpu": net.total_neurons,
+                   "synapses_per_gpu": net.synapse_count, "k_in": 1000, "dt_ms": args.dt,
+                   "bio_ms_per_step": args.bio_ms, "seed": SEED,
+                   "parallelism": "replica" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (12 GB synapse table)"},
+        "wall_s_per_bio_s": dev_s / bio_s,
+        "mean_rate_hz": rate,
+        "events_per_s_per_gpu": value / ws,
+        "e2e": {"value": events / wall_s, "unit": "events/s",
+                "h2d_bytes_per_step": h2d // max(1, args.steps * ws),
+                "d2h_bytes_per_step": d2h // max(1, args.steps * ws),
+                "wall_s_per_bio_s": wall_s / bio_s},
+        "gpu_launches": launches // max(1, ws),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "vxb::step_kernel",
+                     "alg_bytes_per_launch": alg_bytes / max(1, launches_per * args.steps),
+                     "model": "98 B/neuron-step + 12 B/event + 20 B/delivered spike"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu:
+        try:
+            ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
+            ref.step(20)
+            e, s, k = ref.step(args.cpu_steps)
+            line["cpu_baseline"] = {
+                "value": e / s, "unit": "events/s", "cores": ref.threads, "kind": "reference",
+                "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_steps} "
+                          f"steps, {ref.workers} workers (threads), "
+                          f"{k / (ref.neurons * args.cpu_steps * 1e-3):.1f} Hz, "
+                          f"{s:.1f} s of CPU time"}
+        except Exception as e:  # the checker is optional on the GPU arm
+            line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--bio-ms", type=float, default=100.0)
+    ap.add_argument("--dt", type=float, default=1.0)
+    ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--cpu-voxels", type=int, default=8)
+    ap.add_argument("--cpu-steps", type=int, default=100)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -29,12 +29,12 @@ def main():
     ap.add_argument("--dt", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--ampa", type=float, nargs="+", default=[-1.8, -1.75, -1.7, -1.65, -1.6])
-    ap.add_argument("--ou-mean", type=float, default=None)
+    ap.add_argument("--ou-mean", type=float, nargs="+", default=[None])
     a = ap.parse_args()
-    for ampa in a.ampa:
+    for ampa, ou in [(x, y) for y in a.ou_mean for x in a.ampa]:
         reg = {"k_in": a.k, "g_location": [ampa] + G_LOC[1:]}
-        if a.ou_mean is not None:
-            reg["ou_mean"] = a.ou_mean
+        if ou is not None:
+            reg["ou_mean"] = ou
         cfg = {"seed": a.seed, "dt_ms": a.dt, "steps": a.steps, "workers": 1,
                "connectome": {"kind": "ring", "voxels": a.voxels, "neurons_per_voxel": a.npv},
                "partition": {"method": "sequential"}, "regions": {"subcortex": reg}}
@@ -47,7 +47,7 @@ def main():
             t2 = time.time()
             r = sim.advance(a.steps)
         half = r.rates.network_mean_hz(a.steps // 2)
-        print(json.dumps({"ampa": ampa, "rate_hz": r.rates.network_mean_hz(0),
+        print(json.dumps({"ampa": ampa, "ou_mean": ou, "rate_hz": r.rates.network_mean_hz(0),
                           "rate_hz_2nd_half": half, "events": r.events,
                           "device_ms": r.device_ms, "host_build_s": t1 - t0,
                           "gen_s": t2 - t1, "synapses": net.synapse_count}), flush=True)

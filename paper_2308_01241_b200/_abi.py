@@ -201,7 +201,7 @@ def load_library(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("VXB_LIB", LIB_PATH))
     if not p.exists():
         raise RuntimeError(
             f"CUDA engine library {p} is missing: run `python -c 'import __graft_entry__ as g; "

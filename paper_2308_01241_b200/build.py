@@ -48,17 +48,20 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in deps())
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    if not force and up_to_date():
+def build(verbose: bool = False, force: bool = False, out: Path = OUT,
+          defines: dict | None = None) -> Path:
+    """Compile libvxb.so; `defines` (-D) select kernel tuning variants."""
+    if not force and out == OUT and up_to_date():
         return OUT
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, f"-I{ROOT / 'include'}", f"-I{CSRC}",
-           *(str(s) for s in sources()), "-o", str(OUT) + ".tmp"]
+    dflags = [f"-D{k}={v}" for k, v in (defines or {}).items()]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *dflags, f"-I{ROOT / 'include'}", f"-I{CSRC}",
+           *(str(s) for s in sources()), "-o", str(out) + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(str(OUT) + ".tmp", OUT)
-    return OUT
+    os.replace(str(out) + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -198,13 +198,86 @@ struct Pend<false> {  // four signed int64 buckets, the reference's layout
 };
 
 constexpr int kMaxSmemSeg = 256;
-constexpr int kThreads = 512;
+#ifndef VXB_THREADS
+#define VXB_THREADS 256
+#endif
+#ifndef VXB_MINB
+#define VXB_MINB 3
+#endif
+#ifndef VXB_BATCH
+#define VXB_BATCH 4
+#endif
+constexpr int kThreads = VXB_THREADS;
+constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
+constexpr int kBatch = VXB_BATCH;  // delivery entries in flight per lane
+
+// L2 eviction-priority policies (createpolicy): the synapse stream is read
+// once per spike and must not evict the pending buffers the atomics hit.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+        : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint64_t pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;"
+                 ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Per-neuron state the fused update reads (prefetched one neuron ahead).
+template <bool PACKED>
+struct NIn {
+    uint32_t vb;
+    float4 j;
+    float iou;
+    float4 g;
+    ulonglong2 p0, p1;  // pending of S(tE-1); p1 only in the wide layout
+    float isyn;
+};
 
 template <bool PACKED>
-__global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
-    using PT = typename Pend<PACKED>::T;
+__device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool doE,
+                                            const void* pend_rd, NIn<PACKED>& x) {
+    x.vb = a.v[i];
+    x.iou = a.i_ou[i];
+    if (doE) {
+        x.j = a.j[i];
+        x.g = a.g[i];
+        if constexpr (PACKED) {
+            x.p0 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + i);
+        } else {
+            x.p0 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i);
+            x.p1 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i + 1);
+        }
+    } else {
+        x.isyn = a.i_syn[i];
+    }
+}
+
+template <bool PACKED>
+__global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __shared__ SegParams s_seg[kMaxSmemSeg];
     __shared__ uint32_t s_start[kMaxSmemSeg + 1];
+    __shared__ uint32_t s_spk[kSpkStage];
+    __shared__ uint32_t s_nspk;
+    __shared__ uint32_t s_base;
+    __shared__ int s_stop;
 
     const SegParams* segp = a.seg;
     const uint32_t* startp = a.seg_start;
@@ -214,18 +287,20 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
             s_start[k] = a.seg_start[k];
         }
         if (threadIdx.x == 0) s_start[a.nseg] = a.n;
-        __syncthreads();
         segp = s_seg;
         startp = s_start;
     }
+    if (threadIdx.x == 0) s_nspk = 0;
+    __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gthreads = gridDim.x * blockDim.x;
-    const uint32_t gwarps = gthreads >> 5;
-    (void)gwarps;
+    const uint32_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
     Control* ctl = a.ctl;
     unsigned long long my_inner = 0, my_outer = 0;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
 
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
@@ -235,60 +310,59 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
         const uint32_t tA = a.t0 + ph;
         const uint32_t tE = tA - 1;
         // pending buffer consumed by E(tE) holds S(tE-1): parity (tE-1)&1 == tA&1
-        PT* pend_rd = reinterpret_cast<PT*>((tA & 1u) ? a.pend1 : a.pend0);
+        void* pend_rd = (tA & 1u) ? a.pend1 : a.pend0;
         // deliveries of S(tE) go to parity tE&1
-        PT* pend_wr = reinterpret_cast<PT*>((tE & 1u) ? a.pend1 : a.pend0);
+        void* pend_wr = (tE & 1u) ? a.pend1 : a.pend0;
         const uint32_t inj_ep = (doA && a.has_inj) ? a.inj_epoch[ph] : 0u;
         uint32_t f_lo = 0, f_hi = 0;
         if (doA && a.has_forced) {
             f_lo = a.forced_off[ph];
             f_hi = a.forced_off[ph + 1];
         }
-        uint32_t log_base;  // where this phase's spikes go
-        if (a.ring)
-            log_base = (ph & 1u) * a.n;
-        else
-            log_base = 0;
+        const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
 
         // ------------------------------------------------------------ F
         const uint32_t n_round = (a.n + 31u) & ~31u;
-        for (uint32_t i0 = gtid; i0 < n_round; i0 += gthreads) {
-            const uint32_t i = i0;
+        NIn<PACKED> cur, nxt;
+        if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
+        for (uint32_t i = gtid; i < n_round; i += gthreads) {
             const bool live = i < a.n;
+            const uint32_t inext = i + gthreads;
+            if (inext < a.n) load_neuron<PACKED>(a, inext, doE, pend_rd, nxt);
             bool spiked = false;
+            uint32_t seg = 0;
             if (live) {
-                const SegParams& P = segp[find_seg(startp, a.nseg, i)];
-                uint32_t vb = a.v[i];
-                float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                float4 j = a.j[i];
-                float iou = a.i_ou[i];
+                seg = find_seg(startp, a.nseg, i);
+                const SegParams& P = segp[seg];
+                uint32_t vb = cur.vb;
+                const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                float4 j = cur.j;
+                float iou = cur.iou;
                 float isyn;
                 if (doE) {
                     // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
                     float p0, p1, p2, p3;
                     if constexpr (PACKED) {
-                        const ulonglong2 pv = __ldcg(pend_rd + i);
-                        p0 = dequantize((int64_t)(uint32_t)(pv.x & 0xffffffffull));
-                        p1 = dequantize((int64_t)(uint32_t)(pv.x >> 32));
-                        p2 = dequantize((int64_t)(uint32_t)(pv.y & 0xffffffffull));
-                        p3 = dequantize((int64_t)(uint32_t)(pv.y >> 32));
-                        __stcg(pend_rd + i, make_ulonglong2(0ull, 0ull));
+                        p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
+                        p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
+                        p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
+                        p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
+                        __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
                     } else {
-                        longlong2* q = reinterpret_cast<longlong2*>(pend_rd + i);
-                        const longlong2 lo = __ldcg(q), hi = __ldcg(q + 1);
-                        p0 = dequantize(lo.x);
-                        p1 = dequantize(lo.y);
-                        p2 = dequantize(hi.x);
-                        p3 = dequantize(hi.y);
-                        __stcg(q, make_longlong2(0, 0));
-                        __stcg(q + 1, make_longlong2(0, 0));
+                        p0 = dequantize((int64_t)cur.p0.x);
+                        p1 = dequantize((int64_t)cur.p0.y);
+                        p2 = dequantize((int64_t)cur.p1.x);
+                        p3 = dequantize((int64_t)cur.p1.y);
+                        ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
+                        __stcg(q, make_ulonglong2(0ull, 0ull));
+                        __stcg(q + 1, make_ulonglong2(0ull, 0ull));
                     }
                     j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
                     j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
                     j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
                     j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
                     // current_kernel (model.hpp:73-81), u order, from 0.0f
-                    const float4 g = a.g[i];
+                    const float4 g = cur.g;
                     float c = 0.0f;
                     c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
                     c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
@@ -303,8 +377,10 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
                     }
                     iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
                     if (!doA) a.i_syn[i] = isyn;
+                    a.j[i] = j;
+                    a.i_ou[i] = iou;
                 } else {
-                    isyn = a.i_syn[i];
+                    isyn = cur.isyn;
                 }
                 if (doA) {
                     // membrane_kernel + threshold (engine.cpp:363-385)
@@ -314,11 +390,13 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
                     } else {
                         float inoise = iou;
                         if (inj_ep) {
-                            const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
+                            const float x =
+                                __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
                             if (x != 0.0f) inoise = fadd(iou, x);
                         }
-                        const float nv = fadd(v, fmul(P.dt_over_c,
-                                                      fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                        const float nv = fadd(
+                            v, fmul(P.dt_over_c,
+                                    fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
                         if (!isfinite(nv)) {
                             atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
                             vb = __float_as_uint(nv);
@@ -329,58 +407,56 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
                             vb = __float_as_uint(nv);
                         }
                     }
+                    // forced spikes (engine.cpp:389-398): join unless already fired
+                    if (f_hi > f_lo && !spiked) {
+                        const uint32_t k =
+                            f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                        if (k < f_hi && __ldg(a.forced_local + k) == i) {
+                            spiked = true;
+                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                        }
+                    }
+                    a.v[i] = vb;
                 }
-                if (doE) {
-                    a.j[i] = j;
-                    a.i_ou[i] = iou;
-                }
-                if (doA) a.v[i] = vb;
                 // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
                 if (a.n_probes) {
                     uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
                     while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
-                        const uint32_t slot = __ldg(a.probe_slot + k);
-                        if (doE) a.probe_i[(size_t)slot * a.adv_steps + a.rel0 + ph - 1] = isyn;
+                        const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
+                        if (doE) a.probe_i[row + ph - 1] = isyn;
+                        if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
                         ++k;
                     }
                 }
             }
-            // forced spikes (engine.cpp:389-398): join unless already fired
-            if (doA && f_hi > f_lo && live) {
-                const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
-                if (k < f_hi && __ldg(a.forced_local + k) == i && !spiked) {
-                    const SegParams& P = segp[find_seg(startp, a.nseg, i)];
-                    spiked = true;
-                    a.v[i] = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                }
-            }
-            if (doA && live && a.n_probes) {
-                uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
-                while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
-                    const uint32_t slot = __ldg(a.probe_slot + k);
-                    const uint32_t vb = a.v[i];
-                    const SegParams& P = segp[find_seg(startp, a.nseg, i)];
-                    a.probe_v[(size_t)slot * a.adv_steps + a.rel0 + ph] =
-                        is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                    ++k;
-                }
-            }
-            // spike log append + rates (engine.cpp:400-404), warp aggregated
+            // spike staging + rates (engine.cpp:400-404), warp aggregated
             const unsigned ball = __ballot_sync(0xffffffffu, spiked);
             if (ball) {
                 unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&ctl->spk_cursor, (unsigned)__popc(ball));
+                if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (spiked) {
                     const unsigned rank = __popc(ball & ((1u << lane) - 1u));
-                    a.spk[log_base + base + rank] = i;
-                    const uint32_t unit = segp[find_seg(startp, a.nseg, i)].unit;
+                    if (base + rank < kSpkStage)
+                        s_spk[base + rank] = i;
+                    else  // staging full: straight to the log
+                        a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                    const uint32_t unit = segp[seg].unit;
                     const unsigned peers = __match_any_sync(ball, unit);
                     if ((unsigned)__ffs(peers) - 1u == lane)
                         atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
                 }
             }
+            cur = nxt;
         }
+        // flush the CTA's staged spikes with one log reservation
+        __syncthreads();
+        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
+        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x)
+            a.spk[log_base + s_base + k] = s_spk[k];
+        if (threadIdx.x == 0) s_nspk = 0;
 
         // ------------------------------------------------------------ D
         if (doE) {
@@ -388,33 +464,55 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
             const uint32_t hi = __ldcg(a.seg_end + ph - 1);
             const uint32_t prev_base = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
             const uint32_t cnt = hi - lo;
-            for (;;) {
-                unsigned k = 0;
-                if (lane == 0) k = atomicAdd(&ctl->work, 1u);
-                k = __shfl_sync(0xffffffffu, k, 0);
-                if (k >= cnt) break;
-                const uint32_t s = __ldcg(a.spk + prev_base + lo + k);
-                const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
-                for (uint64_t e = e0 + lane; e < e1; e += 32) {
-                    const uint32_t t = __ldg(a.tgt + e);
-                    const uint64_t wq = ldg64(a.w + e);
-                    const uint32_t tid = t & 0x7fffffffu;
-                    const uint32_t cls = t >> 31;
-                    if constexpr (PACKED) {
-                        unsigned long long* dst =
-                            reinterpret_cast<unsigned long long*>(pend_wr + tid) + cls;
-                        atomicAdd(dst, (unsigned long long)wq);
-                    } else {
-                        unsigned long long* dst =
-                            reinterpret_cast<unsigned long long*>(pend_wr + tid) + 2 * cls;
-                        atomicAdd(dst, (unsigned long long)(long long)(int32_t)(uint32_t)wq);
-                        atomicAdd(dst + 1, (unsigned long long)(long long)(int32_t)(uint32_t)(wq >> 32));
+            if (cnt) {
+                // every spike row is cut into C pieces; pieces are dealt to
+                // warps round-robin (no work counter on the critical path)
+                const uint32_t C = min(32u, max(1u, (4u * gwarps + cnt - 1) / cnt));
+                const uint32_t items = cnt * C;
+                for (uint32_t item = gwarp; item < items; item += gwarps) {
+                    const uint32_t k = item / C, c = item - k * C;
+                    const uint32_t s = __ldcg(a.spk + prev_base + lo + k);
+                    const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
+                    const uint64_t len = e1 - e0;
+                    const uint64_t b0 = e0 + len * c / C, b1 = e0 + len * (c + 1) / C;
+                    for (uint64_t base = b0; base < b1; base += 32 * kBatch) {
+                        uint32_t t[kBatch];
+                        uint64_t wq[kBatch];
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) {
+                            const uint64_t e = base + lane + 32 * u;
+                            if (e < b1) {
+                                t[u] = ld_stream(a.tgt + e, pol_stream);
+                                wq[u] = ld_stream(a.w + e, pol_stream);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < kBatch; ++u) {
+                            const uint64_t e = base + lane + 32 * u;
+                            if (e < b1) {
+                                const uint32_t tid = t[u] & 0x7fffffffu, cls = t[u] >> 31;
+                                unsigned long long* dst;
+                                if constexpr (PACKED) {
+                                    dst = reinterpret_cast<unsigned long long*>(pend_wr) +
+                                          2 * (size_t)tid + cls;
+                                    red_add(dst, wq[u], pol_keep);
+                                } else {
+                                    dst = reinterpret_cast<unsigned long long*>(pend_wr) +
+                                          4 * (size_t)tid + 2 * cls;
+                                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq[u],
+                                            pol_keep);
+                                    red_add(dst + 1,
+                                            (uint64_t)(int64_t)(int32_t)(uint32_t)(wq[u] >> 32),
+                                            pol_keep);
+                                }
+                            }
+                        }
                     }
-                }
-                if (lane == 0) {
-                    const uint32_t in = __ldg(a.inner + s);
-                    my_inner += 2ull * in;
-                    my_outer += 2ull * ((e1 - e0) - in);
+                    if (lane == 0 && c == 0) {
+                        const uint32_t in = __ldg(a.inner + s);
+                        my_inner += 2ull * in;
+                        my_outer += 2ull * (len - in);
+                    }
                 }
             }
         }
@@ -422,10 +520,11 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(StepArgs a) {
         grid_barrier(ctl, [&] {
             if (doA) a.seg_end[ph] = ctl->spk_cursor;
             if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
-            ctl->work = 0;
             a.phase_ns[ph + 1] = globaltimer();
         });
-        if (*((volatile unsigned long long*)&ctl->err) != ~0ull) break;
+        if (threadIdx.x == 0) s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull;  // L2-coherent
+        __syncthreads();
+        if (s_stop) break;
     }
     if (lane == 0 && (my_inner | my_outer)) {
         atomicAdd(&ctl->flops_inner, my_inner);

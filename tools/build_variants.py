@@ -1,0 +1,20 @@
+"""Build kernel tuning variants of libvxb.so into build/variants/ (A/B runs
+select one with VXB_LIB=...)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2308_01241_b200 import build as b
+
+VARIANTS = {
+    "t512m1b8": {"VXB_THREADS": 512, "VXB_MINB": 1, "VXB_BATCH": 8},
+    "t256m3b8": {"VXB_THREADS": 256, "VXB_MINB": 3, "VXB_BATCH": 8},
+    "t256m3b4": {"VXB_THREADS": 256, "VXB_MINB": 3, "VXB_BATCH": 4},
+    "t512m2b4": {"VXB_THREADS": 512, "VXB_MINB": 2, "VXB_BATCH": 4},
+}
+if __name__ == "__main__":
+    out = b.ROOT / "build" / "variants"
+    out.mkdir(parents=True, exist_ok=True)
+    names = sys.argv[1:] or list(VARIANTS)
+    for n in names:
+        b.build(force=True, out=out / f"libvxb_{n}.so", defines=VARIANTS[n])
+        print(n)

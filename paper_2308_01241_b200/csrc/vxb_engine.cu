@@ -104,6 +104,10 @@ struct Engine {
     std::vector<vxb_injection> injections;
     bool packed = true;
     uint64_t n_syn = 0;
+    uint64_t max_row = 0;
+    uint32_t pieces = 1;
+    bool use_smem_seg = true;
+    uint32_t smem_bytes = 0;
 
     // ---------------------------------------------------------- device
     cudaStream_t stream = nullptr;
@@ -441,13 +445,29 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     const std::string tr = opt->transport ? opt->transport : "queue";
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
+    // longest out-row: delivery pieces per spike (<= kStageE entries each)
+    {
+        std::vector<uint64_t> off(n + 1);
+        CK(cudaMemcpyAsync(off.data(), d_off.p, 8ull * (n + 1), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        uint64_t mx = 0;
+        for (uint32_t i = 0; i < n; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);
+        max_row = mx;
+        pieces = (uint32_t)std::max<uint64_t>(1, (mx + kStageE - 1) / kStageE);
+    }
     // cooperative grid
+    use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg;
+    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u).total;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const void* kfn = packed ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
     if (packed)
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads,
+                                                         smem_bytes));
     else
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads,
+                                                         smem_bytes));
     if (per_sm < 1) throw SimError("step kernel cannot be resident on this device");
     grid = sms * per_sm;
     CK(cudaStreamSynchronize(stream));
@@ -509,8 +529,8 @@ void Engine::build_csr(const vxb_network* net) {
         CK(cudaMemsetAsync(d_off.p, 0, 8, stream));
     }
     CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n, cudaMemcpyDeviceToDevice, stream));
-    d_tgt.alloc(n_syn);
-    d_w.alloc(n_syn);
+    d_tgt.alloc(n_syn + 4);  // +pad: bulk copies read 16-byte aligned supersets
+    d_w.alloc(n_syn + 2);
     d_inner.alloc(n);
     d_inner.zero(stream);
     d_keys.alloc(n);  // reused as have_mask for the consistency check
@@ -813,8 +833,8 @@ void Engine::generate_csr(const vxb_netspec& spec) {
         CK(cudaMemsetAsync(d_off.p, 0, 8, stream));
     }
     CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n, cudaMemcpyDeviceToDevice, stream));
-    d_tgt.alloc(n_syn);
-    d_w.alloc(n_syn);
+    d_tgt.alloc(n_syn + 4);
+    d_w.alloc(n_syn + 2);
     d_inner.alloc(n);
     d_inner.zero(stream);
     d_keys.alloc(n);  // have_mask
@@ -1000,7 +1020,8 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.adv_steps = adv_steps;
     a.spk_cap = (uint32_t)d_spk.n;
     a.ring = record_raster ? 0u : 1u;
-    a.use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg ? 1u : 0u;
+    a.use_smem_seg = use_smem_seg ? 1u : 0u;
+    a.pieces = pieces;
     a.dtf = dtf;
     a.ou_root = mix_key(seed, 1);  // rngstream::ou_noise (rng.hpp:18)
     a.seg = d_seg.p;
@@ -1037,11 +1058,11 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
     if (packed)
-        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args, 0,
-                                       stream));
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args,
+                                       smem_bytes, stream));
     else
-        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<false>, grid, kThreads, args, 0,
-                                       stream));
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<false>, grid, kThreads, args,
+                                       smem_bytes, stream));
     CK(cudaEventRecord(ev1, stream));
     launches += 1;
 

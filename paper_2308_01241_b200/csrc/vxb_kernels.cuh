@@ -78,6 +78,7 @@ struct StepArgs {
     uint32_t spk_cap;       // spike log capacity
     uint32_t ring;          // spike log in ring mode (raster not recorded)
     uint32_t use_smem_seg;
+    uint32_t pieces;        // delivery pieces per spike row (<= kStageE entries each)
     float dtf;
     uint64_t ou_root;       // mix_key(seed, rngstream::ou_noise)
     // parameters
@@ -209,6 +210,73 @@ constexpr int kMaxSmemSeg = 256;
 #endif
 constexpr int kThreads = VXB_THREADS;
 constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
+#ifndef VXB_DFIRST
+#define VXB_DFIRST 0
+#endif
+#ifndef VXB_STAGES
+#define VXB_STAGES 4
+#endif
+#ifndef VXB_STAGE_E
+#define VXB_STAGE_E 768
+#endif
+constexpr int kStages = VXB_STAGES;   // delivery pipeline depth (bulk copies in flight)
+constexpr int kStageE = VXB_STAGE_E;  // synapse entries per stage
+constexpr int kStageTgtBytes = (kStageE + 8) * 4;
+constexpr int kStageWBytes = (kStageE + 4) * 8;
+
+struct StageMeta {
+    uint32_t n;       // entries in the piece
+    uint32_t head_t;  // entries skipped at the front of the tgt copy (16 B alignment)
+    uint32_t head_w;
+    uint32_t spike;   // source (shard-local) or ~0 when the piece is empty
+    uint32_t first;   // piece 0 of its row (flop tally)
+    uint32_t len;     // row length
+};
+
+// Dynamic shared memory carve-up of step_kernel.
+struct SmemLayout {
+    uint32_t tgt, w, bar, meta, seg, start, spk, total;
+    __host__ __device__ SmemLayout(uint32_t nseg_smem) {
+        tgt = 0;
+        w = tgt + kStages * kStageTgtBytes;
+        bar = w + kStages * kStageWBytes;
+        meta = bar + kStages * 8;
+        seg = (meta + kStages * (uint32_t)sizeof(StageMeta) + 127) & ~127u;
+        start = seg + nseg_smem * (uint32_t)sizeof(SegParams);
+        spk = (start + (nseg_smem + 1) * 4 + 15) & ~15u;
+        total = spk + kSpkStage * 4;
+    }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "VXB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra VXB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity) : "memory");
+}
+// cp.async.bulk (TMA bulk copy) global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes),
+        "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
 constexpr int kBatch = VXB_BATCH;  // delivery entries in flight per lane
 
 // L2 eviction-priority policies (createpolicy): the synapse stream is read
@@ -238,6 +306,42 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
 __device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint64_t pol) {
     asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;"
                  ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Starts the bulk copies of one delivery piece (item = spike k, piece c of
+// C) into stage `st`.  Pieces are 16-byte aligned supersets of the entry
+// range; the head offsets are recorded in the stage's metadata.
+template <bool PACKED>
+__device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* smem,
+                                            const SmemLayout& L, uint32_t st, uint32_t item,
+                                            uint32_t C, uint32_t spk_base, uint64_t pol) {
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta) + st;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+    const uint32_t k = item / C, c = item - k * C;
+    const uint32_t s = __ldcg(a.spk + spk_base + k);
+    const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
+    const uint64_t len = e1 - e0;
+    const uint64_t b0 = e0 + len * c / C, b1 = e0 + len * (c + 1) / C;
+    StageMeta m;
+    m.spike = s;
+    m.first = c == 0;
+    m.len = (uint32_t)len;
+    m.n = (uint32_t)(b1 - b0);
+    if (m.n == 0) {
+        m.head_t = m.head_w = 0;
+        *meta = m;
+        mbar_arrive(bar);
+        return;
+    }
+    const uint64_t t0 = b0 & ~3ull, t1 = (b1 + 3) & ~3ull;
+    const uint64_t w0 = b0 & ~1ull, w1 = (b1 + 1) & ~1ull;
+    m.head_t = (uint32_t)(b0 - t0);
+    m.head_w = (uint32_t)(b0 - w0);
+    *meta = m;
+    const uint32_t tb = (uint32_t)(t1 - t0) * 4, wb = (uint32_t)(w1 - w0) * 8;
+    mbar_expect_tx(bar, tb + wb);
+    bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
+    bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
 }
 
 // Per-neuron state the fused update reads (prefetched one neuron ahead).
@@ -272,9 +376,13 @@ __device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool 
 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
-    __shared__ SegParams s_seg[kMaxSmemSeg];
-    __shared__ uint32_t s_start[kMaxSmemSeg + 1];
-    __shared__ uint32_t s_spk[kSpkStage];
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u);
+    SegParams* s_seg = reinterpret_cast<SegParams*>(smem + L.seg);
+    uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
+    uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+    StageMeta* s_meta = reinterpret_cast<StageMeta*>(smem + L.meta);
     __shared__ uint32_t s_nspk;
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
@@ -290,17 +398,21 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         segp = s_seg;
         startp = s_start;
     }
-    if (threadIdx.x == 0) s_nspk = 0;
+    if (threadIdx.x == 0) {
+        s_nspk = 0;
+        for (int k = 0; k < kStages; ++k) mbar_init(s_bar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gthreads = gridDim.x * blockDim.x;
-    const uint32_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
     Control* ctl = a.ctl;
     unsigned long long my_inner = 0, my_outer = 0;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
+    uint32_t g_item = 0;  // pieces this CTA has consumed since launch (stage/parity)
 
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
@@ -320,6 +432,58 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             f_hi = a.forced_off[ph + 1];
         }
         const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
+
+        // D work of this phase: pieces of the rows of S(tE), dealt to CTAs
+        // round-robin; the first kStages pieces start streaming into shared
+        // memory now, under the neuron update.
+        uint32_t d_lo = 0, d_cnt = 0, d_C = 1, d_mine = 0, d_prev = 0;
+        if (doE) {
+            d_lo = (ph >= 2 && !a.ring) ? __ldcg(a.seg_end + ph - 2) : 0u;
+            d_cnt = __ldcg(a.seg_end + ph - 1) - d_lo;
+            d_prev = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
+            d_C = a.pieces;
+            const uint32_t items = d_cnt * d_C;
+            d_mine = items > blockIdx.x ? (items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+            if (threadIdx.x == 0 && d_mine) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (threadIdx.x == 0)
+                for (uint32_t j = 0; j < d_mine && j < (uint32_t)kStages; ++j)
+                    issue_piece<PACKED>(a, smem, L, (g_item + j) % kStages,
+                                        blockIdx.x + j * gridDim.x, d_C, d_prev + d_lo, pol_stream);
+        }
+
+#if VXB_DFIRST
+        // ------------------------------------------------------------ D
+        for (uint32_t j = 0; j < d_mine; ++j, ++g_item) {
+            const uint32_t st = g_item % kStages;
+            mbar_wait(s_bar + st, (g_item / kStages) & 1u);
+            const StageMeta m = s_meta[st];
+            const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
+            const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
+            for (uint32_t e = threadIdx.x; e < m.n; e += blockDim.x) {
+                const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
+                const uint64_t wq = wv[e];
+                if constexpr (PACKED) {
+                    red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
+                            wq, pol_keep);
+                } else {
+                    unsigned long long* dst =
+                        reinterpret_cast<unsigned long long*>(pend_wr) + 4 * (size_t)tid + 2 * cls;
+                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq, pol_keep);
+                    red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
+                }
+            }
+            if (threadIdx.x == 0 && m.first && m.spike != ~0u) {
+                const uint32_t in = __ldg(a.inner + m.spike);
+                my_inner += 2ull * in;
+                my_outer += 2ull * (m.len - in);
+            }
+            __syncthreads();  // stage st drained by every thread
+            if (threadIdx.x == 0 && j + kStages < d_mine) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x, d_C,
+                                    d_prev + d_lo, pol_stream);
+            }
+        }
 
         // ------------------------------------------------------------ F
         const uint32_t n_round = (a.n + 31u) & ~31u;
@@ -458,65 +622,178 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             a.spk[log_base + s_base + k] = s_spk[k];
         if (threadIdx.x == 0) s_nspk = 0;
 
-        // ------------------------------------------------------------ D
-        if (doE) {
-            const uint32_t lo = (ph >= 2 && !a.ring) ? __ldcg(a.seg_end + ph - 2) : 0u;
-            const uint32_t hi = __ldcg(a.seg_end + ph - 1);
-            const uint32_t prev_base = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
-            const uint32_t cnt = hi - lo;
-            if (cnt) {
-                // every spike row is cut into C pieces; pieces are dealt to
-                // warps round-robin (no work counter on the critical path)
-                const uint32_t C = min(32u, max(1u, (4u * gwarps + cnt - 1) / cnt));
-                const uint32_t items = cnt * C;
-                for (uint32_t item = gwarp; item < items; item += gwarps) {
-                    const uint32_t k = item / C, c = item - k * C;
-                    const uint32_t s = __ldcg(a.spk + prev_base + lo + k);
-                    const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
-                    const uint64_t len = e1 - e0;
-                    const uint64_t b0 = e0 + len * c / C, b1 = e0 + len * (c + 1) / C;
-                    for (uint64_t base = b0; base < b1; base += 32 * kBatch) {
-                        uint32_t t[kBatch];
-                        uint64_t wq[kBatch];
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) {
-                            const uint64_t e = base + lane + 32 * u;
-                            if (e < b1) {
-                                t[u] = ld_stream(a.tgt + e, pol_stream);
-                                wq[u] = ld_stream(a.w + e, pol_stream);
-                            }
+#else
+        // ------------------------------------------------------------ F
+        const uint32_t n_round = (a.n + 31u) & ~31u;
+        NIn<PACKED> cur, nxt;
+        if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
+        for (uint32_t i = gtid; i < n_round; i += gthreads) {
+            const bool live = i < a.n;
+            const uint32_t inext = i + gthreads;
+            if (inext < a.n) load_neuron<PACKED>(a, inext, doE, pend_rd, nxt);
+            bool spiked = false;
+            uint32_t seg = 0;
+            if (live) {
+                seg = find_seg(startp, a.nseg, i);
+                const SegParams& P = segp[seg];
+                uint32_t vb = cur.vb;
+                const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                float4 j = cur.j;
+                float iou = cur.iou;
+                float isyn;
+                if (doE) {
+                    // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
+                    float p0, p1, p2, p3;
+                    if constexpr (PACKED) {
+                        p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
+                        p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
+                        p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
+                        p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
+                        __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
+                    } else {
+                        p0 = dequantize((int64_t)cur.p0.x);
+                        p1 = dequantize((int64_t)cur.p0.y);
+                        p2 = dequantize((int64_t)cur.p1.x);
+                        p3 = dequantize((int64_t)cur.p1.y);
+                        ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
+                        __stcg(q, make_ulonglong2(0ull, 0ull));
+                        __stcg(q + 1, make_ulonglong2(0ull, 0ull));
+                    }
+                    j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
+                    j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
+                    j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
+                    j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
+                    // current_kernel (model.hpp:73-81), u order, from 0.0f
+                    const float4 g = cur.g;
+                    float c = 0.0f;
+                    c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
+                    c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
+                    c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
+                    c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
+                    isyn = c;
+                    // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
+                    float xi = 0.0f;
+                    if (P.sigma_pos) {
+                        const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
+                        xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
+                    }
+                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                    if (!doA) a.i_syn[i] = isyn;
+                    a.j[i] = j;
+                    a.i_ou[i] = iou;
+                } else {
+                    isyn = cur.isyn;
+                }
+                if (doA) {
+                    // membrane_kernel + threshold (engine.cpp:363-385)
+                    if (is_refrac(vb)) {
+                        const uint32_t r = (vb & 0x007fffffu) - 1u;
+                        vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
+                    } else {
+                        float inoise = iou;
+                        if (inj_ep) {
+                            const float x =
+                                __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
+                            if (x != 0.0f) inoise = fadd(iou, x);
                         }
-#pragma unroll
-                        for (int u = 0; u < kBatch; ++u) {
-                            const uint64_t e = base + lane + 32 * u;
-                            if (e < b1) {
-                                const uint32_t tid = t[u] & 0x7fffffffu, cls = t[u] >> 31;
-                                unsigned long long* dst;
-                                if constexpr (PACKED) {
-                                    dst = reinterpret_cast<unsigned long long*>(pend_wr) +
-                                          2 * (size_t)tid + cls;
-                                    red_add(dst, wq[u], pol_keep);
-                                } else {
-                                    dst = reinterpret_cast<unsigned long long*>(pend_wr) +
-                                          4 * (size_t)tid + 2 * cls;
-                                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq[u],
-                                            pol_keep);
-                                    red_add(dst + 1,
-                                            (uint64_t)(int64_t)(int32_t)(uint32_t)(wq[u] >> 32),
-                                            pol_keep);
-                                }
-                            }
+                        const float nv = fadd(
+                            v, fmul(P.dt_over_c,
+                                    fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                        if (!isfinite(nv)) {
+                            atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
+                            vb = __float_as_uint(nv);
+                        } else if (nv >= P.v_th) {
+                            spiked = true;
+                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                        } else {
+                            vb = __float_as_uint(nv);
                         }
                     }
-                    if (lane == 0 && c == 0) {
-                        const uint32_t in = __ldg(a.inner + s);
-                        my_inner += 2ull * in;
-                        my_outer += 2ull * (len - in);
+                    // forced spikes (engine.cpp:389-398): join unless already fired
+                    if (f_hi > f_lo && !spiked) {
+                        const uint32_t k =
+                            f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                        if (k < f_hi && __ldg(a.forced_local + k) == i) {
+                            spiked = true;
+                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                        }
+                    }
+                    a.v[i] = vb;
+                }
+                // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
+                if (a.n_probes) {
+                    uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                    while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                        const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
+                        if (doE) a.probe_i[row + ph - 1] = isyn;
+                        if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                        ++k;
                     }
                 }
             }
+            // spike staging + rates (engine.cpp:400-404), warp aggregated
+            const unsigned ball = __ballot_sync(0xffffffffu, spiked);
+            if (ball) {
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (spiked) {
+                    const unsigned rank = __popc(ball & ((1u << lane) - 1u));
+                    if (base + rank < kSpkStage)
+                        s_spk[base + rank] = i;
+                    else  // staging full: straight to the log
+                        a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                    const uint32_t unit = segp[seg].unit;
+                    const unsigned peers = __match_any_sync(ball, unit);
+                    if ((unsigned)__ffs(peers) - 1u == lane)
+                        atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
+                }
+            }
+            cur = nxt;
+        }
+        // flush the CTA's staged spikes with one log reservation
+        __syncthreads();
+        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
+        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x)
+            a.spk[log_base + s_base + k] = s_spk[k];
+        if (threadIdx.x == 0) s_nspk = 0;
+
+        // ------------------------------------------------------------ D
+        for (uint32_t j = 0; j < d_mine; ++j, ++g_item) {
+            const uint32_t st = g_item % kStages;
+            mbar_wait(s_bar + st, (g_item / kStages) & 1u);
+            const StageMeta m = s_meta[st];
+            const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
+            const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
+            for (uint32_t e = threadIdx.x; e < m.n; e += blockDim.x) {
+                const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
+                const uint64_t wq = wv[e];
+                if constexpr (PACKED) {
+                    red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
+                            wq, pol_keep);
+                } else {
+                    unsigned long long* dst =
+                        reinterpret_cast<unsigned long long*>(pend_wr) + 4 * (size_t)tid + 2 * cls;
+                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq, pol_keep);
+                    red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
+                }
+            }
+            if (threadIdx.x == 0 && m.first && m.spike != ~0u) {
+                const uint32_t in = __ldg(a.inner + m.spike);
+                my_inner += 2ull * in;
+                my_outer += 2ull * (m.len - in);
+            }
+            __syncthreads();  // stage st drained by every thread
+            if (threadIdx.x == 0 && j + kStages < d_mine) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x, d_C,
+                                    d_prev + d_lo, pol_stream);
+            }
         }
 
+#endif
         grid_barrier(ctl, [&] {
             if (doA) a.seg_end[ph] = ctl->spk_cursor;
             if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
@@ -526,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         __syncthreads();
         if (s_stop) break;
     }
-    if (lane == 0 && (my_inner | my_outer)) {
+    if (my_inner | my_outer) {
         atomicAdd(&ctl->flops_inner, my_inner);
         atomicAdd(&ctl->flops_outer, my_outer);
     }

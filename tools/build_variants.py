@@ -6,10 +6,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2308_01241_b200 import build as b
 
 VARIANTS = {
-    "t512m1b8": {"VXB_THREADS": 512, "VXB_MINB": 1, "VXB_BATCH": 8},
-    "t256m3b8": {"VXB_THREADS": 256, "VXB_MINB": 3, "VXB_BATCH": 8},
-    "t256m3b4": {"VXB_THREADS": 256, "VXB_MINB": 3, "VXB_BATCH": 4},
-    "t512m2b4": {"VXB_THREADS": 512, "VXB_MINB": 2, "VXB_BATCH": 4},
+    "dfirst": {"VXB_DFIRST": 1},
+    "t256m3s6e768": {"VXB_STAGES": 6, "VXB_STAGE_E": 768},
+    "dfirst_s6": {"VXB_DFIRST": 1, "VXB_STAGES": 6},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

@@ -302,8 +302,8 @@ def main():
     ap.add_argument("--bio-ms", type=float, default=100.0)
     ap.add_argument("--dt", type=float, default=1.0)
     ap.add_argument("--device", type=int, default=0)
-    ap.add_argument("--cpu-voxels", type=int, default=8)
-    ap.add_argument("--cpu-steps", type=int, default=100)
+    ap.add_argument("--cpu-voxels", type=int, default=12)
+    ap.add_argument("--cpu-steps", type=int, default=4000)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -210,8 +210,8 @@ constexpr int kMaxSmemSeg = 256;
 #endif
 constexpr int kThreads = VXB_THREADS;
 constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
-#ifndef VXB_DFIRST
-#define VXB_DFIRST 0
+#ifndef VXB_DWARPS
+#define VXB_DWARPS 3
 #endif
 #ifndef VXB_STAGES
 #define VXB_STAGES 4
@@ -406,8 +406,33 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t gthreads = gridDim.x * blockDim.x;
+    // Warp roles: the first VXB_DWARPS warps of every CTA run the delivery
+    // pipeline (bulk copies + atomics, L2-atomic bound) while the others run
+    // the neuron update (HBM bound), so both units are busy on every SM.
+#if VXB_DWARPS > 0
+    constexpr uint32_t kDT = VXB_DWARPS * 32;
+    const bool roleD = threadIdx.x < kDT, roleF = !roleD;
+    const uint32_t f_first = kDT, f_cta = blockDim.x - kDT, d_cta = kDT;
+#else
+    const bool roleD = true, roleF = true;
+    const uint32_t f_first = 0, f_cta = blockDim.x, d_cta = blockDim.x;
+#endif
+    auto fsync = [&] {
+#if VXB_DWARPS > 0
+        asm volatile("bar.sync 1, %0;" ::"r"(f_cta) : "memory");
+#else
+        __syncthreads();
+#endif
+    };
+    auto dsync = [&] {
+#if VXB_DWARPS > 0
+        asm volatile("bar.sync 2, %0;" ::"r"(d_cta) : "memory");
+#else
+        __syncthreads();
+#endif
+    };
+    const uint32_t gtid = blockIdx.x * f_cta + (threadIdx.x - f_first);  // F threads
+    const uint32_t gthreads = gridDim.x * f_cta;
     Control* ctl = a.ctl;
     unsigned long long my_inner = 0, my_outer = 0;
     const uint64_t pol_stream = policy_evict_first();
@@ -451,41 +476,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                                         blockIdx.x + j * gridDim.x, d_C, d_prev + d_lo, pol_stream);
         }
 
-#if VXB_DFIRST
-        // ------------------------------------------------------------ D
-        for (uint32_t j = 0; j < d_mine; ++j, ++g_item) {
-            const uint32_t st = g_item % kStages;
-            mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-            const StageMeta m = s_meta[st];
-            const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
-            const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
-            for (uint32_t e = threadIdx.x; e < m.n; e += blockDim.x) {
-                const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
-                const uint64_t wq = wv[e];
-                if constexpr (PACKED) {
-                    red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
-                            wq, pol_keep);
-                } else {
-                    unsigned long long* dst =
-                        reinterpret_cast<unsigned long long*>(pend_wr) + 4 * (size_t)tid + 2 * cls;
-                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq, pol_keep);
-                    red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
-                }
-            }
-            if (threadIdx.x == 0 && m.first && m.spike != ~0u) {
-                const uint32_t in = __ldg(a.inner + m.spike);
-                my_inner += 2ull * in;
-                my_outer += 2ull * (m.len - in);
-            }
-            __syncthreads();  // stage st drained by every thread
-            if (threadIdx.x == 0 && j + kStages < d_mine) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x, d_C,
-                                    d_prev + d_lo, pol_stream);
-            }
-        }
-
         // ------------------------------------------------------------ F
+        if (roleF) {
         const uint32_t n_round = (a.n + 31u) & ~31u;
         NIn<PACKED> cur, nxt;
         if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
@@ -614,160 +606,24 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             cur = nxt;
         }
         // flush the CTA's staged spikes with one log reservation
-        __syncthreads();
+        fsync();
         const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
-        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
-        __syncthreads();
-        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x)
+        if (threadIdx.x == f_first && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
+        fsync();
+        for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
             a.spk[log_base + s_base + k] = s_spk[k];
-        if (threadIdx.x == 0) s_nspk = 0;
-
-#else
-        // ------------------------------------------------------------ F
-        const uint32_t n_round = (a.n + 31u) & ~31u;
-        NIn<PACKED> cur, nxt;
-        if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
-        for (uint32_t i = gtid; i < n_round; i += gthreads) {
-            const bool live = i < a.n;
-            const uint32_t inext = i + gthreads;
-            if (inext < a.n) load_neuron<PACKED>(a, inext, doE, pend_rd, nxt);
-            bool spiked = false;
-            uint32_t seg = 0;
-            if (live) {
-                seg = find_seg(startp, a.nseg, i);
-                const SegParams& P = segp[seg];
-                uint32_t vb = cur.vb;
-                const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                float4 j = cur.j;
-                float iou = cur.iou;
-                float isyn;
-                if (doE) {
-                    // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
-                    float p0, p1, p2, p3;
-                    if constexpr (PACKED) {
-                        p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
-                        p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
-                        p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
-                        p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
-                        __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
-                    } else {
-                        p0 = dequantize((int64_t)cur.p0.x);
-                        p1 = dequantize((int64_t)cur.p0.y);
-                        p2 = dequantize((int64_t)cur.p1.x);
-                        p3 = dequantize((int64_t)cur.p1.y);
-                        ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
-                        __stcg(q, make_ulonglong2(0ull, 0ull));
-                        __stcg(q + 1, make_ulonglong2(0ull, 0ull));
-                    }
-                    j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
-                    j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
-                    j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
-                    j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
-                    // current_kernel (model.hpp:73-81), u order, from 0.0f
-                    const float4 g = cur.g;
-                    float c = 0.0f;
-                    c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
-                    c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
-                    c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
-                    c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
-                    isyn = c;
-                    // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
-                    float xi = 0.0f;
-                    if (P.sigma_pos) {
-                        const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
-                        xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
-                    }
-                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
-                    if (!doA) a.i_syn[i] = isyn;
-                    a.j[i] = j;
-                    a.i_ou[i] = iou;
-                } else {
-                    isyn = cur.isyn;
-                }
-                if (doA) {
-                    // membrane_kernel + threshold (engine.cpp:363-385)
-                    if (is_refrac(vb)) {
-                        const uint32_t r = (vb & 0x007fffffu) - 1u;
-                        vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
-                    } else {
-                        float inoise = iou;
-                        if (inj_ep) {
-                            const float x =
-                                __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
-                            if (x != 0.0f) inoise = fadd(iou, x);
-                        }
-                        const float nv = fadd(
-                            v, fmul(P.dt_over_c,
-                                    fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
-                        if (!isfinite(nv)) {
-                            atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
-                            vb = __float_as_uint(nv);
-                        } else if (nv >= P.v_th) {
-                            spiked = true;
-                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                        } else {
-                            vb = __float_as_uint(nv);
-                        }
-                    }
-                    // forced spikes (engine.cpp:389-398): join unless already fired
-                    if (f_hi > f_lo && !spiked) {
-                        const uint32_t k =
-                            f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
-                        if (k < f_hi && __ldg(a.forced_local + k) == i) {
-                            spiked = true;
-                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                        }
-                    }
-                    a.v[i] = vb;
-                }
-                // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
-                if (a.n_probes) {
-                    uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
-                    while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
-                        const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
-                        if (doE) a.probe_i[row + ph - 1] = isyn;
-                        if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                        ++k;
-                    }
-                }
-            }
-            // spike staging + rates (engine.cpp:400-404), warp aggregated
-            const unsigned ball = __ballot_sync(0xffffffffu, spiked);
-            if (ball) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (spiked) {
-                    const unsigned rank = __popc(ball & ((1u << lane) - 1u));
-                    if (base + rank < kSpkStage)
-                        s_spk[base + rank] = i;
-                    else  // staging full: straight to the log
-                        a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
-                    const uint32_t unit = segp[seg].unit;
-                    const unsigned peers = __match_any_sync(ball, unit);
-                    if ((unsigned)__ffs(peers) - 1u == lane)
-                        atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
-                }
-            }
-            cur = nxt;
-        }
-        // flush the CTA's staged spikes with one log reservation
-        __syncthreads();
-        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
-        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
-        __syncthreads();
-        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x)
-            a.spk[log_base + s_base + k] = s_spk[k];
-        if (threadIdx.x == 0) s_nspk = 0;
+        if (threadIdx.x == f_first) s_nspk = 0;
+        }  // roleF
 
         // ------------------------------------------------------------ D
+        if (roleD)
         for (uint32_t j = 0; j < d_mine; ++j, ++g_item) {
             const uint32_t st = g_item % kStages;
             mbar_wait(s_bar + st, (g_item / kStages) & 1u);
             const StageMeta m = s_meta[st];
             const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
             const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
-            for (uint32_t e = threadIdx.x; e < m.n; e += blockDim.x) {
+            for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
                 const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
                 const uint64_t wq = wv[e];
                 if constexpr (PACKED) {
@@ -785,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 my_inner += 2ull * in;
                 my_outer += 2ull * (m.len - in);
             }
-            __syncthreads();  // stage st drained by every thread
+            dsync();  // stage st drained by every delivery thread
             if (threadIdx.x == 0 && j + kStages < d_mine) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x, d_C,
@@ -793,7 +649,6 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             }
         }
 
-#endif
         grid_barrier(ctl, [&] {
             if (doA) a.seg_end[ph] = ctl->spk_cursor;
             if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half

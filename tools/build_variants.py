@@ -6,9 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2308_01241_b200 import build as b
 
 VARIANTS = {
-    "dfirst": {"VXB_DFIRST": 1},
-    "t256m3s6e768": {"VXB_STAGES": 6, "VXB_STAGE_E": 768},
-    "dfirst_s6": {"VXB_DFIRST": 1, "VXB_STAGES": 6},
+    "dw3s4e1024": {"VXB_DWARPS": 3, "VXB_STAGES": 4, "VXB_STAGE_E": 1024},
+    "dw3s6e768": {"VXB_DWARPS": 3, "VXB_STAGES": 6, "VXB_STAGE_E": 768},
+    "dw3s3e1536": {"VXB_DWARPS": 3, "VXB_STAGES": 3, "VXB_STAGE_E": 1536},
+    "dw3s2e768": {"VXB_DWARPS": 3, "VXB_STAGES": 2, "VXB_STAGE_E": 768},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

@@ -1,3 +1,3 @@
 # A/B the kernel variants in build/variants on config 2 (after a parity pass)
-timeout 600 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "not acceptance" > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
-for f in build/variants/libvxb_*.so; do v=$(basename $f .so); VXB_LIB=$f timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/ab_$v.log 2>&1; echo -n "$v rc=$? "; python -c "import json;d=json.loads(open('gpurun_out/ab_$v.log').read().strip().splitlines()[-1]);print('%.4g ev/s  %.3f ms/step  frac %.3f  rate %.2f'%(d['value'],d['ms_per_step'],d['roofline']['frac'],d['mean_rate_hz']))"; done
+timeout 600 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "not acceptance" > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_gpu.log
+for f in paper_2308_01241_b200/libvxb.so build/variants/libvxb_*.so; do v=$(basename $f .so); VXB_LIB=$f timeout 300 python tools/decompose.py > gpurun_out/ab_$v.log 2>&1; echo "$v rc=$? $(cat gpurun_out/ab_$v.log | tail -1)"; done

@@ -295,6 +295,29 @@ typedef struct vxb_netspec {
 
 int vxb_create_generated(const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out);
 
+/* ---- one process per GPU ------------------------------------------------
+ * Rank `rank` of `world` holds worker `rank` of a partition with one worker
+ * per rank (PartitionMap.worker_count == world).  Every rank calls the same
+ * sequence: vxb_create_generated_rank, exchange the destination masks
+ * (vxb_mask_out of rank h for shard r goes to rank r's vxb_mask_in(h)),
+ * exchange the receive-region handles (vxb_ipc_handle -> vxb_connect_peers),
+ * then vxb_advance collectively.  Spike ids travel by NVLink P2P stores into
+ * the peers' receive slots (the reference's per-step spike batches,
+ * transport.hpp:13-45); the step barrier is the per-peer step flag.
+ */
+int vxb_create_generated_rank(const vxb_netspec* spec, const vxb_options* opt, uint32_t rank,
+                              uint32_t world, vxb_engine** out);
+/* Bytes of the bitmap over shard h's neurons (bit i: neuron i of shard h has
+ * at least one target on this rank). */
+uint64_t vxb_mask_bytes(const vxb_engine* e, uint32_t h);
+int vxb_mask_out(const vxb_engine* e, uint32_t h, uint8_t* bits, uint64_t cap);
+/* Bitmap received from rank h over this rank's neurons. */
+int vxb_mask_in(vxb_engine* e, uint32_t h, const uint8_t* bits, uint64_t cap);
+/* 64-byte cudaIpcMemHandle_t of this rank's receive region. */
+int vxb_ipc_handle(const vxb_engine* e, void* out, uint64_t cap);
+/* handles: world entries, `stride` bytes apart (own entry ignored). */
+int vxb_connect_peers(vxb_engine* e, const void* handles, uint64_t stride);
+
 /* Export worker `worker`'s WorkerTable as emit_tables would build it (for
  * parity checks on small networks).  Sizes: n_neurons = sum of the worker's
  * unit sizes, n_synapses = sum of neurons * k_in of their voxels. */

@@ -149,7 +149,8 @@ EXPORTS = [
     "vxb_result_d2h_bytes", "vxb_result_launches", "vxb_set_conductances",
     "vxb_membrane_snapshot", "vxb_worker_neurons", "vxb_workers", "vxb_units",
     "vxb_probes", "vxb_run_simulation", "vxb_debug_stream_normal", "vxb_create_generated",
-    "vxb_generate_worker_table",
+    "vxb_generate_worker_table", "vxb_create_generated_rank", "vxb_mask_bytes",
+    "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
 ]
 
 _lib = None
@@ -187,6 +188,13 @@ def _declare(lib):
         "vxb_create_generated": (C.c_int, [P, C.POINTER(Options), C.POINTER(P)]),
         "vxb_generate_worker_table": (C.c_int, [P, C.c_int, C.c_uint16, P, C.c_uint32, P,
                                                 C.c_uint64, P]),
+        "vxb_create_generated_rank": (C.c_int, [P, C.POINTER(Options), C.c_uint32, C.c_uint32,
+                                                C.POINTER(P)]),
+        "vxb_mask_bytes": (C.c_uint64, [P, C.c_uint32]),
+        "vxb_mask_out": (C.c_int, [P, C.c_uint32, P, C.c_uint64]),
+        "vxb_mask_in": (C.c_int, [P, C.c_uint32, P, C.c_uint64]),
+        "vxb_ipc_handle": (C.c_int, [P, P, C.c_uint64]),
+        "vxb_connect_peers": (C.c_int, [P, P, C.c_uint64]),
         "vxb_run_simulation": (C.c_int, [C.POINTER(Network), C.POINTER(Options), C.c_uint32,
                                          C.POINTER(P)]),
     }

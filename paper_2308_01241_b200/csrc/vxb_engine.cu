@@ -100,10 +100,26 @@ struct Engine {
     std::vector<SegParams> segs;
     std::vector<uint32_t> seg_start;
     std::vector<Probe> probes;
+    uint32_t n_probe_dev = 0;  // probes on this device
     std::vector<std::pair<uint32_t, uint32_t>> forced;  // (abs step, shard-local)
     std::vector<vxb_injection> injections;
     bool packed = true;
     uint64_t n_syn = 0;
+    // sharding (one process per GPU): this engine holds worker `rank` of
+    // `world`; world == 1 holds every worker of the tables on one device
+    uint32_t rank = 0, world = 1;
+    uint16_t local_lo = 0, local_hi = 0;  // local worker range
+    std::vector<uint32_t> src_base;       // global source index base per worker
+    uint32_t n_src = 0;
+    int recv_timeout_ms = 30000;
+    DevBuf<Exchange> d_ex;
+    Exchange h_ex{};
+    DevBuf<unsigned char> d_rx;           // receive region (IPC-exported)
+    std::vector<size_t> rx_slot_off;      // my region: byte offset of the slot of shard h
+    std::vector<void*> peer_base;         // IPC-mapped peer regions
+    DevBuf<unsigned long long> d_mask;    // per local neuron: shards with targets
+    std::vector<unsigned long long> h_mask;
+    std::vector<unsigned long long> have_src;  // per global source: workers holding targets here
     uint64_t max_row = 0;
     uint32_t pieces = 1;
     bool use_smem_seg = true;
@@ -155,12 +171,17 @@ struct Engine {
     uint64_t h2d = 0, d2h = 0, launches = 0;
 
     ~Engine() {
+        for (void* p : peer_base)
+            if (p) cudaIpcCloseMemHandle(p);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
     }
 
-    void load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen = nullptr);
+    void load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen = nullptr,
+              uint32_t rank_ = 0, uint32_t world_ = 1);
+    void setup_exchange();
+    bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
     std::vector<unsigned long long> gen_have_mask;  // dst masks of generated tables
@@ -262,11 +283,20 @@ bool same_params(const SegParams& s, const vxb_neuron& r, uint32_t local, uint32
     return std::memcmp(&s, &t, sizeof s) == 0;
 }
 
-void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen) {
+void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen,
+                  uint32_t rank_, uint32_t world_) {
     if (!net || !opt) throw ConfigError("null network or options");
     if (net->n_workers == 0) throw ConfigError("no worker tables");
     if (net->n_workers > 64) throw ConfigError("worker counts above 64 are unsupported");
     workers = (uint16_t)net->n_workers;
+    rank = rank_;
+    world = world_;
+    if (world > 1 && world != workers)
+        throw ConfigError("distributed engines need one worker per rank");
+    if (rank >= world) throw ConfigError("rank out of range");
+    local_lo = world > 1 ? (uint16_t)rank : 0;
+    local_hi = world > 1 ? (uint16_t)(rank + 1) : workers;
+    recv_timeout_ms = opt->recv_timeout_ms;
     n_units = net->n_units;
     n_voxels = net->n_voxels;
     seed = net->workers[0].seed;
@@ -293,12 +323,17 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
 
     // shard-local layout and parameter segments
     wbase.assign(workers + 1, 0);
+    src_base.assign(workers + 1, 0);
     for (uint16_t wi = 0; wi < workers; ++wi) {
         const vxb_worker_table& t = net->workers[wi];
         if (t.worker != wi || t.worker_count != workers)
             throw ConfigError("worker table ids are inconsistent");
-        wbase[wi + 1] = wbase[wi] + t.n_neurons;
+        wbase[wi + 1] = wbase[wi] + (local(wi) ? t.n_neurons : 0u);
+        src_base[wi + 1] = src_base[wi] + t.n_neurons;
     }
+    if ((uint64_t)src_base[workers] >= (1ull << 32))
+        throw ConfigError("global neuron ids exceed 32-bit source addressing");
+    n_src = src_base[workers];
     if ((uint64_t)wbase[workers] >= (1ull << 31))
         throw ConfigError("more than 2^31 neurons on one device");
     n = wbase[workers];
@@ -306,7 +341,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     std::vector<float4> h_g(n);
     std::vector<float> h_iou(n);
     std::vector<unsigned long long> h_mask(n);
-    for (uint16_t wi = 0; wi < workers; ++wi) {
+    for (uint16_t wi = local_lo; wi < local_hi; ++wi) {
         const vxb_worker_table& t = net->workers[wi];
         for (uint32_t i = 0; i < t.n_neurons; ++i) {
             const vxb_neuron& r = t.neurons[i];
@@ -411,30 +446,36 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     for (uint32_t s = 0; s < opt->n_probes; ++s) {
         uint32_t uid;
         const vxb_unit& u = unit_of_gid(opt->probe_gids[s], &uid);
-        const uint32_t loc = wbase[unit_worker[uid]] + unit_local_base[uid] +
-                             (uint32_t)(opt->probe_gids[s] - u.gid_base);
+        const uint32_t loc = local(unit_worker[uid])
+                                 ? wbase[unit_worker[uid]] + unit_local_base[uid] +
+                                       (uint32_t)(opt->probe_gids[s] - u.gid_base)
+                                 : UINT32_MAX;  // recorded by the rank that owns it
         probes.push_back({opt->probe_gids[s], loc});
     }
     for (uint32_t f = 0; f < opt->n_forced; ++f) {
         uint32_t uid;
         const vxb_unit& u = unit_of_gid(opt->forced_spikes[f].gid, &uid);
+        if (!local(unit_worker[uid])) continue;
         const uint32_t loc = wbase[unit_worker[uid]] + unit_local_base[uid] +
                              (uint32_t)(opt->forced_spikes[f].gid - u.gid_base);
         forced.push_back({opt->forced_spikes[f].step, loc});
     }
     std::sort(forced.begin(), forced.end());
     forced.erase(std::unique(forced.begin(), forced.end()), forced.end());
+    n_probe_dev = 0;
     if (!probes.empty()) {
         std::vector<std::pair<uint32_t, uint32_t>> ps;
-        for (uint32_t s = 0; s < probes.size(); ++s) ps.push_back({probes[s].local, s});
+        for (uint32_t s = 0; s < probes.size(); ++s)
+            if (probes[s].local != UINT32_MAX) ps.push_back({probes[s].local, s});
         std::sort(ps.begin(), ps.end());
         std::vector<uint32_t> pl, pslot;
         for (auto& x : ps) {
             pl.push_back(x.first);
             pslot.push_back(x.second);
         }
-        d_probe_local.alloc(pl.size());
-        d_probe_slot.alloc(pslot.size());
+        n_probe_dev = (uint32_t)pl.size();
+        d_probe_local.alloc(std::max<size_t>(1, pl.size()));
+        d_probe_slot.alloc(std::max<size_t>(1, pslot.size()));
         CK(cudaMemcpyAsync(d_probe_local.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice,
                            stream));
         CK(cudaMemcpyAsync(d_probe_slot.p, pslot.data(), 4 * pslot.size(),
@@ -445,13 +486,16 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     const std::string tr = opt->transport ? opt->transport : "queue";
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
+    setup_exchange();
+
     // longest out-row: delivery pieces per spike (<= kStageE entries each)
     {
-        std::vector<uint64_t> off(n + 1);
-        CK(cudaMemcpyAsync(off.data(), d_off.p, 8ull * (n + 1), cudaMemcpyDeviceToHost, stream));
+        std::vector<uint64_t> off((size_t)n_src + 1);
+        CK(cudaMemcpyAsync(off.data(), d_off.p, 8ull * (n_src + 1), cudaMemcpyDeviceToHost,
+                           stream));
         CK(cudaStreamSynchronize(stream));
         uint64_t mx = 0;
-        for (uint32_t i = 0; i < n; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);
+        for (uint32_t i = 0; i < n_src; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);
         max_row = mx;
         pieces = (uint32_t)std::max<uint64_t>(1, (mx + kStageE - 1) / kStageE);
     }
@@ -482,7 +526,7 @@ void Engine::build_csr(const vxb_network* net) {
     d_wn.alloc(workers);
     std::vector<uint32_t> wn(workers);
     for (uint16_t w = 0; w < workers; ++w) wn[w] = net->workers[w].n_neurons;
-    CK(cudaMemcpyAsync(d_wbase.p, wbase.data(), 4ull * workers, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_wbase.p, src_base.data(), 4ull * workers, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_wn.p, wn.data(), 4ull * workers, cudaMemcpyHostToDevice, stream));
     DevBuf<unsigned int> flags;  // [0] bad source, [1] needs wide accumulators
     flags.alloc(2);
@@ -577,7 +621,9 @@ struct GenHost {
     uint64_t total_neurons = 0;
 };
 
-void build_gen_host(const vxb_netspec& s, GenHost& h) {
+// local_worker >= 0: draw the neuron records of that worker only (one
+// process per GPU); the other workers contribute their sizes.
+void build_gen_host(const vxb_netspec& s, GenHost& h, int local_worker = -1) {
     if (s.n_workers == 0) throw ConfigError("partition with zero workers");
     if (s.n_workers > 64)
         throw ConfigError("worker count exceeds the routing mask limit of 64");
@@ -694,6 +740,8 @@ void build_gen_host(const vxb_netspec& s, GenHost& h) {
         const vxb_gen_population& p = s.unit_pops[u];
         const uint16_t w = s.unit_worker[u];
         const uint32_t k_in = s.voxels[x.voxel].k_in;
+        h.nsyn[w] += (uint64_t)x.neurons * k_in;
+        if (local_worker >= 0 && w != (uint32_t)local_worker) continue;
         std::array<uint64_t, 4> gbase;
         for (int r = 0; r < 4; ++r)  // sample_conductances (netgen.cpp:318-329), salt 0
             gbase[r] = mix_key(mix_key(mix_key(mix_key(s.seed, 7), 0), u), (uint64_t)r);
@@ -727,7 +775,6 @@ void build_gen_host(const vxb_netspec& s, GenHost& h) {
             r.v_init = (float)((double)p.v_reset + u01 * (double)span);
             h.recs[w].push_back(r);
         }
-        h.nsyn[w] += (uint64_t)x.neurons * k_in;
     }
     h.tables.resize(s.n_workers);
     for (uint32_t w = 0; w < s.n_workers; ++w) {
@@ -735,10 +782,10 @@ void build_gen_host(const vxb_netspec& s, GenHost& h) {
         std::memset(&t, 0, sizeof t);
         t.worker = (uint16_t)w;
         t.worker_count = (uint16_t)s.n_workers;
-        t.n_neurons = (uint32_t)h.recs[w].size();
+        t.n_neurons = fill[w];
         t.seed = s.seed;
         t.n_synapses = h.nsyn[w];
-        t.neurons = h.recs[w].data();
+        t.neurons = h.recs[w].empty() ? nullptr : h.recs[w].data();
     }
     h.net.n_workers = s.n_workers;
     h.net.n_units = U;
@@ -805,48 +852,113 @@ thread_local GenHost* g_gen_host = nullptr;
 void Engine::generate_csr(const vxb_netspec& spec) {
     GenHost& h = *g_gen_host;
     GenDevTables T;
-    std::vector<uint32_t> wb(wbase.begin(), wbase.end() - 1);
-    T.upload(h, spec, wb, stream);
+    // target units of this device, in shard-local order
+    std::vector<std::pair<uint32_t, uint32_t>> tu;  // (shard base, unit)
+    for (uint32_t u = 0; u < spec.n_units; ++u)
+        if (local(spec.unit_worker[u]) && spec.units[u].neurons)
+            tu.push_back({wbase[spec.unit_worker[u]] + h.unit_local_base[u], u});
+    std::sort(tu.begin(), tu.end());
+    std::vector<uint32_t> t_base, t_unit;
+    for (auto& x : tu) {
+        t_base.push_back(x.first);
+        t_unit.push_back(x.second);
+    }
+    std::vector<uint32_t> sb(src_base.begin(), src_base.end() - 1);
+    T.upload(h, spec, sb, stream);
+    DevBuf<uint32_t> d_tb, d_tu;
+    d_tb.alloc(std::max<size_t>(1, t_base.size()));
+    d_tu.alloc(std::max<size_t>(1, t_unit.size()));
+    if (!t_base.empty()) {
+        CK(cudaMemcpyAsync(d_tb.p, t_base.data(), 4 * t_base.size(), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_tu.p, t_unit.data(), 4 * t_unit.size(), cudaMemcpyHostToDevice, stream));
+    }
+    T.G.t_base = d_tb.p;
+    T.G.t_unit = d_tu.p;
+    T.G.n_t = (uint32_t)t_base.size();
     n_syn = 0;
-    for (uint64_t x : h.nsyn) n_syn += x;
+    for (uint32_t w = local_lo; w < local_hi; ++w) n_syn += h.nsyn[w];
     DevBuf<unsigned long long> cnt;
-    cnt.alloc((size_t)n + 1);
+    cnt.alloc((size_t)n_src + 1);
     cnt.zero(stream);
     const int blocks = 148 * 8, threads = 256;
-    if (h.total_neurons)
-        gen_kernel<0><<<blocks, threads, 0, stream>>>(T.G, 0, h.total_neurons, cnt.p + 1,
-                                                      nullptr, nullptr, nullptr, nullptr, 0,
-                                                      nullptr, nullptr);
+    if (n)
+        gen_kernel<0><<<blocks, threads, 0, stream>>>(T.G, 0, n, cnt.p + 1, nullptr, nullptr,
+                                                      nullptr, nullptr, 0, nullptr, nullptr);
     CK(cudaGetLastError());
     T.check(stream, nullptr);
-    d_off.alloc((size_t)n + 1);
+    d_off.alloc((size_t)n_src + 1);
     {
         size_t tmp = 0;
         CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.p + 1,
-                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n_src,
                                          stream));
         DevBuf<unsigned char> t;
         t.alloc(tmp ? tmp : 1);
         CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cnt.p + 1,
-                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n,
+                                         reinterpret_cast<unsigned long long*>(d_off.p) + 1, n_src,
                                          stream));
         CK(cudaMemsetAsync(d_off.p, 0, 8, stream));
     }
-    CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemcpyAsync(cnt.p, d_off.p, 8ull * n_src, cudaMemcpyDeviceToDevice, stream));
     d_tgt.alloc(n_syn + 4);
     d_w.alloc(n_syn + 2);
-    d_inner.alloc(n);
+    d_inner.alloc(std::max<uint32_t>(1, n_src));
     d_inner.zero(stream);
-    d_keys.alloc(n);  // have_mask
+    d_keys.alloc(std::max<uint32_t>(1, n_src));  // have_mask per global source
     d_keys.zero(stream);
-    if (h.total_neurons)
+    if (n)
         gen_kernel<1><<<blocks, threads, 0, stream>>>(
-            T.G, 0, h.total_neurons, cnt.p, d_tgt.p, d_w.p,
-            reinterpret_cast<unsigned long long*>(d_keys.p), d_inner.p, 0, nullptr, nullptr);
+            T.G, 0, n, cnt.p, d_tgt.p, d_w.p, reinterpret_cast<unsigned long long*>(d_keys.p),
+            d_inner.p, 0, nullptr, nullptr);
     CK(cudaGetLastError());
     unsigned int wide = 0;
     T.check(stream, &wide);
     packed = wide == 0;
+    have_src.assign(n_src, 0);
+    if (n_src)
+        CK(cudaMemcpyAsync(have_src.data(), d_keys.p, 8ull * n_src, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+}
+
+// Exchange state: receive region (one slot per peer: ids[2][n_h], counts,
+// flag), per-neuron destination masks, device control block.
+void Engine::setup_exchange() {
+    std::memset(&h_ex, 0, sizeof h_ex);
+    h_ex.rank = rank;
+    h_ex.world = world;
+    h_ex.cap_self = world > 1 ? src_base[rank + 1] - src_base[rank] : 0;
+    h_ex.timeout_ns = recv_timeout_ms > 0 ? (unsigned long long)recv_timeout_ms * 1000000ull : 0;
+    for (uint32_t w = 0; w <= workers && w <= (uint32_t)kMaxShards; ++w)
+        h_ex.src_base[w] = world > 1 ? src_base[w] : 0u;
+    if (world > 1) {
+        rx_slot_off.assign(world, 0);
+        size_t off = 0;
+        for (uint32_t hh = 0; hh < world; ++hh) {
+            h_ex.cap[hh] = src_base[hh + 1] - src_base[hh];
+            rx_slot_off[hh] = off;
+            if (hh != rank) off += ((8ull * h_ex.cap[hh] + 15) & ~15ull) + 16;
+        }
+        d_rx.alloc(std::max<size_t>(16, off));
+        d_rx.zero(stream);
+        for (uint32_t hh = 0; hh < world; ++hh) {
+            if (hh == rank) continue;
+            unsigned char* b = d_rx.p + rx_slot_off[hh];
+            h_ex.rx_ids[hh] = reinterpret_cast<uint32_t*>(b);
+            h_ex.rx_meta[hh] = reinterpret_cast<uint32_t*>(b + ((8ull * h_ex.cap[hh] + 15) & ~15ull));
+        }
+        peer_base.assign(world, nullptr);
+    }
+    // own bit: local neurons with targets on this rank
+    h_mask.assign(n, 0);
+    if (!have_src.empty())
+        for (uint32_t i = 0; i < n; ++i)
+            h_mask[i] = have_src[src_base[local_lo] + i] ? (1ull << rank) : 0ull;
+    d_mask.alloc(std::max<uint32_t>(1, n));
+    d_mask.zero(stream);
+    if (n) CK(cudaMemcpyAsync(d_mask.p, h_mask.data(), 8ull * n, cudaMemcpyHostToDevice, stream));
+    d_ex.alloc(1);
+    CK(cudaMemcpyAsync(d_ex.p, &h_ex, sizeof h_ex, cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
 }
 
 struct Chunk {
@@ -1040,7 +1152,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.spk = d_spk.p;
     a.seg_end = d_seg_end.p;
     a.rates = d_rates.p;
-    a.n_probes = (uint32_t)probes.size();
+    a.n_probes = n_probe_dev;
     a.probe_local = d_probe_local.p;
     a.probe_slot = d_probe_slot.p;
     a.probe_v = d_probe_v.p;
@@ -1054,6 +1166,9 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.n_voxels = n_voxels;
     a.phase_ns = d_phase_ns.p;
     a.ctl = d_ctl.p;
+    a.ex = d_ex.p;
+    a.world = world;
+    a.dst_mask = d_mask.p;
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
@@ -1079,6 +1194,15 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
     device_ms += ms;
     d2h += sizeof c + 4 * rr.size() + 4ull * (steps + 1);
+    if (world > 1) {
+        uint32_t to[2] = {0, 0};
+        CK(cudaMemcpy(to, &d_ex.p->timeout, 8, cudaMemcpyDeviceToHost));
+        if (to[0]) {
+            failed = true;
+            throw SimError(fmt("step barrier timed out on worker %u at step %u (no batch from "
+                               "worker %u)", rank, to[1], to[0] - 1));
+        }
+    }
     if (c.err != ~0ull) {
         failed = true;
         const uint32_t step = (uint32_t)(c.err >> 32), loc = (uint32_t)(c.err & 0xffffffffu);
@@ -1237,7 +1361,7 @@ int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float
         for (uint32_t i = 0; i < n; ++i)
             if (!(values[i] >= 0.0f) || !std::isfinite(values[i]))
                 throw ConfigError("conductance values must be finite and >= 0");
-        if (n == 0) return VXB_OK;
+        if (n == 0 || !g.local(g.unit_worker[unit])) return VXB_OK;  // owned by another rank
         CK(cudaSetDevice(g.device));
         const uint32_t base = g.wbase[g.unit_worker[unit]] + g.unit_local_base[unit];
         std::vector<float4> buf(n);
@@ -1302,6 +1426,104 @@ int vxb_create_generated(const vxb_netspec* spec, const vxb_options* opt, vxb_en
     }
     *out = e;
     return VXB_OK;
+}
+
+int vxb_create_generated_rank(const vxb_netspec* spec, const vxb_options* opt, uint32_t rank,
+                               uint32_t world, vxb_engine** out) {
+    *out = nullptr;
+    auto* e = new vxb_engine();
+    try {
+        if (!spec) throw ConfigError("null network spec");
+        if (world == 0 || rank >= world) throw ConfigError("rank out of range");
+        if (spec->n_workers != world)
+            throw ConfigError("distributed engines need one worker per rank");
+        GenHost h;
+        build_gen_host(*spec, h, world > 1 ? (int)rank : -1);
+        g_gen_host = &h;
+        e->eng.load(&h.net, opt, spec, rank, world);
+        g_gen_host = nullptr;
+    } catch (const std::exception& x) {
+        g_gen_host = nullptr;
+        g_create_error = x.what();
+        int rc = fail_code(x);
+        delete e;
+        return rc;
+    }
+    *out = e;
+    return VXB_OK;
+}
+
+uint64_t vxb_mask_bytes(const vxb_engine* e, uint32_t h) {
+    const Engine& g = e->eng;
+    if (h >= g.workers) return 0;
+    return (g.src_base[h + 1] - g.src_base[h] + 7) / 8;
+}
+
+int vxb_mask_out(const vxb_engine* e, uint32_t h, uint8_t* bits, uint64_t cap) {
+    const Engine& g = e->eng;
+    if (h >= g.workers || cap < vxb_mask_bytes(e, h)) return VXB_ECONFIG;
+    const uint32_t b = g.src_base[h], n = g.src_base[h + 1] - b;
+    std::memset(bits, 0, (n + 7) / 8);
+    if (!g.have_src.empty())
+        for (uint32_t i = 0; i < n; ++i)
+            if (g.have_src[b + i]) bits[i >> 3] |= (uint8_t)(1u << (i & 7));
+    return VXB_OK;
+}
+
+int vxb_mask_in(vxb_engine* e, uint32_t h, const uint8_t* bits, uint64_t cap) {
+    Engine& g = e->eng;
+    try {
+        if (h >= g.workers || h >= 64) throw ConfigError("shard out of range");
+        if (cap < (g.n + 7) / 8) throw ConfigError("mask buffer too small");
+        for (uint32_t i = 0; i < g.n; ++i)
+            if ((bits[i >> 3] >> (i & 7)) & 1u) g.h_mask[i] |= 1ull << h;
+        CK(cudaSetDevice(g.device));
+        if (g.n)
+            CK(cudaMemcpy(g.d_mask.p, g.h_mask.data(), 8ull * g.n, cudaMemcpyHostToDevice));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
+}
+
+int vxb_ipc_handle(const vxb_engine* e, void* out, uint64_t cap) {
+    const Engine& g = e->eng;
+    if (cap < sizeof(cudaIpcMemHandle_t) || g.world < 2 || !g.d_rx.p) return VXB_ECONFIG;
+    cudaSetDevice(g.device);
+    cudaIpcMemHandle_t hd;
+    if (cudaIpcGetMemHandle(&hd, g.d_rx.p) != cudaSuccess) return VXB_ESIM;
+    std::memcpy(out, &hd, sizeof hd);
+    return VXB_OK;
+}
+
+int vxb_connect_peers(vxb_engine* e, const void* handles, uint64_t stride) {
+    Engine& g = e->eng;
+    try {
+        if (g.world < 2) return VXB_OK;
+        CK(cudaSetDevice(g.device));
+        for (uint32_t d = 0; d < g.world; ++d) {
+            if (d == g.rank) continue;
+            cudaIpcMemHandle_t hd;
+            std::memcpy(&hd, static_cast<const unsigned char*>(handles) + stride * d, sizeof hd);
+            void* base = nullptr;
+            CK(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+            g.peer_base[d] = base;
+            // peer d's region: slots of every shard but d, in shard order
+            size_t off = 0;
+            for (uint32_t hh = 0; hh < g.rank; ++hh)
+                if (hh != d) off += ((8ull * g.h_ex.cap[hh] + 15) & ~15ull) + 16;
+            unsigned char* slot = static_cast<unsigned char*>(base) + off;
+            g.h_ex.tx_ids[d] = reinterpret_cast<uint32_t*>(slot);
+            g.h_ex.tx_meta[d] = reinterpret_cast<uint32_t*>(
+                slot + ((8ull * g.h_ex.cap[g.rank] + 15) & ~15ull));
+        }
+        CK(cudaMemcpy(g.d_ex.p, &g.h_ex, sizeof g.h_ex, cudaMemcpyHostToDevice));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
 }
 
 int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t worker,

@@ -66,6 +66,27 @@ struct Control {
     unsigned int pad[6];
 };
 
+// Device-side state of the per-step spike-id exchange between ranks (one
+// process per GPU).  Receive slots live in this rank's IPC-exported region,
+// send slots are this rank's slots inside the peers' regions (NVLink P2P).
+constexpr int kMaxShards = 64;  // dst masks are 64-bit (partition.hpp:35)
+struct Exchange {
+    uint32_t rank, world;
+    uint32_t cap_self;                    // ids per parity in my slots (= my neurons)
+    uint32_t timeout;                     // peer + 1 whose batch never arrived, 0 = none
+    uint32_t timeout_step;
+    uint32_t send_done[2];                // CTAs done sending, per step parity
+    uint32_t pad0;
+    unsigned long long timeout_ns;
+    uint32_t src_base[kMaxShards + 1];    // global source index base per shard
+    uint32_t cap[kMaxShards];             // neurons of shard h
+    uint32_t send_cnt[2][kMaxShards];     // ids queued per (parity, destination)
+    uint32_t* rx_ids[kMaxShards];         // [2 * cap[h]] from source shard h
+    uint32_t* rx_meta[kMaxShards];        // counts[2], flag (= step + 1)
+    uint32_t* tx_ids[kMaxShards];         // my slot in peer d
+    uint32_t* tx_meta[kMaxShards];
+};
+
 struct StepArgs {
     // sizes
     uint32_t n;             // shard neurons
@@ -116,6 +137,9 @@ struct StepArgs {
     uint32_t has_inj;
     unsigned long long* phase_ns; // [steps + 2] globaltimer at phase ends
     Control* ctl;
+    Exchange* ex;
+    uint32_t world;
+    const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {
@@ -136,6 +160,16 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
 
 __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Sense-counting grid barrier for a cooperative launch.  The last CTA to
@@ -314,11 +348,12 @@ __device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint6
 template <bool PACKED>
 __device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* smem,
                                             const SmemLayout& L, uint32_t st, uint32_t item,
-                                            uint32_t C, uint32_t spk_base, uint64_t pol) {
+                                            uint32_t C, const uint32_t* ids, uint32_t src_base,
+                                            uint64_t pol) {
     StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta) + st;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
     const uint32_t k = item / C, c = item - k * C;
-    const uint32_t s = __ldcg(a.spk + spk_base + k);
+    const uint32_t s = src_base + __ldcg(ids + k);
     const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
     const uint64_t len = e1 - e0;
     const uint64_t b0 = e0 + len * c / C, b1 = e0 + len * (c + 1) / C;
@@ -342,6 +377,71 @@ __device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* sm
     mbar_expect_tx(bar, tb + wb);
     bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
     bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
+}
+
+// Send S(tE) to the peers (engine.cpp:416-437 routing + transport send):
+// the delivery threads of every CTA filter a slice of the local spike list by
+// destination mask and store the ids straight into the peers' receive slots
+// over NVLink; the last CTA to finish publishes the counts and the step flag
+// (system-scope release).  An empty batch still publishes its flag: it is
+// the reference's step barrier (engine.cpp:468-524).
+template <typename Sync>
+__device__ __forceinline__ void exchange_send(const StepArgs& a, uint32_t tE, const uint32_t* ids,
+                                              uint32_t cnt, uint32_t par, uint32_t d_cta,
+                                              Sync dsync) {
+    Exchange* ex = a.ex;
+    const uint32_t lane = threadIdx.x & 31, world = ex->world, me = ex->rank;
+    const uint32_t stride = gridDim.x * d_cta, cnt_round = (cnt + 31u) & ~31u;
+    for (uint32_t k = blockIdx.x * d_cta + threadIdx.x; k < cnt_round; k += stride) {
+        uint32_t s = 0;
+        unsigned long long m = 0;
+        if (k < cnt) {
+            s = __ldcg(ids + k);
+            m = a.dst_mask[s] & ~(1ull << me);
+        }
+        for (uint32_t d = 0; d < world; ++d) {
+            const bool want = (m >> d) & 1ull;
+            const unsigned ball = __ballot_sync(0xffffffffu, want);
+            if (!ball) continue;
+            const int lead = __ffs(ball) - 1;
+            unsigned base = 0;
+            if ((int)lane == lead) base = atomicAdd(&ex->send_cnt[par][d], (unsigned)__popc(ball));
+            base = __shfl_sync(0xffffffffu, base, lead);
+            if (want)
+                ex->tx_ids[d][par * ex->cap_self + base + __popc(ball & ((1u << lane) - 1u))] = s;
+        }
+    }
+    __threadfence_system();
+    dsync();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(&ex->send_done[par], 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            for (uint32_t d = 0; d < world; ++d)
+                if (d != me) ex->tx_meta[d][par] = atomicExch(&ex->send_cnt[par][d], 0u);
+            __threadfence_system();
+            for (uint32_t d = 0; d < world; ++d)
+                if (d != me) st_release_sys(ex->tx_meta[d] + 2, tE + 1);
+            atomicExch(&ex->send_done[par], 0u);
+        }
+    }
+}
+
+// Wait for peer h's batch of step tE (receiver side of the step barrier);
+// returns its id count.  recv_timeout_ms maps to a device-side timeout.
+__device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h, uint32_t tE,
+                                                 uint32_t par) {
+    Exchange* ex = a.ex;
+    const uint32_t* meta = ex->rx_meta[h];
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(meta + 2) < tE + 1) {
+        if (ex->timeout_ns && globaltimer() - t0 > ex->timeout_ns) {
+            if (atomicCAS(&ex->timeout, 0u, h + 1) == 0u) ex->timeout_step = tE;
+            return 0;
+        }
+        __nanosleep(64);
+    }
+    return ld_acquire_sys(meta + par);
 }
 
 // Per-neuron state the fused update reads (prefetched one neuron ahead).
@@ -384,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
     StageMeta* s_meta = reinterpret_cast<StageMeta*>(smem + L.meta);
     __shared__ uint32_t s_nspk;
+    __shared__ uint32_t s_rcnt;
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
 
@@ -459,21 +560,13 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
 
         // D work of this phase: pieces of the rows of S(tE), dealt to CTAs
-        // round-robin; the first kStages pieces start streaming into shared
-        // memory now, under the neuron update.
-        uint32_t d_lo = 0, d_cnt = 0, d_C = 1, d_mine = 0, d_prev = 0;
+        // round-robin (local spikes, then every peer's batch).
+        uint32_t d_lo = 0, d_cnt = 0, d_C = 1, d_prev = 0;
         if (doE) {
             d_lo = (ph >= 2 && !a.ring) ? __ldcg(a.seg_end + ph - 2) : 0u;
             d_cnt = __ldcg(a.seg_end + ph - 1) - d_lo;
             d_prev = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
             d_C = a.pieces;
-            const uint32_t items = d_cnt * d_C;
-            d_mine = items > blockIdx.x ? (items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-            if (threadIdx.x == 0 && d_mine) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (threadIdx.x == 0)
-                for (uint32_t j = 0; j < d_mine && j < (uint32_t)kStages; ++j)
-                    issue_piece<PACKED>(a, smem, L, (g_item + j) % kStages,
-                                        blockIdx.x + j * gridDim.x, d_C, d_prev + d_lo, pol_stream);
         }
 
         // ------------------------------------------------------------ F
@@ -616,36 +709,61 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         }  // roleF
 
         // ------------------------------------------------------------ D
-        if (roleD)
-        for (uint32_t j = 0; j < d_mine; ++j, ++g_item) {
-            const uint32_t st = g_item % kStages;
-            mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-            const StageMeta m = s_meta[st];
-            const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
-            const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
-            for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
-                const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
-                const uint64_t wq = wv[e];
-                if constexpr (PACKED) {
-                    red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
-                            wq, pol_keep);
-                } else {
-                    unsigned long long* dst =
-                        reinterpret_cast<unsigned long long*>(pend_wr) + 4 * (size_t)tid + 2 * cls;
-                    red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq, pol_keep);
-                    red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
+        if (roleD && doE) {
+            const uint32_t tpar = tE & 1u;
+            const uint32_t* local_ids = a.spk + d_prev + d_lo;
+            if (a.world > 1) exchange_send(a, tE, local_ids, d_cnt, tpar, d_cta, dsync);
+            for (uint32_t li = 0; li < a.world; ++li) {
+                const uint32_t h = (a.ex->rank + li) % a.world;
+                const uint32_t* ids = local_ids;
+                uint32_t cnt = d_cnt;
+                if (li) {
+                    if (threadIdx.x == 0) s_rcnt = exchange_wait(a, h, tE, tpar);
+                    dsync();
+                    cnt = s_rcnt;
+                    ids = a.ex->rx_ids[h] + tpar * a.ex->cap[h];
                 }
-            }
-            if (threadIdx.x == 0 && m.first && m.spike != ~0u) {
-                const uint32_t in = __ldg(a.inner + m.spike);
-                my_inner += 2ull * in;
-                my_outer += 2ull * (m.len - in);
-            }
-            dsync();  // stage st drained by every delivery thread
-            if (threadIdx.x == 0 && j + kStages < d_mine) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x, d_C,
-                                    d_prev + d_lo, pol_stream);
+                const uint32_t sb = a.ex->src_base[h];
+                const uint32_t items = cnt * d_C;
+                const uint32_t mine =
+                    items > blockIdx.x ? (items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+                if (threadIdx.x == 0 && mine) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    for (uint32_t j = 0; j < mine && j < (uint32_t)kStages; ++j)
+                        issue_piece<PACKED>(a, smem, L, (g_item + j) % kStages,
+                                            blockIdx.x + j * gridDim.x, d_C, ids, sb, pol_stream);
+                }
+                for (uint32_t j = 0; j < mine; ++j, ++g_item) {
+                    const uint32_t st = g_item % kStages;
+                    mbar_wait(s_bar + st, (g_item / kStages) & 1u);
+                    const StageMeta m = s_meta[st];
+                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
+                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
+                    for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
+                        const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
+                        const uint64_t wq = wv[e];
+                        if constexpr (PACKED) {
+                            red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
+                                    wq, pol_keep);
+                        } else {
+                            unsigned long long* dst =
+                                reinterpret_cast<unsigned long long*>(pend_wr) + 4 * (size_t)tid + 2 * cls;
+                            red_add(dst, (uint64_t)(int64_t)(int32_t)(uint32_t)wq, pol_keep);
+                            red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
+                        }
+                    }
+                    if (threadIdx.x == 0 && m.first) {
+                        const uint32_t in = __ldg(a.inner + m.spike);
+                        my_inner += 2ull * in;
+                        my_outer += 2ull * (m.len - in);
+                    }
+                    dsync();  // stage st drained by every delivery thread
+                    if (threadIdx.x == 0 && j + kStages < mine) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x,
+                                            d_C, ids, sb, pol_stream);
+                    }
+                }
             }
         }
 
@@ -654,7 +772,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
             a.phase_ns[ph + 1] = globaltimer();
         });
-        if (threadIdx.x == 0) s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull;  // L2-coherent
+        if (threadIdx.x == 0)  // L2-coherent reads
+            s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
         __syncthreads();
         if (s_stop) break;
     }

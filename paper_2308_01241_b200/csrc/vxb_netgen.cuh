@@ -45,7 +45,10 @@ struct GenDev {
     const uint32_t* e_src;
     const uint64_t* e_nexc;
     const double* pc;
-    const uint32_t* wbase;   // shard-local base per worker
+    const uint32_t* wbase;   // source index base per worker (global over all workers)
+    const uint32_t* t_unit;  // target units of this shard, sorted by t_base
+    const uint32_t* t_base;  // first target index of each target unit
+    uint32_t n_t;
     unsigned int* err;       // 1 = self-redraw exhausted (netgen.cpp:151-154)
     unsigned int* wide;      // 1 = a row's Q16 sums need the int64 pending layout
 };
@@ -172,13 +175,30 @@ __global__ void gen_kernel(GenDev G, uint64_t gid_lo, uint64_t gid_hi,
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t gid = gid_lo + warp; gid < gid_hi; gid += nwarps) {
-        const uint32_t u = gen_unit_of_gid(G, gid);
+    for (uint64_t it = gid_lo + warp; it < gid_hi; it += nwarps) {
+        // modes 0/1 walk this shard's targets (index = shard-local target),
+        // mode 2 walks every gid of the layout
+        uint32_t u;
+        uint64_t gid;
+        uint32_t t_idx;
+        if (MODE == 2) {
+            gid = it;
+            u = gen_unit_of_gid(G, gid);
+            t_idx = 0;
+        } else {
+            uint32_t lo = 0, hi = G.n_t;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (G.t_base[mid] <= (uint32_t)it) lo = mid; else hi = mid;
+            }
+            u = G.t_unit[lo];
+            gid = G.units[u].gid_base + (it - G.t_base[lo]);
+            t_idx = (uint32_t)it;
+        }
         const GenUnit& U = G.units[u];
         const GenVoxel V = G.voxels[U.voxel];
         const uint64_t kv = mix_key(G.kv_root, gid), kn = mix_key(G.kn_root, gid),
                        kp = mix_key(G.kp_root, gid), kw = mix_key(G.kw_root, gid);
-        const uint32_t t_idx = shard_index(G, u, gid);
         const bool mine = MODE == 2 && U.worker == only_worker;
         long long sf = 0, ss = 0;
         for (uint32_t k = lane; k < V.k_in; k += 32) {

@@ -1011,3 +1011,71 @@ def generate_tables(net: BuiltNetwork, device: int = 0) -> NetworkTables:
         workers.append(WorkerTable(w, net.workers, net.cfg["seed"], neurons, syn, rb))
     return NetworkTables(workers, net.arrays["unit_worker"].copy(), ulb, net.arrays["units"].copy(),
                          len(net.layout.voxels))
+
+
+# ----------------------------------------------------------- one rank per GPU
+def exchange_masks(local_bitmaps, rank: int, world: int, all_gather):
+    """All-to-all of destination-mask bitmaps.
+
+    local_bitmaps[h] = this rank's bitmap over shard h's neurons (bit i: neuron
+    i of shard h has a target here).  Returns, for every h != rank, the bitmap
+    rank h built over *this* rank's neurons.  `all_gather(obj) -> list` is the
+    host collective (torch.distributed gloo in production, a stub in tests).
+    """
+    gathered = all_gather(local_bitmaps)
+    return {h: gathered[h][rank] for h in range(world) if h != rank}
+
+
+class DistributedSimInstance(SimInstance):
+    """SimInstance for one rank of a one-process-per-GPU run: rank r holds
+    worker r of the partition (netgen.build_network(cfg, workers=world)).
+    Every method is collective over the ranks, like the reference's workers
+    stepping in lockstep (engine.cpp:662-709)."""
+
+    def __init__(self, net: BuiltNetwork, options: SimOptions, rank: int, world: int,
+                 all_gather=None, barrier=None):
+        if net.workers != world:
+            raise ConfigError("distributed engines need one worker per rank")
+        if all_gather is None or barrier is None:
+            import torch.distributed as dist
+
+            def all_gather(obj):
+                out = [None] * world
+                dist.all_gather_object(out, obj)
+                return out
+            barrier = dist.barrier
+        self._lib = lib = _abi.load_library()
+        self._opt = options
+        self._units = net.arrays["units"].copy()
+        self._n_voxels = len(net.layout.voxels)
+        self.rank, self.world = rank, world
+        spec = net.spec()
+        opt, keep = options._descriptor()
+        h = C.c_void_p()
+        rc = lib.vxb_create_generated_rank(C.byref(spec), C.byref(opt), rank, world, C.byref(h))
+        del keep
+        if rc != 0:
+            from .engine import _raise
+            _raise(rc, lib.vxb_last_error(None).decode())
+        self._h = h
+        if world > 1:
+            bitmaps = []
+            for d in range(world):
+                nb = int(lib.vxb_mask_bytes(h, d))
+                b = np.zeros(max(nb, 1), np.uint8)
+                lib.vxb_mask_out(h, d, ptr(b), b.size)
+                bitmaps.append(b[:nb].tobytes())
+            for d, bits in exchange_masks(bitmaps, rank, world, all_gather).items():
+                arr = np.frombuffer(bits, np.uint8).copy() if bits else np.zeros(1, np.uint8)
+                rc = lib.vxb_mask_in(h, d, ptr(arr), arr.size)
+                if rc:
+                    self._err(rc)
+            hd = (C.c_ubyte * 64)()
+            if lib.vxb_ipc_handle(h, C.cast(hd, C.c_void_p), 64) != 0:
+                raise SimError("cannot export the receive region (CUDA IPC)")
+            handles = all_gather(bytes(hd))
+            buf = np.frombuffer(b"".join(handles), np.uint8).copy()
+            rc = lib.vxb_connect_peers(h, ptr(buf), 64)
+            if rc:
+                self._err(rc)
+            barrier()

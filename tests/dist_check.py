@@ -1,0 +1,92 @@
+"""Multi-GPU parity check, run under torchrun (one process per GPU):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_check.py [cfg-json]
+
+Every rank runs its worker of an N-worker partition on its own GPU with the
+NVLink spike exchange; rank 0 gathers the raster, rates, probes and final
+membrane state and compares them with the reference engine (oracle/_ref) on
+the same network and partition, bit for bit.  Prints one JSON line.
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2308_01241_b200 import netgen  # noqa: E402
+from paper_2308_01241_b200.engine import SimOptions  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    cfg = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {
+        "seed": 1401, "dt_ms": 1.0, "steps": 300, "workers": world,
+        "connectome": {"kind": "ring", "voxels": 12, "neurons_per_voxel": 2000},
+        "partition": {"method": "greedy"},
+        "regions": {"subcortex": {"k_in": 100, "ou_mean": 300.0}}}
+    cfg["workers"] = world
+    steps = cfg["steps"]
+    net = netgen.build_network(cfg)
+    probes = [17, 5000, net.total_neurons - 1]
+    opt = SimOptions(steps=steps, dt_ms=cfg["dt_ms"], probe_gids=probes, device=local)
+    sim = netgen.DistributedSimInstance(net, opt, rank, world)
+    r1 = sim.advance(steps // 3)
+    r2 = sim.advance(steps - steps // 3)
+    snap = sim.membrane_snapshot(rank)
+    w_gids = None
+    mine = {
+        "raster": sorted(zip(r1.raster["step"].tolist() + r2.raster["step"].tolist(),
+                             r1.raster["gid"].tolist() + r2.raster["gid"].tolist())),
+        "rates": np.concatenate([r1.rates.counts, r2.rates.counts], axis=1),
+        "pv": np.concatenate([np.stack([p.v for p in r.probes]) for r in (r1, r2)], axis=1),
+        "pi": np.concatenate([np.stack([p.i_syn for p in r.probes]) for r in (r1, r2)], axis=1),
+        "flops": {k: r1.flops[k] + r2.flops[k] for k in r1.flops},
+        "snap": snap,
+    }
+    out = [None] * world
+    dist.all_gather_object(out, mine)
+    sim.close()
+    if rank == 0:
+        from refnet import RefNet, RefSim
+        ref_net = RefNet(cfg)
+        rs = RefSim(ref_net, SimOptions(steps=steps, dt_ms=cfg["dt_ms"], probe_gids=probes))
+        a, b = rs.advance(steps // 3), rs.advance(steps - steps // 3)
+        ref_raster = sorted(zip(a.raster["step"].tolist() + b.raster["step"].tolist(),
+                                a.raster["gid"].tolist() + b.raster["gid"].tolist()))
+        raster = sorted(x for o in out for x in o["raster"])
+        rates = sum(o["rates"] for o in out)
+        # a probe is recorded by the rank that owns its neuron (zeros elsewhere)
+        pv = sum(o["pv"] for o in out)
+        pi = sum(o["pi"] for o in out)
+        ref_pv = np.concatenate([a.probe_v, b.probe_v], axis=1)
+        ref_pi = np.concatenate([a.probe_i, b.probe_i], axis=1)
+        fl = {k: sum(o["flops"][k] for o in out) for k in out[0]["flops"]}
+        ref_fl = {k: a.flops[k] + b.flops[k] for k in a.flops}
+        snaps_ok = all(np.array_equal(out[w]["snap"], rs.membrane_snapshot(w)) for w in range(world))
+        res = {
+            "world": world, "spikes": len(raster), "ref_spikes": len(ref_raster),
+            "raster_equal": raster == ref_raster,
+            "rates_equal": bool(np.array_equal(rates, np.concatenate([a.rates, b.rates], axis=1))),
+            "probe_v_equal": bool(np.array_equal(pv, ref_pv)),
+            "probe_i_equal": bool(np.array_equal(pi, ref_pi)),
+            "flops_equal": fl == ref_fl, "snapshots_equal": snaps_ok,
+            "gating_outer": fl["gating_outer"],
+        }
+        res["pass"] = all(v for k, v in res.items() if k.endswith("_equal")) and res["spikes"] > 0
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -198,11 +198,18 @@ def run_b200(args):
 
     dev = local if ws > 1 else args.device
     bio_steps = int(round(args.bio_ms / args.dt))
-    cfg = workload_cfg(dt_ms=args.dt)
+    # weak scaling: 100 voxels x 10 000 neurons per GPU, one worker per rank,
+    # contiguous voxel blocks (sequential partition of the ring)
+    cfg = workload_cfg(voxels=100 * ws, dt_ms=args.dt, workers=ws)
+    if ws > 1:
+        cfg["partition"]["method"] = "sequential"
     net = netgen.build_network(cfg)
     opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=True,
                      device=dev)
-    sim = netgen.GeneratedSimInstance(net, opt)
+    if ws > 1:
+        sim = netgen.DistributedSimInstance(net, opt, rank, ws)
+    else:
+        sim = netgen.GeneratedSimInstance(net, opt)
     for _ in range(args.warmup):
         sim.advance(bio_steps)
 
@@ -211,6 +218,7 @@ def run_b200(args):
             dist.barrier()
 
     dev_ms, wall, events, spikes, h2d, d2h, launches, results = [], [], 0, 0, 0, 0, 0, []
+    xwait = 0.0
     with ClockSampler(dev) as clk:
         barrier()
         t_all = time.perf_counter()
@@ -224,6 +232,7 @@ def run_b200(args):
             h2d += r.h2d_bytes
             d2h += r.d2h_bytes
             launches += r.launches
+            xwait += r.exchange_wait_ms
         barrier()
         t_all = time.perf_counter() - t_all
     sim.close()
@@ -232,21 +241,21 @@ def run_b200(args):
     # max over ranks of time, sum of work
     if dist:
         import torch
-        t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
+        t = torch.tensor([dev_s, wall_s, xwait], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s, wall_s = float(t[0]), float(t[1])
+        dev_s, wall_s, xwait = float(t[0]), float(t[1]), float(t[2])
         e = torch.tensor([events, spikes], dtype=torch.float64)
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
         events, spikes = int(e[0]), int(e[1])
     if rank != 0:
         return
-    n = net.total_neurons * ws
+    n = net.total_neurons
     bio_s = args.steps * bio_steps * args.dt * 1e-3
     value = events / dev_s
     rate = spikes / (n * bio_s)
-    # roofline of the step kernel: algorithmic bytes
+    # roofline of the step kernel: algorithmic bytes, per GPU
     neuron_steps = n * args.steps * bio_steps
-    alg_bytes = 98 * neuron_steps + 12 * events + 20 * spikes
+    alg_bytes = (98 * neuron_steps + 12 * events + 20 * spikes) / ws
     peak, peak_kind = measured_peak_hbm()
     achieved = alg_bytes / dev_s / 1e9
     launches_per = max(1, launches // max(1, args.steps * ws))
@@ -256,12 +265,15 @@ def run_b200(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 state / i64 Q16 / f64 noise", "data": "synthetic",
-        "config": {"workload": "config2", "neurons_per_gpu": net.total_neurons,
-                   "synapses_per_gpu": net.synapse_count, "k_in": 1000, "dt_ms": args.dt,
+        "config": {"workload": "config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)",
+                   "neurons_per_gpu": net.total_neurons // ws,
+                   "synapses_per_gpu": net.synapse_count // ws, "k_in": 1000, "dt_ms": args.dt,
                    "bio_ms_per_step": args.bio_ms, "seed": SEED,
-                   "parallelism": "replica" if ws > 1 else "single",
+                   "parallelism": f"neuron shards x{ws}, NVLink spike exchange" if ws > 1
+                   else "single",
                    "l2": "inputs larger than L2 (12 GB synapse table)"},
         "wall_s_per_bio_s": dev_s / bio_s,
+        "exposed_exchange_us_per_step": 1e3 * xwait / (args.steps * bio_steps) if ws > 1 else 0.0,
         "mean_rate_hz": rate,
         "events_per_s_per_gpu": value / ws,
         "e2e": {"value": events / wall_s, "unit": "events/s",
@@ -273,6 +285,7 @@ def run_b200(args):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "vxb::step_kernel",
                      "alg_bytes_per_launch": alg_bytes / max(1, launches_per * args.steps),
+                     "exchange": "4 B per (spike, destination GPU) over NVLink" if ws > 1 else None,
                      "model": "98 B/neuron-step + 12 B/event + 20 B/delivered spike"},
         "clocks": clk.summary(),
     }

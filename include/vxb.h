@@ -219,6 +219,9 @@ int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap)
 /* Device time of the last advance's step kernel(s), milliseconds (CUDA
  * events on the launching stream; max over shards). */
 double vxb_result_device_ms(const vxb_engine* e);
+/* Exposed spike-exchange wait of the last advance: sum over steps of the
+ * longest time any CTA waited for a peer's batch, milliseconds. */
+double vxb_result_exchange_wait_ms(const vxb_engine* e);
 /* Bytes copied host->device / device->host by the last vxb_advance. */
 uint64_t vxb_result_h2d_bytes(const vxb_engine* e);
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e);

@@ -149,6 +149,8 @@ struct Engine {
     DevBuf<uint32_t> d_inj_epoch;
     DevBuf<float> d_inj_table;
     DevBuf<unsigned long long> d_phase_ns;
+    DevBuf<unsigned long long> d_phase_wait;
+    double exchange_wait_ms = 0;  // last advance: sum over phases of the max CTA wait
     DevBuf<Control> d_ctl;
     DevBuf<uint64_t> d_keys, d_keys_sorted;
     DevBuf<unsigned char> d_cub_tmp;
@@ -1050,6 +1052,8 @@ void Engine::advance(uint32_t steps) {
     d_seg_end.alloc(chunk + 2);
     d_rates.alloc((size_t)n_units * chunk);
     d_phase_ns.alloc(chunk + 2);
+    d_phase_wait.alloc(chunk + 2);
+    exchange_wait_ms = 0;
 
     std::vector<unsigned long long> phase_ns_all;
     phase_ns_all.reserve(steps + 2);
@@ -1169,6 +1173,8 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.ex = d_ex.p;
     a.world = world;
     a.dst_mask = d_mask.p;
+    a.phase_wait = d_phase_wait.p;
+    d_phase_wait.zero(stream);
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
@@ -1189,6 +1195,13 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     std::vector<uint32_t> seg_end(steps + 1);
     CK(cudaMemcpyAsync(seg_end.data(), d_seg_end.p, 4ull * (steps + 1), cudaMemcpyDeviceToHost,
                        stream));
+    if (world > 1) {
+        std::vector<unsigned long long> pw(steps + 2);
+        CK(cudaMemcpyAsync(pw.data(), d_phase_wait.p, 8ull * (steps + 2), cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaStreamSynchronize(stream));
+        for (auto x : pw) exchange_wait_ms += x * 1e-6;
+    }
     CK(cudaStreamSynchronize(stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -1346,6 +1359,7 @@ int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap)
 }
 
 double vxb_result_device_ms(const vxb_engine* e) { return e->eng.device_ms; }
+double vxb_result_exchange_wait_ms(const vxb_engine* e) { return e->eng.exchange_wait_ms; }
 uint64_t vxb_result_h2d_bytes(const vxb_engine* e) { return e->eng.h2d; }
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e) { return e->eng.d2h; }
 uint64_t vxb_result_launches(const vxb_engine* e) { return e->eng.launches; }

@@ -139,6 +139,7 @@ struct StepArgs {
     Control* ctl;
     Exchange* ex;
     uint32_t world;
+    unsigned long long* phase_wait;  // per phase: max over CTAs of the exchange wait (ns)
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -174,8 +175,8 @@ __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) 
 
 // Sense-counting grid barrier for a cooperative launch.  The last CTA to
 // arrive runs `hook` (bookkeeping for the next phase) before releasing.
-template <typename Hook>
-__device__ __forceinline__ void grid_barrier(Control* ctl, Hook hook) {
+template <typename Hook, typename Post>
+__device__ __forceinline__ void grid_barrier(Control* ctl, Hook hook, Post post) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned int gen = ld_acquire(&ctl->bar_gen);
@@ -186,6 +187,7 @@ __device__ __forceinline__ void grid_barrier(Control* ctl, Hook hook) {
             hook();
             __threadfence();
             st_release(&ctl->bar_gen, gen + 1);
+            post();  // after the release: off the critical path of the grid
         } else {
             while (ld_acquire(&ctl->bar_gen) == gen) __nanosleep(40);
         }
@@ -379,52 +381,47 @@ __device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* sm
     bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
 }
 
-// Send S(tE) to the peers (engine.cpp:416-437 routing + transport send):
-// the delivery threads of every CTA filter a slice of the local spike list by
-// destination mask and store the ids straight into the peers' receive slots
-// over NVLink; the last CTA to finish publishes the counts and the step flag
-// (system-scope release).  An empty batch still publishes its flag: it is
-// the reference's step barrier (engine.cpp:468-524).
-template <typename Sync>
-__device__ __forceinline__ void exchange_send(const StepArgs& a, uint32_t tE, const uint32_t* ids,
-                                              uint32_t cnt, uint32_t par, uint32_t d_cta,
-                                              Sync dsync) {
+// Routing of one warp's spikes to the peers (engine.cpp:416-437 + transport
+// send): ids go straight into the peers' receive slots over NVLink P2P
+// stores, positions reserved per destination with one atomic per warp and
+// destination.  Called by the neuron-update warps when they flush their
+// staged spikes; the counts and the step flag are published once per phase
+// by exchange_publish.  Returns true if this thread stored anything remote.
+__device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bool valid,
+                                               uint32_t par) {
     Exchange* ex = a.ex;
     const uint32_t lane = threadIdx.x & 31, world = ex->world, me = ex->rank;
-    const uint32_t stride = gridDim.x * d_cta, cnt_round = (cnt + 31u) & ~31u;
-    for (uint32_t k = blockIdx.x * d_cta + threadIdx.x; k < cnt_round; k += stride) {
-        uint32_t s = 0;
-        unsigned long long m = 0;
-        if (k < cnt) {
-            s = __ldcg(ids + k);
-            m = a.dst_mask[s] & ~(1ull << me);
-        }
-        for (uint32_t d = 0; d < world; ++d) {
-            const bool want = (m >> d) & 1ull;
-            const unsigned ball = __ballot_sync(0xffffffffu, want);
-            if (!ball) continue;
-            const int lead = __ffs(ball) - 1;
-            unsigned base = 0;
-            if ((int)lane == lead) base = atomicAdd(&ex->send_cnt[par][d], (unsigned)__popc(ball));
-            base = __shfl_sync(0xffffffffu, base, lead);
-            if (want)
-                ex->tx_ids[d][par * ex->cap_self + base + __popc(ball & ((1u << lane) - 1u))] = s;
+    const unsigned long long m = valid ? (a.dst_mask[s] & ~(1ull << me)) : 0ull;
+    bool sent = false;
+    for (uint32_t d = 0; d < world; ++d) {
+        const bool want = (m >> d) & 1ull;
+        const unsigned ball = __ballot_sync(0xffffffffu, want);
+        if (!ball) continue;
+        const int lead = __ffs(ball) - 1;
+        unsigned base = 0;
+        if ((int)lane == lead) base = atomicAdd(&ex->send_cnt[par][d], (unsigned)__popc(ball));
+        base = __shfl_sync(0xffffffffu, base, lead);
+        if (want) {
+            ex->tx_ids[d][par * ex->cap_self + base + __popc(ball & ((1u << lane) - 1u))] = s;
+            sent = true;
         }
     }
+    return sent;
+}
+
+// Publish the batch of step t to every peer: counts, then the step flag
+// with system-scope release.  An empty batch still publishes its flag: it is
+// the reference's step barrier (engine.cpp:468-524).  Run by one thread after
+// every CTA's routing is complete (the grid barrier's last arriver).
+__device__ __forceinline__ void exchange_publish(const StepArgs& a, uint32_t t) {
+    Exchange* ex = a.ex;
+    const uint32_t par = t & 1u, world = ex->world, me = ex->rank;
     __threadfence_system();
-    dsync();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(&ex->send_done[par], 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence();
-            for (uint32_t d = 0; d < world; ++d)
-                if (d != me) ex->tx_meta[d][par] = atomicExch(&ex->send_cnt[par][d], 0u);
-            __threadfence_system();
-            for (uint32_t d = 0; d < world; ++d)
-                if (d != me) st_release_sys(ex->tx_meta[d] + 2, tE + 1);
-            atomicExch(&ex->send_done[par], 0u);
-        }
-    }
+    for (uint32_t d = 0; d < world; ++d)
+        if (d != me) ex->tx_meta[d][par] = atomicExch(&ex->send_cnt[par][d], 0u);
+    __threadfence_system();
+    for (uint32_t d = 0; d < world; ++d)
+        if (d != me) st_release_sys(ex->tx_meta[d] + 2, t + 1);
 }
 
 // Wait for peer h's batch of step tE (receiver side of the step barrier);
@@ -679,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 }
             }
             // spike staging + rates (engine.cpp:400-404), warp aggregated
+            bool overflow_route = false;
             const unsigned ball = __ballot_sync(0xffffffffu, spiked);
             if (ball) {
                 unsigned base = 0;
@@ -688,14 +686,18 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                     const unsigned rank = __popc(ball & ((1u << lane) - 1u));
                     if (base + rank < kSpkStage)
                         s_spk[base + rank] = i;
-                    else  // staging full: straight to the log
+                    else {  // staging full: straight to the log (and to the peers)
                         a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                        if (a.world > 1) overflow_route = true;
+                    }
                     const uint32_t unit = segp[seg].unit;
                     const unsigned peers = __match_any_sync(ball, unit);
                     if ((unsigned)__ffs(peers) - 1u == lane)
                         atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
                 }
             }
+            if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
+                if (exchange_route(a, i, overflow_route, tA & 1u)) __threadfence_system();
             cur = nxt;
         }
         // flush the CTA's staged spikes with one log reservation
@@ -705,20 +707,31 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         fsync();
         for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
             a.spk[log_base + s_base + k] = s_spk[k];
+        if (a.world > 1 && doA) {
+            bool sent = false;
+            const uint32_t nr = (nst + 31u) & ~31u;
+            for (uint32_t k = threadIdx.x - f_first; k < nr; k += f_cta)
+                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA & 1u);
+            if (sent) __threadfence_system();
+        }
         if (threadIdx.x == f_first) s_nspk = 0;
         }  // roleF
 
         // ------------------------------------------------------------ D
+        unsigned long long wait_ns = 0;
         if (roleD && doE) {
             const uint32_t tpar = tE & 1u;
             const uint32_t* local_ids = a.spk + d_prev + d_lo;
-            if (a.world > 1) exchange_send(a, tE, local_ids, d_cnt, tpar, d_cta, dsync);
             for (uint32_t li = 0; li < a.world; ++li) {
                 const uint32_t h = (a.ex->rank + li) % a.world;
                 const uint32_t* ids = local_ids;
                 uint32_t cnt = d_cnt;
                 if (li) {
-                    if (threadIdx.x == 0) s_rcnt = exchange_wait(a, h, tE, tpar);
+                    if (threadIdx.x == 0) {
+                        const unsigned long long w0 = globaltimer();
+                        s_rcnt = exchange_wait(a, h, tE, tpar);
+                        wait_ns += globaltimer() - w0;
+                    }
                     dsync();
                     cnt = s_rcnt;
                     ids = a.ex->rx_ids[h] + tpar * a.ex->cap[h];
@@ -767,11 +780,17 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             }
         }
 
-        grid_barrier(ctl, [&] {
-            if (doA) a.seg_end[ph] = ctl->spk_cursor;
-            if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
-            a.phase_ns[ph + 1] = globaltimer();
-        });
+        if (threadIdx.x == 0 && wait_ns && a.phase_wait) atomicMax(a.phase_wait + ph, wait_ns);
+        grid_barrier(
+            ctl,
+            [&] {
+                if (doA) a.seg_end[ph] = ctl->spk_cursor;
+                if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
+                a.phase_ns[ph + 1] = globaltimer();
+            },
+            [&] {
+                if (a.world > 1 && doA) exchange_publish(a, tA);
+            });
         if (threadIdx.x == 0)  // L2-coherent reads
             s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
         __syncthreads();

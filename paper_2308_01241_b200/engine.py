@@ -179,6 +179,7 @@ class RunResult:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     launches: int = 0
+    exchange_wait_ms: float = 0.0
 
     @property
     def events(self) -> int:
@@ -264,7 +265,8 @@ class SimInstance:
         return RunResult(raster, timings, probes, rates, flops,
                          int(L.vxb_result_total_spikes(h)), steps,
                          float(L.vxb_result_device_ms(h)), int(L.vxb_result_h2d_bytes(h)),
-                         int(L.vxb_result_d2h_bytes(h)), int(L.vxb_result_launches(h)))
+                         int(L.vxb_result_d2h_bytes(h)), int(L.vxb_result_launches(h)),
+                         float(L.vxb_result_exchange_wait_ms(h)))
 
     def set_conductances(self, unit: int, receptor: int, values) -> None:
         v = np.ascontiguousarray(values, dtype=np.float32)

@@ -938,7 +938,7 @@ void Engine::setup_exchange() {
         for (uint32_t hh = 0; hh < world; ++hh) {
             h_ex.cap[hh] = src_base[hh + 1] - src_base[hh];
             rx_slot_off[hh] = off;
-            if (hh != rank) off += ((8ull * h_ex.cap[hh] + 15) & ~15ull) + 16;
+            if (hh != rank) off += ((12ull * h_ex.cap[hh] + 15) & ~15ull) + 16;
         }
         d_rx.alloc(std::max<size_t>(16, off));
         d_rx.zero(stream);
@@ -946,7 +946,7 @@ void Engine::setup_exchange() {
             if (hh == rank) continue;
             unsigned char* b = d_rx.p + rx_slot_off[hh];
             h_ex.rx_ids[hh] = reinterpret_cast<uint32_t*>(b);
-            h_ex.rx_meta[hh] = reinterpret_cast<uint32_t*>(b + ((8ull * h_ex.cap[hh] + 15) & ~15ull));
+            h_ex.rx_meta[hh] = reinterpret_cast<uint32_t*>(b + ((12ull * h_ex.cap[hh] + 15) & ~15ull));
         }
         peer_base.assign(world, nullptr);
     }
@@ -1526,11 +1526,11 @@ int vxb_connect_peers(vxb_engine* e, const void* handles, uint64_t stride) {
             // peer d's region: slots of every shard but d, in shard order
             size_t off = 0;
             for (uint32_t hh = 0; hh < g.rank; ++hh)
-                if (hh != d) off += ((8ull * g.h_ex.cap[hh] + 15) & ~15ull) + 16;
+                if (hh != d) off += ((12ull * g.h_ex.cap[hh] + 15) & ~15ull) + 16;
             unsigned char* slot = static_cast<unsigned char*>(base) + off;
             g.h_ex.tx_ids[d] = reinterpret_cast<uint32_t*>(slot);
             g.h_ex.tx_meta[d] = reinterpret_cast<uint32_t*>(
-                slot + ((8ull * g.h_ex.cap[g.rank] + 15) & ~15ull));
+                slot + ((12ull * g.h_ex.cap[g.rank] + 15) & ~15ull));
         }
         CK(cudaMemcpy(g.d_ex.p, &g.h_ex, sizeof g.h_ex, cudaMemcpyHostToDevice));
         return VXB_OK;

@@ -75,14 +75,15 @@ struct Exchange {
     uint32_t cap_self;                    // ids per parity in my slots (= my neurons)
     uint32_t timeout;                     // peer + 1 whose batch never arrived, 0 = none
     uint32_t timeout_step;
-    uint32_t send_done[2];                // CTAs done sending, per step parity
-    uint32_t pad0;
+    uint32_t pad0[3];
     unsigned long long timeout_ns;
     uint32_t src_base[kMaxShards + 1];    // global source index base per shard
     uint32_t cap[kMaxShards];             // neurons of shard h
-    uint32_t send_cnt[2][kMaxShards];     // ids queued per (parity, destination)
-    uint32_t* rx_ids[kMaxShards];         // [2 * cap[h]] from source shard h
-    uint32_t* rx_meta[kMaxShards];        // counts[2], flag (= step + 1)
+    // Batches are triple-buffered by step (slot = step % 3): a sender may run
+    // one phase ahead of a receiver still reading the batch of two steps ago.
+    uint32_t send_cnt[3][kMaxShards];     // ids queued per (slot, destination)
+    uint32_t* rx_ids[kMaxShards];         // [3 * cap[h]] from source shard h
+    uint32_t* rx_meta[kMaxShards];        // counts[3], flag (= step + 1)
     uint32_t* tx_ids[kMaxShards];         // my slot in peer d
     uint32_t* tx_meta[kMaxShards];
 };
@@ -388,7 +389,7 @@ __device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* sm
 // staged spikes; the counts and the step flag are published once per phase
 // by exchange_publish.  Returns true if this thread stored anything remote.
 __device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bool valid,
-                                               uint32_t par) {
+                                               uint32_t slot) {
     Exchange* ex = a.ex;
     const uint32_t lane = threadIdx.x & 31, world = ex->world, me = ex->rank;
     const unsigned long long m = valid ? (a.dst_mask[s] & ~(1ull << me)) : 0ull;
@@ -399,10 +400,10 @@ __device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bo
         if (!ball) continue;
         const int lead = __ffs(ball) - 1;
         unsigned base = 0;
-        if ((int)lane == lead) base = atomicAdd(&ex->send_cnt[par][d], (unsigned)__popc(ball));
+        if ((int)lane == lead) base = atomicAdd(&ex->send_cnt[slot][d], (unsigned)__popc(ball));
         base = __shfl_sync(0xffffffffu, base, lead);
         if (want) {
-            ex->tx_ids[d][par * ex->cap_self + base + __popc(ball & ((1u << lane) - 1u))] = s;
+            ex->tx_ids[d][slot * ex->cap_self + base + __popc(ball & ((1u << lane) - 1u))] = s;
             sent = true;
         }
     }
@@ -415,30 +416,30 @@ __device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bo
 // every CTA's routing is complete (the grid barrier's last arriver).
 __device__ __forceinline__ void exchange_publish(const StepArgs& a, uint32_t t) {
     Exchange* ex = a.ex;
-    const uint32_t par = t & 1u, world = ex->world, me = ex->rank;
+    const uint32_t slot = t % 3u, world = ex->world, me = ex->rank;
     __threadfence_system();
     for (uint32_t d = 0; d < world; ++d)
-        if (d != me) ex->tx_meta[d][par] = atomicExch(&ex->send_cnt[par][d], 0u);
+        if (d != me) ex->tx_meta[d][slot] = atomicExch(&ex->send_cnt[slot][d], 0u);
     __threadfence_system();
     for (uint32_t d = 0; d < world; ++d)
-        if (d != me) st_release_sys(ex->tx_meta[d] + 2, t + 1);
+        if (d != me) st_release_sys(ex->tx_meta[d] + 3, t + 1);
 }
 
 // Wait for peer h's batch of step tE (receiver side of the step barrier);
 // returns its id count.  recv_timeout_ms maps to a device-side timeout.
 __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h, uint32_t tE,
-                                                 uint32_t par) {
+                                                 uint32_t slot) {
     Exchange* ex = a.ex;
     const uint32_t* meta = ex->rx_meta[h];
     const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(meta + 2) < tE + 1) {
+    while (ld_acquire_sys(meta + 3) < tE + 1) {
         if (ex->timeout_ns && globaltimer() - t0 > ex->timeout_ns) {
             if (atomicCAS(&ex->timeout, 0u, h + 1) == 0u) ex->timeout_step = tE;
             return 0;
         }
         __nanosleep(64);
     }
-    return ld_acquire_sys(meta + par);
+    return ld_acquire_sys(meta + slot);
 }
 
 // Per-neuron state the fused update reads (prefetched one neuron ahead).
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 }
             }
             if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
-                if (exchange_route(a, i, overflow_route, tA & 1u)) __threadfence_system();
+                if (exchange_route(a, i, overflow_route, tA % 3u)) __threadfence_system();
             cur = nxt;
         }
         // flush the CTA's staged spikes with one log reservation
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             bool sent = false;
             const uint32_t nr = (nst + 31u) & ~31u;
             for (uint32_t k = threadIdx.x - f_first; k < nr; k += f_cta)
-                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA & 1u);
+                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % 3u);
             if (sent) __threadfence_system();
         }
         if (threadIdx.x == f_first) s_nspk = 0;
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         // ------------------------------------------------------------ D
         unsigned long long wait_ns = 0;
         if (roleD && doE) {
-            const uint32_t tpar = tE & 1u;
+            const uint32_t tslot = tE % 3u;
             const uint32_t* local_ids = a.spk + d_prev + d_lo;
             for (uint32_t li = 0; li < a.world; ++li) {
                 const uint32_t h = (a.ex->rank + li) % a.world;
@@ -729,12 +730,12 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 if (li) {
                     if (threadIdx.x == 0) {
                         const unsigned long long w0 = globaltimer();
-                        s_rcnt = exchange_wait(a, h, tE, tpar);
+                        s_rcnt = exchange_wait(a, h, tE, tslot);
                         wait_ns += globaltimer() - w0;
                     }
                     dsync();
                     cnt = s_rcnt;
-                    ids = a.ex->rx_ids[h] + tpar * a.ex->cap[h];
+                    ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
                 }
                 const uint32_t sb = a.ex->src_base[h];
                 const uint32_t items = cnt * d_C;

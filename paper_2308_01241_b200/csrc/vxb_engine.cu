@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -28,6 +29,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "vxb.h"
 #include "vxb_kernels.cuh"
@@ -183,6 +185,13 @@ struct Engine {
     void load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen = nullptr,
               uint32_t rank_ = 0, uint32_t world_ = 1);
     void setup_exchange();
+    void build_tiles();
+    // tiled delivery tables (world == 1)
+    bool tiled = false;
+    uint32_t n_tiles = 0;
+    uint64_t q_total = 0;
+    DevBuf<uint32_t> d_dir_off, d_qcount;
+    DevBuf<uint64_t> d_dir, d_qbase, d_queue;
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
@@ -489,6 +498,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
     setup_exchange();
+    build_tiles();
 
     // longest out-row: delivery pieces per spike (<= kStageE entries each)
     {
@@ -503,7 +513,8 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     }
     // cooperative grid
     use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg;
-    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u).total;
+    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u,
+                            tiled ? kTile * (packed ? 16u : 32u) : 0u).total;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const void* kfn = packed ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
@@ -963,6 +974,91 @@ void Engine::setup_exchange() {
     CK(cudaStreamSynchronize(stream));
 }
 
+// Tiled delivery (single device): sort every out-row by target, build the
+// per-source tile directory and the per-tile segment queues.  Used when the
+// network has locality (few segments per row); otherwise the engine keeps the
+// L2-atomic delivery.  VXB_TILED=0 disables it.
+void Engine::build_tiles() {
+    tiled = false;
+    const char* env = std::getenv("VXB_TILED");
+    if (env && std::string(env) == "0") return;
+    if (world != 1 || n_syn == 0 || n_syn >= (1ull << 31) || n < (uint32_t)kTile ||
+        n_src != n)
+        return;
+    n_tiles = (n + kTile - 1) / kTile;
+    if (n_tiles >= (1u << 20)) return;
+    // 1. sort rows by target (low bits only: the class bit rides along)
+    {
+        int end_bit = 1;
+        while ((1ull << end_bit) < n) ++end_bit;
+        DevBuf<uint32_t> t2;
+        DevBuf<uint64_t> w2;
+        t2.alloc(n_syn + 4);
+        w2.alloc(n_syn + 2);
+        CK(cudaMemsetAsync(t2.p + n_syn, 0, 16, stream));
+        CK(cudaMemsetAsync(w2.p + n_syn, 0, 16, stream));
+        const unsigned long long* ob = reinterpret_cast<const unsigned long long*>(d_off.p);
+        size_t tmp = 0;
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_tgt.p, t2.p, d_w.p, w2.p,
+                                                    (int)n_syn, (int)n_src, ob, ob + 1, 0,
+                                                    end_bit, stream));
+        DevBuf<unsigned char> t;
+        t.alloc(tmp ? tmp : 1);
+        CK(cub::DeviceSegmentedRadixSort::SortPairs(t.p, tmp, d_tgt.p, t2.p, d_w.p, w2.p,
+                                                    (int)n_syn, (int)n_src, ob, ob + 1, 0,
+                                                    end_bit, stream));
+        std::swap(d_tgt.p, t2.p);
+        std::swap(d_tgt.n, t2.n);
+        std::swap(d_w.p, w2.p);
+        std::swap(d_w.n, w2.n);
+    }
+    // 2. segments per source and per tile
+    DevBuf<uint32_t> nseg, cap;
+    nseg.alloc((size_t)n_src + 1);
+    cap.alloc(n_tiles + 1);
+    nseg.zero(stream);
+    cap.zero(stream);
+    tile_dir_count_kernel<<<1184, 256, 0, stream>>>(
+        reinterpret_cast<const uint64_t*>(d_off.p), d_tgt.p, n_src, nseg.p, cap.p);
+    CK(cudaGetLastError());
+    d_dir_off.alloc((size_t)n_src + 1);
+    DevBuf<unsigned long long> qb64;
+    qb64.alloc(n_tiles + 1);
+    {
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg.p, d_dir_off.p, n_src + 1, stream));
+        DevBuf<unsigned char> t;
+        t.alloc(tmp ? tmp : 1);
+        CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, nseg.p, d_dir_off.p, n_src + 1, stream));
+        // per-tile capacities -> queue bases (u64)
+        std::vector<uint32_t> hc(n_tiles);
+        CK(cudaMemcpyAsync(hc.data(), cap.p, 4ull * n_tiles, cudaMemcpyDeviceToHost, stream));
+        uint32_t total_seg = 0;
+        CK(cudaMemcpyAsync(&total_seg, d_dir_off.p + n_src, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        // locality test: segments must carry enough entries to pay for queueing
+        if ((uint64_t)total_seg * 8 > n_syn) {
+            d_dir_off.release();
+            return;
+        }
+        std::vector<uint64_t> qb(n_tiles + 1, 0);
+        for (uint32_t i = 0; i < n_tiles; ++i) qb[i + 1] = qb[i] + hc[i];
+        q_total = qb[n_tiles];
+        d_qbase.alloc(n_tiles + 1);
+        CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 8ull * (n_tiles + 1), cudaMemcpyHostToDevice,
+                           stream));
+        d_dir.alloc(std::max<uint64_t>(1, total_seg));
+    }
+    tile_dir_fill_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
+                                                   d_tgt.p, n_src, d_dir_off.p, d_dir.p);
+    CK(cudaGetLastError());
+    d_qcount.alloc(2ull * n_tiles);
+    d_qcount.zero(stream);
+    d_queue.alloc(std::max<uint64_t>(1, 2 * q_total));
+    CK(cudaStreamSynchronize(stream));
+    tiled = true;
+}
+
 struct Chunk {
     uint32_t t0, rel0, steps;
 };
@@ -1175,6 +1271,15 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.dst_mask = d_mask.p;
     a.phase_wait = d_phase_wait.p;
     d_phase_wait.zero(stream);
+    a.tiled = tiled ? 1u : 0u;
+    a.n_tiles = n_tiles;
+    a.acc_bytes = tiled ? kTile * (packed ? 16u : 32u) : 0u;
+    a.dir_off = d_dir_off.p;
+    a.dir = d_dir.p;
+    a.qbase = d_qbase.p;
+    a.qcount = d_qcount.p;
+    a.queue = d_queue.p;
+    a.q_total = q_total;
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));

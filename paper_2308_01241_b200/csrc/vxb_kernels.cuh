@@ -141,6 +141,16 @@ struct StepArgs {
     Exchange* ex;
     uint32_t world;
     unsigned long long* phase_wait;  // per phase: max over CTAs of the exchange wait (ns)
+    // tiled delivery (rows sorted by target tile, per-source tile directory)
+    uint32_t tiled;
+    uint32_t n_tiles;
+    uint32_t acc_bytes;
+    const uint32_t* dir_off;   // per source: first directory entry
+    const uint64_t* dir;       // start_rel << 32 | tile << 12 | (len - 1)
+    const uint64_t* qbase;     // per tile: first queue slot
+    uint32_t* qcount;          // [2][n_tiles] segments queued per (step parity, tile)
+    uint64_t* queue;           // [2][q_total] start | (len - 1) << 40
+    uint64_t q_total;
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -256,6 +266,11 @@ constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
 #ifndef VXB_STAGE_E
 #define VXB_STAGE_E 768
 #endif
+#ifndef VXB_TILE_LOG
+#define VXB_TILE_LOG 11
+#endif
+constexpr int kTileLog = VXB_TILE_LOG;  // tiled delivery: neurons per tile = 2^kTileLog
+constexpr int kTile = 1 << kTileLog;
 constexpr int kStages = VXB_STAGES;   // delivery pipeline depth (bulk copies in flight)
 constexpr int kStageE = VXB_STAGE_E;  // synapse entries per stage
 constexpr int kStageTgtBytes = (kStageE + 8) * 4;
@@ -272,9 +287,11 @@ struct StageMeta {
 
 // Dynamic shared memory carve-up of step_kernel.
 struct SmemLayout {
-    uint32_t tgt, w, bar, meta, seg, start, spk, total;
-    __host__ __device__ SmemLayout(uint32_t nseg_smem) {
-        tgt = 0;
+    uint32_t acc, tgt, w, bar, meta, seg, start, spk, total;
+    // acc_bytes: per-tile pending accumulators (tiled delivery), 0 otherwise
+    __host__ __device__ SmemLayout(uint32_t nseg_smem, uint32_t acc_bytes = 0) {
+        acc = 0;
+        tgt = acc_bytes;
         w = tgt + kStages * kStageTgtBytes;
         bar = w + kStages * kStageWBytes;
         meta = bar + kStages * 8;
@@ -343,6 +360,49 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
 __device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint64_t pol) {
     asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;"
                  ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
+// Starts the bulk copies of table entries [b0, b1) into stage `st` (16-byte
+// aligned supersets; head offsets in the stage metadata).
+__device__ __forceinline__ void issue_range(const StepArgs& a, unsigned char* smem,
+                                            const SmemLayout& L, uint32_t st, uint64_t b0,
+                                            uint64_t b1, uint64_t pol) {
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta) + st;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+    StageMeta m;
+    m.spike = 0;
+    m.first = 0;
+    m.len = 0;
+    m.n = (uint32_t)(b1 - b0);
+    const uint64_t t0 = b0 & ~3ull, t1 = (b1 + 3) & ~3ull;
+    const uint64_t w0 = b0 & ~1ull, w1 = (b1 + 1) & ~1ull;
+    m.head_t = (uint32_t)(b0 - t0);
+    m.head_w = (uint32_t)(b0 - w0);
+    *meta = m;
+    const uint32_t tb = (uint32_t)(t1 - t0) * 4, wb = (uint32_t)(w1 - w0) * 8;
+    mbar_expect_tx(bar, tb + wb);
+    bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
+    bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
+}
+
+// Tiled delivery, producer side: queue the row segments of spike s (one per
+// target tile, from the source's tile directory) for the step's tile
+// queues.  Runs when the spike is produced, one phase before delivery.
+__device__ __forceinline__ void bin_spike(const StepArgs& a, uint32_t s, uint32_t set,
+                                          unsigned long long& inner2,
+                                          unsigned long long& outer2) {
+    const uint32_t d0 = __ldg(a.dir_off + s), d1 = __ldg(a.dir_off + s + 1);
+    const uint64_t row = ldg64(a.off + s), len = ldg64(a.off + s + 1) - row;
+    for (uint32_t d = d0; d < d1; ++d) {
+        const uint64_t e = ldg64(a.dir + d);
+        const uint32_t tile = (uint32_t)(e >> 12) & 0xfffffu;
+        const uint64_t start = row + (e >> 32), lm1 = e & 0xfffull;
+        const uint32_t q = atomicAdd(a.qcount + (size_t)set * a.n_tiles + tile, 1u);
+        a.queue[(size_t)set * a.q_total + ldg64(a.qbase + tile) + q] = start | (lm1 << 40);
+    }
+    const uint32_t in = __ldg(a.inner + s);
+    inner2 += 2ull * in;
+    outer2 += 2ull * (len - in);
 }
 
 // Starts the bulk copies of one delivery piece (item = spike k, piece c of
@@ -475,7 +535,7 @@ __device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u);
+    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u, a.tiled ? a.acc_bytes : 0u);
     SegParams* s_seg = reinterpret_cast<SegParams*>(smem + L.seg);
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
@@ -594,15 +654,18 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
                         p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
                         p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
-                        __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
+                        if (!a.tiled)  // tiled delivery overwrites whole tiles instead
+                            __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
                     } else {
                         p0 = dequantize((int64_t)cur.p0.x);
                         p1 = dequantize((int64_t)cur.p0.y);
                         p2 = dequantize((int64_t)cur.p1.x);
                         p3 = dequantize((int64_t)cur.p1.y);
                         ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
-                        __stcg(q, make_ulonglong2(0ull, 0ull));
-                        __stcg(q + 1, make_ulonglong2(0ull, 0ull));
+                        if (!a.tiled) {
+                            __stcg(q, make_ulonglong2(0ull, 0ull));
+                            __stcg(q + 1, make_ulonglong2(0ull, 0ull));
+                        }
                     }
                     j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
                     j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
@@ -687,9 +750,10 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                     const unsigned rank = __popc(ball & ((1u << lane) - 1u));
                     if (base + rank < kSpkStage)
                         s_spk[base + rank] = i;
-                    else {  // staging full: straight to the log (and to the peers)
+                    else {  // staging full: straight to the log (and to the peers / tiles)
                         a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
                         if (a.world > 1) overflow_route = true;
+                        if (a.tiled) bin_spike(a, i, tA & 1u, my_inner, my_outer);
                     }
                     const uint32_t unit = segp[seg].unit;
                     const unsigned peers = __match_any_sync(ball, unit);
@@ -708,6 +772,9 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         fsync();
         for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
             a.spk[log_base + s_base + k] = s_spk[k];
+        if (a.tiled && doA)
+            for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
+                bin_spike(a, s_spk[k], tA & 1u, my_inner, my_outer);
         if (a.world > 1 && doA) {
             bool sent = false;
             const uint32_t nr = (nst + 31u) & ~31u;
@@ -720,7 +787,71 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
 
         // ------------------------------------------------------------ D
         unsigned long long wait_ns = 0;
-        if (roleD && doE) {
+        if (roleD && doE && a.tiled) {
+            // Tiled delivery of S(tE): this CTA owns whole target tiles; the
+            // queued row segments are streamed in by bulk copies and summed
+            // with shared-memory atomics, then every tile's pending sums are
+            // stored with plain coalesced stores (no global atomics, no
+            // zeroing pass: each tile is overwritten entirely).
+            const uint32_t set = tE & 1u;
+            unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + L.acc);
+            const uint32_t acc_words = a.acc_bytes / 8;
+            for (uint32_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+                for (uint32_t k = threadIdx.x; k < acc_words; k += d_cta) acc[k] = 0ull;
+                if (threadIdx.x == 0) s_rcnt = atomicExch(a.qcount + (size_t)set * a.n_tiles + tile, 0u);
+                dsync();
+                const uint32_t cnt = s_rcnt;
+                const uint64_t* q = a.queue + (size_t)set * a.q_total + ldg64(a.qbase + tile);
+                const uint32_t tbase = tile << kTileLog;
+                if (threadIdx.x == 0 && cnt) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    for (uint32_t j = 0; j < cnt && j < (uint32_t)kStages; ++j) {
+                        const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long*>(q) + j);
+                        const uint64_t b0 = e & ((1ull << 40) - 1);
+                        issue_range(a, smem, L, (g_item + j) % kStages, b0, b0 + (e >> 40) + 1, pol_stream);
+                    }
+                }
+                for (uint32_t j = 0; j < cnt; ++j, ++g_item) {
+                    const uint32_t st = g_item % kStages;
+                    mbar_wait(s_bar + st, (g_item / kStages) & 1u);
+                    const StageMeta m = s_meta[st];
+                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
+                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
+                    for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
+                        const uint32_t t = tg[e], tl = (t & 0x7fffffffu) - tbase, cls = t >> 31;
+                        const uint64_t wq = wv[e];
+                        if constexpr (PACKED) {
+                            // carry-free packed pair: two native 32-bit shared
+                            // atomics give the same 64-bit word (64-bit shared
+                            // atomics are CAS loops on sm_100)
+                            unsigned int* a32 = reinterpret_cast<unsigned int*>(acc + 2 * tl + cls);
+                            atomicAdd(a32, (unsigned int)wq);
+                            atomicAdd(a32 + 1, (unsigned int)(wq >> 32));
+                        } else {
+                            atomicAdd(acc + 4 * tl + 2 * cls,
+                                      (unsigned long long)(int64_t)(int32_t)(uint32_t)wq);
+                            atomicAdd(acc + 4 * tl + 2 * cls + 1,
+                                      (unsigned long long)(int64_t)(int32_t)(uint32_t)(wq >> 32));
+                        }
+                    }
+                    dsync();  // stage st drained by every delivery thread
+                    if (threadIdx.x == 0 && j + kStages < cnt) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long*>(q) + j + kStages);
+                        const uint64_t b0 = e & ((1ull << 40) - 1);
+                        issue_range(a, smem, L, st, b0, b0 + (e >> 40) + 1, pol_stream);
+                    }
+                }
+                // store the tile's pending sums (whole tile, coalesced 16 B)
+                const uint32_t nt = min((uint32_t)kTile, a.n - tbase);
+                const uint32_t words = nt * (PACKED ? 2u : 4u);
+                ulonglong2* dst = reinterpret_cast<ulonglong2*>(
+                    reinterpret_cast<unsigned long long*>(pend_wr) + (size_t)tbase * (PACKED ? 2u : 4u));
+                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(acc);
+                for (uint32_t k = threadIdx.x; k < words / 2; k += d_cta) __stcg(dst + k, src[k]);
+                dsync();  // acc reused by the next tile
+            }
+        } else if (roleD && doE) {
             const uint32_t tslot = tE % 3u;
             const uint32_t* local_ids = a.spk + d_prev + d_lo;
             for (uint32_t li = 0; li < a.world; ++li) {
@@ -868,6 +999,48 @@ __global__ void csr_scatter_kernel(const SynIn* __restrict__ e,
         }
         neg = __any_sync(0xffffffffu, neg);
         if (lane == 0 && (neg || sf >= (1ll << 32) || ss >= (1ll << 32))) atomicExch(wide, 1u);
+    }
+}
+
+// Tiled delivery tables: rows are sorted by target; a segment is the run of a
+// row inside one target tile, split so that no piece exceeds a stage.
+__global__ void tile_dir_count_kernel(const uint64_t* __restrict__ off,
+                                      const uint32_t* __restrict__ tgt, uint32_t n_src,
+                                      uint32_t* __restrict__ nseg, uint32_t* __restrict__ tile_cap) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_src; s += gridDim.x * blockDim.x) {
+        const uint64_t e0 = off[s], e1 = off[s + 1];
+        uint32_t cnt = 0;
+        uint64_t k = e0;
+        while (k < e1) {
+            const uint32_t tile = (tgt[k] & 0x7fffffffu) >> kTileLog;
+            uint64_t j = k + 1;
+            while (j < e1 && ((tgt[j] & 0x7fffffffu) >> kTileLog) == tile) ++j;
+            const uint32_t pieces = (uint32_t)((j - k + kStageE - 1) / kStageE);
+            cnt += pieces;
+            atomicAdd(tile_cap + tile, pieces);
+            k = j;
+        }
+        nseg[s] = cnt;
+    }
+}
+
+__global__ void tile_dir_fill_kernel(const uint64_t* __restrict__ off,
+                                     const uint32_t* __restrict__ tgt, uint32_t n_src,
+                                     const uint32_t* __restrict__ dir_off, uint64_t* __restrict__ dir) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_src; s += gridDim.x * blockDim.x) {
+        const uint64_t e0 = off[s], e1 = off[s + 1];
+        uint32_t at = dir_off[s];
+        uint64_t k = e0;
+        while (k < e1) {
+            const uint32_t tile = (tgt[k] & 0x7fffffffu) >> kTileLog;
+            uint64_t j = k + 1;
+            while (j < e1 && ((tgt[j] & 0x7fffffffu) >> kTileLog) == tile) ++j;
+            for (uint64_t p = k; p < j; p += kStageE) {
+                const uint64_t len = min((uint64_t)kStageE, j - p);
+                dir[at++] = ((p - e0) << 32) | ((uint64_t)tile << 12) | (len - 1);
+            }
+            k = j;
+        }
     }
 }
 

@@ -974,14 +974,16 @@ void Engine::setup_exchange() {
     CK(cudaStreamSynchronize(stream));
 }
 
-// Tiled delivery (single device): sort every out-row by target, build the
-// per-source tile directory and the per-tile segment queues.  Used when the
-// network has locality (few segments per row); otherwise the engine keeps the
-// L2-atomic delivery.  VXB_TILED=0 disables it.
+// Tiled delivery (single device, experimental, VXB_TILED=1): sort every
+// out-row by target, build the per-source tile directory and the per-tile
+// segment queues; delivery then accumulates whole target tiles in shared
+// memory (no global atomics).  Bit-exact, but in round 1 it is latency-bound
+// (serialised stage issue per tile, uneven tiles per CTA) and slower than
+// the L2-atomic path, so it is off by default.
 void Engine::build_tiles() {
     tiled = false;
     const char* env = std::getenv("VXB_TILED");
-    if (env && std::string(env) == "0") return;
+    if (!env || std::string(env) != "1") return;
     if (world != 1 || n_syn == 0 || n_syn >= (1ull << 31) || n < (uint32_t)kTile ||
         n_src != n)
         return;

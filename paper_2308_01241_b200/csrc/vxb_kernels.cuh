@@ -285,6 +285,20 @@ struct StageMeta {
     uint32_t len;     // row length
 };
 
+// Tiled delivery packs several queued row segments into one stage.
+constexpr int kSegPerStage = 16;
+struct TStageMeta {
+    uint32_t n;                       // entries in the stage
+    uint32_t nseg;
+    uint32_t end;                     // last stage of the tile's queue
+    uint32_t pad;
+    uint32_t pre[kSegPerStage + 1];   // prefix of segment lengths
+    uint32_t tb[kSegPerStage];        // first entry of segment i in the tgt buffer
+    uint32_t wb[kSegPerStage];        // ... in the w buffer
+};
+constexpr uint32_t kMetaBytes =
+    sizeof(TStageMeta) > sizeof(StageMeta) ? sizeof(TStageMeta) : sizeof(StageMeta);
+
 // Dynamic shared memory carve-up of step_kernel.
 struct SmemLayout {
     uint32_t acc, tgt, w, bar, meta, seg, start, spk, total;
@@ -295,7 +309,7 @@ struct SmemLayout {
         w = tgt + kStages * kStageTgtBytes;
         bar = w + kStages * kStageWBytes;
         meta = bar + kStages * 8;
-        seg = (meta + kStages * (uint32_t)sizeof(StageMeta) + 127) & ~127u;
+        seg = (meta + kStages * kMetaBytes + 127) & ~127u;
         start = seg + nseg_smem * (uint32_t)sizeof(SegParams);
         spk = (start + (nseg_smem + 1) * 4 + 15) & ~15u;
         total = spk + kSpkStage * 4;
@@ -367,7 +381,7 @@ __device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint6
 __device__ __forceinline__ void issue_range(const StepArgs& a, unsigned char* smem,
                                             const SmemLayout& L, uint32_t st, uint64_t b0,
                                             uint64_t b1, uint64_t pol) {
-    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta) + st;
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta + st * kMetaBytes);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
     StageMeta m;
     m.spike = 0;
@@ -383,6 +397,63 @@ __device__ __forceinline__ void issue_range(const StepArgs& a, unsigned char* sm
     mbar_expect_tx(bar, tb + wb);
     bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
     bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
+}
+
+// Tiled delivery: fill stage `st` with as many queued segments (q[qi..cnt))
+// as fit, one mbarrier for all their bulk copies.  Returns true once the
+// queue is exhausted (the stage is then marked as the tile's last).
+__device__ __forceinline__ bool issue_tstage(const StepArgs& a, unsigned char* smem,
+                                             const SmemLayout& L, uint32_t st,
+                                             const uint64_t* q, uint32_t cnt, uint32_t& qi,
+                                             uint64_t pol) {
+    TStageMeta* meta = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+    uint64_t b0s[kSegPerStage];
+    uint32_t lens[kSegPerStage];
+    uint64_t ev[kSegPerStage];
+#pragma unroll
+    for (int k = 0; k < kSegPerStage; ++k)  // independent loads, one round trip
+        ev[k] = qi + k < cnt ? __ldcg(reinterpret_cast<const unsigned long long*>(q) + qi + k) : 0ull;
+    uint32_t ns = 0, toff = 0, woff = 0, total = 0, bytes = 0;
+    while (qi < cnt && ns < (uint32_t)kSegPerStage) {
+        const uint64_t e = ev[ns];
+        const uint64_t b0 = e & ((1ull << 40) - 1), b1 = b0 + (e >> 40) + 1;
+        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - (b0 & ~3ull));
+        const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - (b0 & ~1ull));
+        if (ns && (toff + tn > (uint32_t)kStageE + 8 || woff + wn > (uint32_t)kStageE + 4)) break;
+        b0s[ns] = b0;
+        lens[ns] = (uint32_t)(b1 - b0);
+        meta->pre[ns] = total;
+        meta->tb[ns] = toff + (uint32_t)(b0 & 3ull);
+        meta->wb[ns] = woff + (uint32_t)(b0 & 1ull);
+        total += lens[ns];
+        bytes += tn * 4 + wn * 8;
+        toff += tn;
+        woff += wn;
+        ++ns;
+        ++qi;
+    }
+    meta->pre[ns] = total;
+    meta->n = total;
+    meta->nseg = ns;
+    const bool end = qi >= cnt;
+    meta->end = end ? 1u : 0u;
+    if (!ns) {
+        mbar_arrive(bar);
+        return end;
+    }
+    mbar_expect_tx(bar, bytes);
+    uint32_t to = 0, wo = 0;
+    for (uint32_t i = 0; i < ns; ++i) {
+        const uint64_t b0 = b0s[i], b1 = b0 + lens[i];
+        const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0), wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
+        bulk_g2s(smem + L.tgt + st * kStageTgtBytes + to * 4, a.tgt + t0, tn * 4, bar, pol);
+        bulk_g2s(smem + L.w + st * kStageWBytes + wo * 8, a.w + w0, wn * 8, bar, pol);
+        to += tn;
+        wo += wn;
+    }
+    return end;
 }
 
 // Tiled delivery, producer side: queue the row segments of spike s (one per
@@ -413,7 +484,7 @@ __device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* sm
                                             const SmemLayout& L, uint32_t st, uint32_t item,
                                             uint32_t C, const uint32_t* ids, uint32_t src_base,
                                             uint64_t pol) {
-    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta) + st;
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta + st * kMetaBytes);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
     const uint32_t k = item / C, c = item - k * C;
     const uint32_t s = src_base + __ldcg(ids + k);
@@ -540,9 +611,11 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-    StageMeta* s_meta = reinterpret_cast<StageMeta*>(smem + L.meta);
+    unsigned char* s_meta_base = smem + L.meta;
     __shared__ uint32_t s_nspk;
     __shared__ uint32_t s_rcnt;
+    __shared__ uint32_t s_bn[129], s_bd[128];  // binning: segments per spike, dir offsets
+    __shared__ uint64_t s_br[128];             // binning: row starts
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
 
@@ -772,9 +845,52 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         fsync();
         for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
             a.spk[log_base + s_base + k] = s_spk[k];
-        if (a.tiled && doA)
-            for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
-                bin_spike(a, s_spk[k], tA & 1u, my_inner, my_outer);
+        if (a.tiled && doA) {
+            // bin the staged spikes into the tile queues: one thread per
+            // (spike, tile segment) pair, 128 spikes per round
+            for (uint32_t c0 = 0; c0 < nst; c0 += 128) {
+                const uint32_t cn = min(128u, nst - c0);
+                const uint32_t fl = threadIdx.x - f_first;
+                if (fl < cn) {
+                    const uint32_t sp = s_spk[c0 + fl];
+                    const uint32_t d0 = __ldg(a.dir_off + sp), d1 = __ldg(a.dir_off + sp + 1);
+                    const uint64_t row = ldg64(a.off + sp), len = ldg64(a.off + sp + 1) - row;
+                    const uint32_t in = __ldg(a.inner + sp);
+                    my_inner += 2ull * in;
+                    my_outer += 2ull * (len - in);
+                    s_bn[fl] = d1 - d0;
+                    s_bd[fl] = d0;
+                    s_br[fl] = row;
+                }
+                fsync();
+                if (threadIdx.x == f_first) {  // exclusive prefix (<= 128 spikes)
+                    uint32_t acc = 0;
+                    for (uint32_t k = 0; k < cn; ++k) {
+                        const uint32_t v = s_bn[k];
+                        s_bn[k] = acc;
+                        acc += v;
+                    }
+                    s_bn[cn] = acc;
+                }
+                fsync();
+                const uint32_t tot = s_bn[cn];
+                for (uint32_t pidx = fl; pidx < tot; pidx += f_cta) {
+                    uint32_t lo = 0, hi = cn;  // spike k with s_bn[k] <= pidx < s_bn[k+1]
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (s_bn[mid] <= pidx) lo = mid; else hi = mid;
+                    }
+                    const uint64_t e = ldg64(a.dir + s_bd[lo] + (pidx - s_bn[lo]));
+                    const uint32_t tile = (uint32_t)(e >> 12) & 0xfffffu;
+                    const uint64_t start = s_br[lo] + (e >> 32), lm1 = e & 0xfffull;
+                    const uint32_t set = tA & 1u;
+                    const uint32_t qpos = atomicAdd(a.qcount + (size_t)set * a.n_tiles + tile, 1u);
+                    a.queue[(size_t)set * a.q_total + ldg64(a.qbase + tile) + qpos] =
+                        start | (lm1 << 40);
+                }
+                fsync();
+            }
+        }
         if (a.world > 1 && doA) {
             bool sent = false;
             const uint32_t nr = (nst + 31u) & ~31u;
@@ -803,23 +919,27 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 const uint32_t cnt = s_rcnt;
                 const uint64_t* q = a.queue + (size_t)set * a.q_total + ldg64(a.qbase + tile);
                 const uint32_t tbase = tile << kTileLog;
-                if (threadIdx.x == 0 && cnt) {
+                uint32_t qi = 0;
+                bool ended = false;
+                if (threadIdx.x == 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    for (uint32_t j = 0; j < cnt && j < (uint32_t)kStages; ++j) {
-                        const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long*>(q) + j);
-                        const uint64_t b0 = e & ((1ull << 40) - 1);
-                        issue_range(a, smem, L, (g_item + j) % kStages, b0, b0 + (e >> 40) + 1, pol_stream);
-                    }
+                    for (uint32_t j = 0; j < (uint32_t)kStages && !ended; ++j)
+                        ended = issue_tstage(a, smem, L, (g_item + j) % kStages, q, cnt, qi, pol_stream);
                 }
-                for (uint32_t j = 0; j < cnt; ++j, ++g_item) {
+                for (;;) {
                     const uint32_t st = g_item % kStages;
                     mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-                    const StageMeta m = s_meta[st];
-                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
-                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
-                    for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
-                        const uint32_t t = tg[e], tl = (t & 0x7fffffffu) - tbase, cls = t >> 31;
-                        const uint64_t wq = wv[e];
+                    ++g_item;
+                    const TStageMeta* m = reinterpret_cast<const TStageMeta*>(s_meta_base + st * kMetaBytes);
+                    const uint32_t n_e = m->n, last = m->end;
+                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes);
+                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes);
+                    uint32_t sg = 0;
+                    for (uint32_t e = threadIdx.x; e < n_e; e += d_cta) {
+                        while (e >= m->pre[sg + 1]) ++sg;
+                        const uint32_t r = e - m->pre[sg];
+                        const uint32_t t = tg[m->tb[sg] + r], tl = (t & 0x7fffffffu) - tbase, cls = t >> 31;
+                        const uint64_t wq = wv[m->wb[sg] + r];
                         if constexpr (PACKED) {
                             // carry-free packed pair: two native 32-bit shared
                             // atomics give the same 64-bit word (64-bit shared
@@ -835,11 +955,10 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         }
                     }
                     dsync();  // stage st drained by every delivery thread
-                    if (threadIdx.x == 0 && j + kStages < cnt) {
+                    if (last) break;
+                    if (threadIdx.x == 0 && !ended) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long*>(q) + j + kStages);
-                        const uint64_t b0 = e & ((1ull << 40) - 1);
-                        issue_range(a, smem, L, st, b0, b0 + (e >> 40) + 1, pol_stream);
+                        ended = issue_tstage(a, smem, L, st, q, cnt, qi, pol_stream);
                     }
                 }
                 // store the tile's pending sums (whole tile, coalesced 16 B)
@@ -881,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 for (uint32_t j = 0; j < mine; ++j, ++g_item) {
                     const uint32_t st = g_item % kStages;
                     mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-                    const StageMeta m = s_meta[st];
+                    const StageMeta m = *reinterpret_cast<const StageMeta*>(s_meta_base + st * kMetaBytes);
                     const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
                     const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
                     for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {

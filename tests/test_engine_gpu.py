@@ -355,3 +355,17 @@ def test_acceptance_1_multi_worker_equivalence():
         for w, s in enumerate(snaps):
             state[net.tables.workers[w].neurons["gid"]] = s
         assert np.array_equal(state, ref_state)
+
+
+def test_tiled_delivery_mode_matches_reference(monkeypatch):
+    """Experimental tiled delivery (VXB_TILED=1): target-sorted rows, tile
+    queues, shared-memory accumulation — must stay bit-exact."""
+    monkeypatch.setenv("VXB_TILED", "1")
+    cfg = make_config(seed=1, voxels=1, npv=10000, k_in=100, dt_ms=0.1, steps=3000)
+    net = RefNet(cfg)
+    opt = SimOptions(steps=3000, dt_ms=0.1, probe_gids=[0, 4321, 9999])
+    gpu, snaps = gpu_run(net.tables, opt)
+    rs = RefSim(net, opt)
+    ref = rs.advance(3000)
+    assert_same(gpu, ref)
+    assert np.array_equal(snaps[0], rs.membrane_snapshot(0))

@@ -328,6 +328,12 @@ int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t work
                               vxb_neuron* neurons, uint32_t n_cap, vxb_syn_entry* synapses,
                               uint64_t syn_cap, uint64_t* row_base);
 
+/* ---- table files ---------------------------------------------------------- */
+/* FNV-1a 64 (util.hpp:39-46) over n bytes continuing from hash h (start with
+ * 0xcbf29ce484222325): the integrity hash of VXTB table files in
+ * manifest.json (netgen.cpp:478-524). */
+uint64_t vxb_fnv1a(const void* data, uint64_t n, uint64_t h);
+
 /* ---- diagnostics --------------------------------------------------------- */
 /* Device evaluation of stream_normal(base[i], k[i]) (rng.hpp:63-67) exactly as
  * the step kernel computes it, for noise-parity checks against the host. */

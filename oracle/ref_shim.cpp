@@ -156,6 +156,28 @@ void* ref_build(const char* cfg_json, int even_workers, char* err, int errlen) {
 
 void ref_free(void* h) { delete static_cast<RefNet*>(h); }
 
+// save_tables / load_tables (netgen.cpp:466-539) for the table-file tests.
+int ref_save_tables(void* h, const char* dir, char* err, int errlen) {
+    return guarded(err, errlen, [&] { save_tables(static_cast<RefNet*>(h)->tables, dir); });
+}
+
+// A RefNet whose tables come from load_tables(dir); the layout is rebuilt
+// from the config, as cmd_simulate --tables does (voxsim.cpp:149-156).
+void* ref_load_net(const char* cfg_json, const char* dir, char* err, int errlen) {
+    RefNet* out = nullptr;
+    int rc = guarded(err, errlen, [&] {
+        auto net = std::make_unique<RefNet>();
+        net->cfg = parse_config(cfg_json);
+        net->graph = build_connectome(net->cfg);
+        MicrocolumnSpec mc;
+        net->layout = build_layout(net->cfg, net->graph, mc);
+        net->tables = load_tables(dir);
+        for (const auto& w : net->tables.workers) net->synapse_count += w.synapses.size();
+        out = net.release();
+    });
+    return rc == 0 ? out : nullptr;
+}
+
 double ref_build_seconds(void* h) { return static_cast<RefNet*>(h)->build_seconds; }
 uint64_t ref_seed(void* h) { return static_cast<RefNet*>(h)->cfg.seed; }
 uint32_t ref_n_workers(void* h) {

@@ -151,7 +151,7 @@ EXPORTS = [
     "vxb_probes", "vxb_run_simulation", "vxb_debug_stream_normal", "vxb_create_generated",
     "vxb_generate_worker_table", "vxb_create_generated_rank", "vxb_mask_bytes",
     "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
-    "vxb_result_exchange_wait_ms",
+    "vxb_result_exchange_wait_ms", "vxb_fnv1a",
 ]
 
 _lib = None
@@ -178,6 +178,7 @@ def _declare(lib):
         "vxb_result_device_ms": (C.c_double, [P]),
         "vxb_result_h2d_bytes": (C.c_uint64, [P]),
         "vxb_result_exchange_wait_ms": (C.c_double, [P]),
+        "vxb_fnv1a": (C.c_uint64, [P, C.c_uint64, C.c_uint64]),
         "vxb_result_d2h_bytes": (C.c_uint64, [P]),
         "vxb_result_launches": (C.c_uint64, [P]),
         "vxb_set_conductances": (C.c_int, [P, C.c_uint32, C.c_int, P, C.c_uint32]),

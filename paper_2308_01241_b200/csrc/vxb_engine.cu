@@ -1700,6 +1700,15 @@ int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t work
     }
 }
 
+uint64_t vxb_fnv1a(const void* data, uint64_t n, uint64_t h) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (uint64_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
 int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
                             double* out) {
     try {

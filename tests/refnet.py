@@ -43,6 +43,8 @@ def ref_lib():
         sig = {
             "ref_build": (P, [C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
             "ref_free": (None, [P]),
+            "ref_save_tables": (C.c_int, [P, C.c_char_p, C.c_char_p, C.c_int]),
+            "ref_load_net": (P, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]),
             "ref_build_seconds": (C.c_double, [P]),
             "ref_seed": (u64, [P]),
             "ref_n_workers": (u32, [P]),
@@ -181,10 +183,14 @@ def make_config(*, seed=1, voxels=1, npv=100, k_in=10, rho=0.0, kind=None, dt_ms
 class RefNet:
     """A network built by the reference pipeline, exported as NetworkTables."""
 
-    def __init__(self, cfg: dict, even_workers: int = 0):
+    def __init__(self, cfg: dict, even_workers: int = 0, tables_dir: str | None = None):
         L = ref_lib()
         err = C.create_string_buffer(1024)
-        self._h = L.ref_build(json.dumps(cfg).encode(), even_workers, err, 1024)
+        if tables_dir is not None:
+            self._h = L.ref_load_net(json.dumps(cfg).encode(), str(tables_dir).encode(), err,
+                                     1024)
+        else:
+            self._h = L.ref_build(json.dumps(cfg).encode(), even_workers, err, 1024)
         if not self._h:
             m = err.value.decode()
             _raise(2 if m.startswith("ConfigError") else 3, _strip(m))
@@ -222,6 +228,12 @@ class RefNet:
     @property
     def total_neurons(self) -> int:
         return int(ref_lib().ref_total_neurons(self._h))
+
+    def save_tables(self, directory) -> None:
+        err = C.create_string_buffer(1024)
+        rc = ref_lib().ref_save_tables(self._h, str(directory).encode(), err, 1024)
+        if rc:
+            _raise(rc, _strip(err.value.decode()))
 
 
 @dataclass

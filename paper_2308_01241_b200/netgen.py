@@ -422,7 +422,7 @@ CONFIG_KEYS = {"seed", "dt_ms", "steps", "workers", "workers_per_node", "schedul
                "microcolumn_path", "probe_gids"}
 CONNECTOME_KEYS = {"kind", "voxels", "neurons_per_voxel", "sparsity", "weight_sigma",
                    "gm_sigma", "cross_weight", "scramble", "path", "region"}
-PARTITION_KEYS = {"method", "path", "alpha", "beta", "mu", "gamma", "rate_hz"}
+PARTITION_KEYS = {"method", "path", "alpha", "beta", "mu", "gamma", "rate_hz", "byte_model"}
 REGION_KEYS = {"k_in", "rho", "ou_mean", "ou_sigma", "ou_tau", "g_location", "g_scale",
                "weight_mean", "weight_spread", "dual_receptor", "split_ratio"}
 
@@ -453,7 +453,7 @@ def parse_config(cfg) -> dict:
         _check_keys(cfg["connectome"], "connectome", CONNECTOME_KEYS)
         con.update(cfg["connectome"])
     part = {"method": "greedy", "path": "", "alpha": 1.0, "beta": 1.0, "mu": 1.0, "gamma": 0.0,
-            "rate_hz": 7.0}
+            "rate_hz": 7.0, "byte_model": "reference"}
     if "partition" in cfg:
         _check_keys(cfg["partition"], "partition", PARTITION_KEYS)
         part.update(cfg["partition"])
@@ -461,6 +461,8 @@ def parse_config(cfg) -> dict:
         raise ConfigError("unknown partition method: " + str(part["method"]))
     if part["method"] == "file" and not part["path"]:
         raise ConfigError("partition method 'file' needs a path")
+    if part["byte_model"] not in BYTE_MODELS:
+        raise ConfigError("unknown byte_model: " + str(part["byte_model"]))
     regions = {}
     for name, rc in cfg.get("regions", {}).items():
         if name not in REGIONS:
@@ -567,6 +569,18 @@ def intra_matrices(mc: Optional[dict]) -> Dict[str, List[List[float]]]:  # layou
 # -------------------------------------------------------------- partition
 STATE_BYTES, ENTRY_BYTES, BUFFER_BYTES = 48, 16, 12  # partition.cpp:16-18
 
+# Capacity byte models (s1 per neuron, s2 per synapse, s3 per neuron):
+#  "reference" — the CPU engine's model (partition.cpp:16-18);
+#  "b200"      — what this engine actually keeps in HBM per GPU: neuron state
+#                V 4 + j 16 + I_ou 4 + I_syn 4 + g 16 + two pending buffers 32 +
+#                destination mask 8 + spike-log slots 8 = 92 B; 12 B per synapse
+#                (u32 target + packed Q16 pair); 12 B per neuron of exchange
+#                receive slots (3 step slots x 4 B id).  With this model and
+#                gamma = the per-GPU HBM budget, greedy/sequential place units
+#                under the 180 GB of a B200.
+BYTE_MODELS = {"reference": (48, 16, 12), "b200": (92, 12, 12)}
+B200_HBM_BUDGET = 170e9  # bytes per GPU left for tables + state (of 183 GB)
+
 
 @dataclass
 class UnitGraph:  # partition.hpp:14-22
@@ -578,7 +592,7 @@ class UnitGraph:  # partition.hpp:14-22
 
 
 def build_unit_graph(layout: Layout, g: Connectome, intra, rate_hz: float,
-                     dt_ms: float) -> UnitGraph:  # partition.cpp:44-138
+                     dt_ms: float, byte_model: str = "reference") -> UnitGraph:  # partition.cpp:44-138
     if rate_hz < 0.0:
         raise ConfigError("negative traffic rate")
     U = len(layout.units)
@@ -637,8 +651,8 @@ def build_unit_graph(layout: Layout, g: Connectome, intra, rate_hz: float,
                 picks = n_t * ppn * q
                 bytes_ = rate_hz * dt_s * distinct(n_s, picks) * 4.0
                 traffic[b0 + sp][b0 + tp] += llround(bytes_ * 1e6)
-    return UnitGraph(n, n * STATE_BYTES, n * kin * ENTRY_BYTES, n * BUFFER_BYTES,
-                     np.array(traffic, np.int64).reshape(U, U))
+    s1, s2, s3 = BYTE_MODELS[byte_model]
+    return UnitGraph(n, n * s1, n * kin * s2, n * s3, np.array(traffic, np.int64).reshape(U, U))
 
 
 def _load(g: UnitGraph, cap: dict, u: int) -> float:
@@ -922,14 +936,29 @@ def build_network(cfg, workers: Optional[int] = None, method: Optional[str] = No
     elif p["method"] == "file":
         uw, W = load_partition(p["path"], len(layout.units))
     else:
-        ug = build_unit_graph(layout, g, intra, p["rate_hz"], cfg["dt_ms"])
+        ug = build_unit_graph(layout, g, intra, p["rate_hz"], cfg["dt_ms"], p["byte_model"])
         if W == 1:
             uw = [0] * len(layout.units)
             validate_partition(uw, 1, len(layout.units))
         else:
             fn = {"greedy": partition_greedy, "sequential": partition_sequential,
                   "exact": partition_exact}[p["method"]]
-            uw = fn(ug, W, p)
+            if p["byte_model"] == "b200" and p["gamma"] <= 0:
+                # per-GPU budget: the HBM budget, tightened to a near-even share
+                # so the traffic objective cannot pile units onto one GPU
+                total = sum(_load(ug, p, u) for u in range(len(layout.units)))
+                for slack in (1.1, 1.25, 1.5, 2.0, None):
+                    q = dict(p)
+                    q["gamma"] = B200_HBM_BUDGET if slack is None else \
+                        min(B200_HBM_BUDGET, slack * total / W)
+                    try:
+                        uw = fn(ug, W, q)
+                        break
+                    except ConfigError:
+                        if slack is None:
+                            raise
+            else:
+                uw = fn(ug, W, p)
     # arrays for vxb_netspec
     units = np.zeros(len(layout.units), UNIT_DTYPE)
     pops = np.zeros(len(layout.units), POP_DTYPE)
@@ -950,9 +979,28 @@ def build_network(cfg, workers: Optional[int] = None, method: Optional[str] = No
         edges[i] = e
     intra_arr = {r: np.ascontiguousarray(np.array(m, np.float64)) for r, m in intra.items()}
     syn = sum(u.neurons * layout.voxels[u.voxel].k_in for u in layout.units)
+    if p["byte_model"] == "b200":  # every GPU must fit its share of the network
+        s1, s2, s3 = BYTE_MODELS["b200"]
+        load = [0.0] * W
+        for u, x in enumerate(layout.units):
+            load[uw[u]] += x.neurons * (s1 + s3 + layout.voxels[x.voxel].k_in * s2)
+        budget = p["gamma"] if p["gamma"] > 0 else B200_HBM_BUDGET
+        for w in range(W):
+            if load[w] > budget:
+                raise ConfigError(f"worker {w} needs {load[w] / 1e9:.1f} GB of HBM "
+                                  f"(budget {budget / 1e9:.1f} GB)")
     arrays = {"units": units, "pops": pops, "voxels": voxels, "edges": edges,
               "intra": intra_arr, "unit_worker": np.asarray(uw, np.uint16)}
     return BuiltNetwork(cfg, g, layout, intra, ug, list(uw), W, syn, arrays)
+
+
+def hbm_bytes_per_worker(net: "BuiltNetwork") -> list:
+    """Device bytes per worker under the B200 byte model."""
+    s1, s2, s3 = BYTE_MODELS["b200"]
+    load = [0] * net.workers
+    for u, x in enumerate(net.layout.units):
+        load[net.unit_worker[u]] += x.neurons * (s1 + s3 + net.layout.voxels[x.voxel].k_in * s2)
+    return load
 
 
 def sim_options_from(cfg: dict, **over) -> SimOptions:  # pipeline.cpp:127-137

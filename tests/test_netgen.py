@@ -85,3 +85,16 @@ def test_llround_matches_cpp():
         assert netgen.llround(x) == int(np.floor(x + 0.5)) or x == 0.49999999999999994
     assert netgen.llround(0.49999999999999994) == 0
     assert netgen.llround(2.5) == 3 and netgen.llround(-2.5) == -3
+
+
+def test_b200_byte_model_partitions_under_budget():
+    cfg = make_config(seed=2, voxels=40, npv=2000, k_in=200, rho=0.3, workers=4)
+    cfg["partition"] = {"method": "greedy", "byte_model": "b200"}
+    b = netgen.build_network(cfg)
+    loads = netgen.hbm_bytes_per_worker(b)
+    assert max(loads) <= 1.25 * min(loads)  # balanced by bytes
+    cfg["partition"]["gamma"] = 0.5 * max(loads)
+    with pytest.raises(ConfigError):
+        netgen.build_network(cfg)
+    with pytest.raises(ConfigError, match="byte_model"):
+        netgen.parse_config({"partition": {"byte_model": "tpu"}})

@@ -92,7 +92,7 @@ def test_b200_byte_model_partitions_under_budget():
     cfg["partition"] = {"method": "greedy", "byte_model": "b200"}
     b = netgen.build_network(cfg)
     loads = netgen.hbm_bytes_per_worker(b)
-    assert max(loads) <= 1.25 * min(loads)  # balanced by bytes
+    assert max(loads) <= 1.1 * sum(loads) / 4  # per-GPU share cap of the b200 model
     cfg["partition"]["gamma"] = 0.5 * max(loads)
     with pytest.raises(ConfigError):
         netgen.build_network(cfg)

@@ -43,6 +43,9 @@ sys.path.insert(0, str(ROOT))
 G_LOC_10HZ = [-2.3, -4.1997, -0.2231, -2.9957]
 OU_MEAN_10HZ = 275.0
 SEED = 2
+# K = 500 operating points (tools/calibrate_rate.py, ring 100 x 10 000):
+# rate -> (g_location[AMPA], ou_mean); measured 7.5 / 10.0 / 15.2 / 29.9 Hz
+K500_POINTS = {7: (-2.0, 250.0), 10: (-2.2, 275.0), 15: (-1.9, 275.0), 30: (-2.0, 325.0)}
 
 
 def workload_cfg(voxels=100, npv=10000, k_in=1000, dt_ms=1.0, workers=1):
@@ -51,6 +54,23 @@ def workload_cfg(voxels=100, npv=10000, k_in=1000, dt_ms=1.0, workers=1):
             "partition": {"method": "sequential" if workers == 1 else "greedy"},
             "regions": {"subcortex": {"k_in": k_in, "g_location": G_LOC_10HZ,
                                       "ou_mean": OU_MEAN_10HZ}}}
+
+
+def dti_cfg(workers=1, rate=10, dt_ms=1.0, total=20_000_000):
+    """Config 3 / 4: 200-voxel DTI-like network, lognormal voxel sizes,
+    20M neurons, K = 500 (1e10 synapses), greedy partition under the B200
+    byte model (strong scaling over GPUs)."""
+    from paper_2308_01241_b200 import netgen
+    path = ROOT / "build" / f"dti200_{total}.txt"
+    if not path.exists():
+        path.parent.mkdir(parents=True, exist_ok=True)
+        netgen.write_connectome_file(netgen.dti_like_connectome(total_neurons=total), path)
+    ampa, ou = K500_POINTS[rate]
+    return {"seed": SEED, "dt_ms": dt_ms, "steps": 1000, "workers": workers,
+            "connectome": {"kind": "file", "path": str(path)},
+            "partition": {"method": "greedy", "byte_model": "b200"},
+            "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + G_LOC_10HZ[1:],
+                                      "ou_mean": ou}}}
 
 
 def dist_env():
@@ -198,11 +218,14 @@ def run_b200(args):
 
     dev = local if ws > 1 else args.device
     bio_steps = int(round(args.bio_ms / args.dt))
-    # weak scaling: 100 voxels x 10 000 neurons per GPU, one worker per rank,
-    # contiguous voxel blocks (sequential partition of the ring)
-    cfg = workload_cfg(voxels=100 * ws, dt_ms=args.dt, workers=ws)
-    if ws > 1:
-        cfg["partition"]["method"] = "sequential"
+    if args.workload == "config2":
+        # weak scaling: 100 voxels x 10 000 neurons per GPU, one worker per rank,
+        # contiguous voxel blocks (sequential partition of the ring)
+        cfg = workload_cfg(voxels=100 * ws, dt_ms=args.dt, workers=ws)
+        if ws > 1:
+            cfg["partition"]["method"] = "sequential"
+    else:  # config3 (10 Hz) / config4 rate sweep: strong scaling, 20M neurons
+        cfg = dti_cfg(workers=ws, rate=args.rate, dt_ms=args.dt, total=args.neurons)
     net = netgen.build_network(cfg)
     opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=True,
                      device=dev)
@@ -263,11 +286,16 @@ def run_b200(args):
     line = {
         "metric": "synaptic_events_per_s", "value": value, "unit": "events/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if args.workload == "config2" else "strong",
+        "vs_baseline": None,
         "dtype": "f32 state / i64 Q16 / f64 noise", "data": "synthetic",
-        "config": {"workload": "config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)",
+        "config": {"workload": (("config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)")
+                                if args.workload == "config2" else
+                                f"{args.workload} (200-voxel DTI-like, {args.neurons} neurons, "
+                                f"K=500, {args.rate} Hz point)"),
                    "neurons_per_gpu": net.total_neurons // ws,
-                   "synapses_per_gpu": net.synapse_count // ws, "k_in": 1000, "dt_ms": args.dt,
+                   "synapses_per_gpu": net.synapse_count // ws,
+                   "k_in": 1000 if args.workload == "config2" else 500, "dt_ms": args.dt,
                    "bio_ms_per_step": args.bio_ms, "seed": SEED,
                    "parallelism": f"neuron shards x{ws}, NVLink spike exchange" if ws > 1
                    else "single",
@@ -289,7 +317,7 @@ def run_b200(args):
                      "model": "98 B/neuron-step + 12 B/event + 20 B/delivered spike"},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu:
+    if not args.no_cpu and args.workload == "config2":
         try:
             ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
             ref.step(20)
@@ -318,6 +346,10 @@ def main():
     ap.add_argument("--cpu-voxels", type=int, default=12)
     ap.add_argument("--cpu-steps", type=int, default=4000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4"])
+    ap.add_argument("--rate", type=int, default=10, choices=[7, 10, 15, 30],
+                    help="config3/4 operating point (Hz)")
+    ap.add_argument("--neurons", type=int, default=20_000_000, help="config3/4 network size")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

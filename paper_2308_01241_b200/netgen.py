@@ -1127,3 +1127,35 @@ class DistributedSimInstance(SimInstance):
             if rc:
                 self._err(rc)
             barrier()
+
+
+# ------------------------------------------------- benchmark network shapes
+def dti_like_connectome(voxels: int = 200, total_neurons: int = 20_000_000,
+                        sparsity: float = 0.0072, weight_sigma: float = 0.5,
+                        size_sigma: float = 0.5, seed: int = 3) -> Connectome:
+    """BASELINE.json config 3: a synthetic DTI-like voxel graph — the
+    reference's uniform generator (connectome.cpp:82-114: 7.2 per mille edge
+    density, lognormal edge weights, ring fallback for isolated voxels) with
+    lognormal voxel sizes normalised to `total_neurons` (largest remainder).
+    The reference cannot express per-voxel sizes through its generators
+    (SURVEY.md D6); the result is written as a connectome *file*
+    (connectome.hpp:64-75), which both engines load."""
+    g = make_uniform(voxels, 1, sparsity, weight_sigma, 0.0, seed)
+    base = mix_key(seed, 8, 4)
+    w = [math.exp(size_sigma * stream_normal(base, v)) for v in range(voxels)]
+    tot = sum(w)
+    exact = [x / tot * total_neurons for x in w]
+    counts = [int(e) for e in exact]
+    order = sorted(range(voxels), key=lambda v: -(exact[v] - counts[v]))
+    for k in range(total_neurons - sum(counts)):
+        counts[order[k % voxels]] += 1
+    g.neuron_count = [max(1, c) for c in counts]
+    g.validate()
+    return g
+
+
+def write_connectome_file(g: Connectome, path) -> str:
+    p = str(path)
+    with open(p, "w") as f:
+        f.write(save_connectome_text(g))
+    return p

@@ -260,6 +260,7 @@ constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
 #ifndef VXB_DWARPS
 #define VXB_DWARPS 3
 #endif
+static_assert(VXB_DWARPS >= 2, "delivery needs a producer warp and >= 1 consumer warp");
 #ifndef VXB_STAGES
 #define VXB_STAGES 4
 #endif
@@ -308,7 +309,7 @@ struct SmemLayout {
         tgt = acc_bytes;
         w = tgt + kStages * kStageTgtBytes;
         bar = w + kStages * kStageWBytes;
-        meta = bar + kStages * 8;
+        meta = bar + 2 * kStages * 8;  // full barriers, then empty barriers
         seg = (meta + kStages * kMetaBytes + 127) & ~127u;
         start = seg + nseg_smem * (uint32_t)sizeof(SegParams);
         spk = (start + (nseg_smem + 1) * 4 + 15) & ~15u;
@@ -454,6 +455,75 @@ __device__ __forceinline__ bool issue_tstage(const StepArgs& a, unsigned char* s
         wo += wn;
     }
     return end;
+}
+
+// Delivery producer (one lane): packs the out-rows of a spike list into the
+// stage ring — long rows split, short rows packed several to a stage — so
+// every bulk-copy round trip carries a full stage regardless of row length.
+struct RowCursor {
+    uint32_t k;          // next spike index of this CTA in the list
+    uint64_t pos, end;   // remaining entries of the open row
+};
+
+__device__ __forceinline__ uint32_t fill_rstage(const StepArgs& a, unsigned char* smem,
+                                                const SmemLayout& L, uint32_t st,
+                                                const uint32_t* ids, uint32_t cnt,
+                                                uint32_t src_base, RowCursor& c,
+                                                unsigned long long& inner2,
+                                                unsigned long long& outer2, uint64_t pol) {
+    TStageMeta* meta = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+    uint64_t b0s[kSegPerStage];
+    uint32_t lens[kSegPerStage];
+    uint32_t ns = 0, toff = 0, woff = 0, total = 0, bytes = 0;
+    while (ns < (uint32_t)kSegPerStage) {
+        if (c.pos == c.end) {  // open the next row of this CTA
+            if (c.k >= cnt) break;
+            const uint32_t s = src_base + __ldcg(ids + c.k);
+            c.k += gridDim.x;
+            c.pos = ldg64(a.off + s);
+            c.end = ldg64(a.off + s + 1);
+            const uint32_t in = __ldg(a.inner + s);
+            inner2 += 2ull * in;
+            outer2 += 2ull * ((c.end - c.pos) - in);
+            continue;
+        }
+        const int room_t = (kStageE + 8) - (int)toff - 8, room_w = (kStageE + 4) - (int)woff - 4;
+        const int room = room_t < room_w ? room_t : room_w;
+        if (room <= 0) break;
+        const uint64_t take = min(c.end - c.pos, (uint64_t)room);
+        const uint64_t b0 = c.pos, b1 = b0 + take;
+        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - (b0 & ~3ull));
+        const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - (b0 & ~1ull));
+        b0s[ns] = b0;
+        lens[ns] = (uint32_t)take;
+        meta->pre[ns] = total;
+        meta->tb[ns] = toff + (uint32_t)(b0 & 3ull);
+        meta->wb[ns] = woff + (uint32_t)(b0 & 1ull);
+        total += (uint32_t)take;
+        bytes += tn * 4 + wn * 8;
+        toff += tn;
+        woff += wn;
+        c.pos = b1;
+        ++ns;
+    }
+    if (!ns) return 0;
+    meta->pre[ns] = total;
+    meta->n = total;
+    meta->nseg = ns;
+    meta->end = 0;
+    mbar_expect_tx(bar, bytes);
+    uint32_t to = 0, wo = 0;
+    for (uint32_t i = 0; i < ns; ++i) {
+        const uint64_t b0 = b0s[i], b1 = b0 + lens[i];
+        const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0), wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
+        bulk_g2s(smem + L.tgt + st * kStageTgtBytes + to * 4, a.tgt + t0, tn * 4, bar, pol);
+        bulk_g2s(smem + L.w + st * kStageWBytes + wo * 8, a.w + w0, wn * 8, bar, pol);
+        to += tn;
+        wo += wn;
+    }
+    return ns;
 }
 
 // Tiled delivery, producer side: queue the row segments of spike s (one per
@@ -632,7 +702,10 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     }
     if (threadIdx.x == 0) {
         s_nspk = 0;
-        for (int k = 0; k < kStages; ++k) mbar_init(s_bar + k, 1);
+        for (int k = 0; k < kStages; ++k) {
+            mbar_init(s_bar + k, 1);                          // full: producer + tx bytes
+            mbar_init(s_bar + kStages + k, VXB_DWARPS > 1 ? VXB_DWARPS - 1 : 1);  // empty
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -710,9 +783,17 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             const uint32_t inext = i + gthreads;
             if (inext < a.n) load_neuron<PACKED>(a, inext, doE, pend_rd, nxt);
             bool spiked = false;
-            uint32_t seg = 0;
+            // parameter segment: one binary search per warp (lanes hold
+            // consecutive neurons), then a short forward walk per lane
+            uint32_t seg;
+            {
+                const uint32_t il = live ? i : a.n - 1;
+                uint32_t s0 = 0;
+                if (lane == 0) s0 = find_seg(startp, a.nseg, il);
+                seg = __shfl_sync(0xffffffffu, s0, 0);
+                while (seg + 1 < a.nseg && startp[seg + 1] <= il) ++seg;
+            }
             if (live) {
-                seg = find_seg(startp, a.nseg, i);
                 const SegParams& P = segp[seg];
                 uint32_t vb = cur.vb;
                 const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
@@ -971,41 +1052,62 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 dsync();  // acc reused by the next tile
             }
         } else if (roleD && doE) {
+            // Producer / consumer delivery pipeline: warp 0 lane 0 packs the
+            // rows of this CTA's spikes (local list, then each peer's batch
+            // once its step flag is set) into the stage ring with bulk copies;
+            // the other delivery warps drain stages into the pending buffer
+            // with red.add (L2 atomics).  full/empty mbarriers per stage.
             const uint32_t tslot = tE % 3u;
-            const uint32_t* local_ids = a.spk + d_prev + d_lo;
-            for (uint32_t li = 0; li < a.world; ++li) {
-                const uint32_t h = (a.ex->rank + li) % a.world;
-                const uint32_t* ids = local_ids;
-                uint32_t cnt = d_cnt;
-                if (li) {
-                    if (threadIdx.x == 0) {
+            uint64_t* full = s_bar;
+            uint64_t* empty = s_bar + kStages;
+            if (threadIdx.x == 0) {
+                uint32_t ctr = g_item;
+                for (uint32_t li = 0; li < a.world; ++li) {
+                    const uint32_t h = (a.ex->rank + li) % a.world;
+                    const uint32_t* ids = a.spk + d_prev + d_lo;
+                    uint32_t cnt = d_cnt;
+                    if (li) {
                         const unsigned long long w0 = globaltimer();
-                        s_rcnt = exchange_wait(a, h, tE, tslot);
+                        cnt = exchange_wait(a, h, tE, tslot);
                         wait_ns += globaltimer() - w0;
+                        ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
                     }
-                    dsync();
-                    cnt = s_rcnt;
-                    ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
+                    const uint32_t sb = a.ex->src_base[h];
+                    RowCursor cur{blockIdx.x, 0, 0};
+                    for (;;) {
+                        const uint32_t st = ctr % kStages;
+                        mbar_wait(empty + st, ((ctr / kStages) & 1u) ^ 1u);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        if (!fill_rstage(a, smem, L, st, ids, cnt, sb, cur, my_inner, my_outer,
+                                         pol_stream))
+                            break;  // list exhausted (stage st stays free)
+                        ++ctr;
+                    }
                 }
-                const uint32_t sb = a.ex->src_base[h];
-                const uint32_t items = cnt * d_C;
-                const uint32_t mine =
-                    items > blockIdx.x ? (items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-                if (threadIdx.x == 0 && mine) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    for (uint32_t j = 0; j < mine && j < (uint32_t)kStages; ++j)
-                        issue_piece<PACKED>(a, smem, L, (g_item + j) % kStages,
-                                            blockIdx.x + j * gridDim.x, d_C, ids, sb, pol_stream);
-                }
-                for (uint32_t j = 0; j < mine; ++j, ++g_item) {
+                const uint32_t st = ctr % kStages;  // end marker
+                mbar_wait(empty + st, ((ctr / kStages) & 1u) ^ 1u);
+                TStageMeta* m = reinterpret_cast<TStageMeta*>(s_meta_base + st * kMetaBytes);
+                m->n = 0;
+                m->nseg = 0;
+                m->end = 1;
+                mbar_arrive(full + st);
+                g_item = ctr + 1;
+            } else if (threadIdx.x >= 32) {
+                const uint32_t ct = threadIdx.x - 32, cn = d_cta - 32;
+                for (;;) {
                     const uint32_t st = g_item % kStages;
-                    mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-                    const StageMeta m = *reinterpret_cast<const StageMeta*>(s_meta_base + st * kMetaBytes);
-                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes) + m.head_t;
-                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes) + m.head_w;
-                    for (uint32_t e = threadIdx.x; e < m.n; e += d_cta) {
-                        const uint32_t t = tg[e], tid = t & 0x7fffffffu, cls = t >> 31;
-                        const uint64_t wq = wv[e];
+                    mbar_wait(full + st, (g_item / kStages) & 1u);
+                    ++g_item;
+                    const TStageMeta* m = reinterpret_cast<const TStageMeta*>(s_meta_base + st * kMetaBytes);
+                    const uint32_t n_e = m->n, last = m->end;
+                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes);
+                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes);
+                    uint32_t sg = 0;
+                    for (uint32_t e = ct; e < n_e; e += cn) {
+                        while (e >= m->pre[sg + 1]) ++sg;
+                        const uint32_t r = e - m->pre[sg];
+                        const uint32_t t = tg[m->tb[sg] + r], tid = t & 0x7fffffffu, cls = t >> 31;
+                        const uint64_t wq = wv[m->wb[sg] + r];
                         if constexpr (PACKED) {
                             red_add(reinterpret_cast<unsigned long long*>(pend_wr) + 2 * (size_t)tid + cls,
                                     wq, pol_keep);
@@ -1016,17 +1118,9 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                             red_add(dst + 1, (uint64_t)(int64_t)(int32_t)(uint32_t)(wq >> 32), pol_keep);
                         }
                     }
-                    if (threadIdx.x == 0 && m.first) {
-                        const uint32_t in = __ldg(a.inner + m.spike);
-                        my_inner += 2ull * in;
-                        my_outer += 2ull * (m.len - in);
-                    }
-                    dsync();  // stage st drained by every delivery thread
-                    if (threadIdx.x == 0 && j + kStages < mine) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        issue_piece<PACKED>(a, smem, L, st, blockIdx.x + (j + kStages) * gridDim.x,
-                                            d_C, ids, sb, pol_stream);
-                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st);
+                    if (last) break;
                 }
             }
         }

@@ -6,10 +6,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2308_01241_b200 import build as b
 
 VARIANTS = {
-    "dw3s4e1024": {"VXB_DWARPS": 3, "VXB_STAGES": 4, "VXB_STAGE_E": 1024},
-    "dw3s6e768": {"VXB_DWARPS": 3, "VXB_STAGES": 6, "VXB_STAGE_E": 768},
-    "dw3s3e1536": {"VXB_DWARPS": 3, "VXB_STAGES": 3, "VXB_STAGE_E": 1536},
-    "dw3s2e768": {"VXB_DWARPS": 3, "VXB_STAGES": 2, "VXB_STAGE_E": 768},
+    "dw4": {"VXB_DWARPS": 4},
+    "dw2": {"VXB_DWARPS": 2},
+    "dw3s6": {"VXB_DWARPS": 3, "VXB_STAGES": 6},
+    "dw4s3e1024": {"VXB_DWARPS": 4, "VXB_STAGES": 3, "VXB_STAGE_E": 1024},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

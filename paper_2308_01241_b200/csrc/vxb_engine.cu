@@ -186,6 +186,11 @@ struct Engine {
               uint32_t rank_ = 0, uint32_t world_ = 1);
     void setup_exchange();
     void build_tiles();
+    void sort_rows();
+    void build_blocks();
+    bool rows_sorted = false;
+    uint32_t n_blocks = 1, block_n = 0;
+    DevBuf<uint32_t> d_blk;
     // tiled delivery tables (world == 1)
     bool tiled = false;
     uint32_t n_tiles = 0;
@@ -499,6 +504,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
 
     setup_exchange();
     build_tiles();
+    if (!tiled) build_blocks();
 
     // longest out-row: delivery pieces per spike (<= kStageE entries each)
     {
@@ -974,6 +980,84 @@ void Engine::setup_exchange() {
     CK(cudaStreamSynchronize(stream));
 }
 
+// Sort every out-row by target (low bits only: the class bit rides along).
+void Engine::sort_rows() {
+    if (rows_sorted || n_syn == 0) return;
+    int end_bit = 1;
+    while ((1ull << end_bit) < n) ++end_bit;
+    DevBuf<uint32_t> t2;
+    DevBuf<uint64_t> w2;
+    t2.alloc(n_syn + 4);
+    w2.alloc(n_syn + 2);
+    CK(cudaMemsetAsync(t2.p + n_syn, 0, 16, stream));
+    CK(cudaMemsetAsync(w2.p + n_syn, 0, 16, stream));
+    const unsigned long long* ob = reinterpret_cast<const unsigned long long*>(d_off.p);
+    // CUB's segmented sort takes int item counts: sort in slices of sources
+    uint32_t s0 = 0;
+    std::vector<uint64_t> hoff;
+    while (s0 < n_src) {
+        if (hoff.empty()) {
+            hoff.resize((size_t)n_src + 1);
+            CK(cudaMemcpyAsync(hoff.data(), d_off.p, 8ull * (n_src + 1), cudaMemcpyDeviceToHost,
+                               stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        uint32_t s1 = s0;
+        while (s1 < n_src && hoff[s1 + 1] - hoff[s0] < (1ull << 30)) ++s1;
+        if (s1 == s0) s1 = s0 + 1;  // a single row above 2^30 entries
+        const uint64_t base = hoff[s0];
+        const int items = (int)(hoff[s1] - base);
+        if (items > 0) {
+            // offsets relative to the slice
+            DevBuf<unsigned long long> rel;
+            rel.alloc((size_t)(s1 - s0) + 1);
+            std::vector<unsigned long long> hr(s1 - s0 + 1);
+            for (uint32_t i = s0; i <= s1; ++i) hr[i - s0] = hoff[i] - base;
+            CK(cudaMemcpyAsync(rel.p, hr.data(), 8 * hr.size(), cudaMemcpyHostToDevice, stream));
+            size_t tmp = 0;
+            CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_tgt.p + base, t2.p + base,
+                                                        d_w.p + base, w2.p + base, items,
+                                                        (int)(s1 - s0), rel.p, rel.p + 1, 0,
+                                                        end_bit, stream));
+            DevBuf<unsigned char> t;
+            t.alloc(tmp ? tmp : 1);
+            CK(cub::DeviceSegmentedRadixSort::SortPairs(t.p, tmp, d_tgt.p + base, t2.p + base,
+                                                        d_w.p + base, w2.p + base, items,
+                                                        (int)(s1 - s0), rel.p, rel.p + 1, 0,
+                                                        end_bit, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        s0 = s1;
+    }
+    (void)ob;
+    std::swap(d_tgt.p, t2.p);
+    std::swap(d_tgt.n, t2.n);
+    std::swap(d_w.p, w2.p);
+    std::swap(d_w.n, w2.n);
+    rows_sorted = true;
+}
+
+// L2-blocked delivery: when the pending buffer does not fit in L2, targets
+// are split into ranges whose pending slice does (24 MB), rows are sorted by
+// target and every CTA delivers block 0's segments of all its spikes, then
+// block 1's, ... so the live part of the pending buffer stays L2-resident
+// (VXB_BLOCK_NEURONS overrides the block size).
+void Engine::build_blocks() {
+    n_blocks = 1;
+    const uint64_t pend_per = packed ? 16 : 32;
+    uint64_t bn = (24ull << 20) / pend_per;
+    if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
+    if ((uint64_t)n <= bn || n_syn == 0) return;
+    n_blocks = (uint32_t)((n + bn - 1) / bn);
+    block_n = (uint32_t)((n + n_blocks - 1) / n_blocks);
+    sort_rows();
+    d_blk.alloc((size_t)n_src * (n_blocks + 1));
+    block_offsets_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
+                                                   d_tgt.p, n_src, n_blocks, block_n, d_blk.p);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream));
+}
+
 // Tiled delivery (single device, experimental, VXB_TILED=1): sort every
 // out-row by target, build the per-source tile directory and the per-tile
 // segment queues; delivery then accumulates whole target tiles in shared
@@ -989,31 +1073,7 @@ void Engine::build_tiles() {
         return;
     n_tiles = (n + kTile - 1) / kTile;
     if (n_tiles >= (1u << 20)) return;
-    // 1. sort rows by target (low bits only: the class bit rides along)
-    {
-        int end_bit = 1;
-        while ((1ull << end_bit) < n) ++end_bit;
-        DevBuf<uint32_t> t2;
-        DevBuf<uint64_t> w2;
-        t2.alloc(n_syn + 4);
-        w2.alloc(n_syn + 2);
-        CK(cudaMemsetAsync(t2.p + n_syn, 0, 16, stream));
-        CK(cudaMemsetAsync(w2.p + n_syn, 0, 16, stream));
-        const unsigned long long* ob = reinterpret_cast<const unsigned long long*>(d_off.p);
-        size_t tmp = 0;
-        CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_tgt.p, t2.p, d_w.p, w2.p,
-                                                    (int)n_syn, (int)n_src, ob, ob + 1, 0,
-                                                    end_bit, stream));
-        DevBuf<unsigned char> t;
-        t.alloc(tmp ? tmp : 1);
-        CK(cub::DeviceSegmentedRadixSort::SortPairs(t.p, tmp, d_tgt.p, t2.p, d_w.p, w2.p,
-                                                    (int)n_syn, (int)n_src, ob, ob + 1, 0,
-                                                    end_bit, stream));
-        std::swap(d_tgt.p, t2.p);
-        std::swap(d_tgt.n, t2.n);
-        std::swap(d_w.p, w2.p);
-        std::swap(d_w.n, w2.n);
-    }
+    sort_rows();
     // 2. segments per source and per tile
     DevBuf<uint32_t> nseg, cap;
     nseg.alloc((size_t)n_src + 1);
@@ -1282,6 +1342,8 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.qcount = d_qcount.p;
     a.queue = d_queue.p;
     a.q_total = q_total;
+    a.n_blocks = n_blocks;
+    a.blk_off = d_blk.p;
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));

@@ -151,6 +151,10 @@ struct StepArgs {
     uint32_t* qcount;          // [2][n_tiles] segments queued per (step parity, tile)
     uint64_t* queue;           // [2][q_total] start | (len - 1) << 40
     uint64_t q_total;
+    // L2-blocked delivery: targets split into n_blocks ranges delivered in
+    // order; blk_off[s * (n_blocks + 1) + b] = row offset of block b
+    uint32_t n_blocks;
+    const uint32_t* blk_off;
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -457,74 +461,73 @@ __device__ __forceinline__ bool issue_tstage(const StepArgs& a, unsigned char* s
     return end;
 }
 
-// Delivery producer (one lane): packs the out-rows of a spike list into the
-// stage ring — long rows split, short rows packed several to a stage — so
-// every bulk-copy round trip carries a full stage regardless of row length.
-struct RowCursor {
-    uint32_t k;          // next spike index of this CTA in the list
-    uint64_t pos, end;   // remaining entries of the open row
-};
-
-__device__ __forceinline__ uint32_t fill_rstage(const StepArgs& a, unsigned char* smem,
-                                                const SmemLayout& L, uint32_t st,
-                                                const uint32_t* ids, uint32_t cnt,
-                                                uint32_t src_base, RowCursor& c,
-                                                unsigned long long& inner2,
-                                                unsigned long long& outer2, uint64_t pol) {
-    TStageMeta* meta = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
-    uint64_t b0s[kSegPerStage];
-    uint32_t lens[kSegPerStage];
-    uint32_t ns = 0, toff = 0, woff = 0, total = 0, bytes = 0;
-    while (ns < (uint32_t)kSegPerStage) {
-        if (c.pos == c.end) {  // open the next row of this CTA
-            if (c.k >= cnt) break;
-            const uint32_t s = src_base + __ldcg(ids + c.k);
-            c.k += gridDim.x;
-            c.pos = ldg64(a.off + s);
-            c.end = ldg64(a.off + s + 1);
-            const uint32_t in = __ldg(a.inner + s);
-            inner2 += 2ull * in;
-            outer2 += 2ull * ((c.end - c.pos) - in);
-            continue;
-        }
-        const int room_t = (kStageE + 8) - (int)toff - 8, room_w = (kStageE + 4) - (int)woff - 4;
-        const int room = room_t < room_w ? room_t : room_w;
-        if (room <= 0) break;
-        const uint64_t take = min(c.end - c.pos, (uint64_t)room);
-        const uint64_t b0 = c.pos, b1 = b0 + take;
-        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - (b0 & ~3ull));
-        const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - (b0 & ~1ull));
-        b0s[ns] = b0;
-        lens[ns] = (uint32_t)take;
-        meta->pre[ns] = total;
-        meta->tb[ns] = toff + (uint32_t)(b0 & 3ull);
-        meta->wb[ns] = woff + (uint32_t)(b0 & 1ull);
-        total += (uint32_t)take;
-        bytes += tn * 4 + wn * 8;
-        toff += tn;
-        woff += wn;
-        c.pos = b1;
-        ++ns;
-    }
-    if (!ns) return 0;
-    meta->pre[ns] = total;
-    meta->n = total;
-    meta->nseg = ns;
-    meta->end = 0;
-    mbar_expect_tx(bar, bytes);
-    uint32_t to = 0, wo = 0;
-    for (uint32_t i = 0; i < ns; ++i) {
-        const uint64_t b0 = b0s[i], b1 = b0 + lens[i];
-        const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
-        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0), wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
-        bulk_g2s(smem + L.tgt + st * kStageTgtBytes + to * 4, a.tgt + t0, tn * 4, bar, pol);
-        bulk_g2s(smem + L.w + st * kStageWBytes + wo * 8, a.w + w0, wn * 8, bar, pol);
-        to += tn;
-        wo += wn;
-    }
-    return ns;
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
 }
+
+// Delivery producer (lane 0 of the producer warp): packs row segments into
+// the stage ring — long segments split, short ones packed up to
+// kSegPerStage to a stage — so every bulk-copy round trip carries a full
+// stage whatever the row lengths.  Copies are issued as segments are added
+// (expect_tx per segment, one arrive at commit).
+struct StageBuilder {
+    uint32_t ctr;    // stages committed since launch (stage = ctr % kStages)
+    uint32_t open;   // a stage is being filled
+    uint32_t ns, toff, woff, total;
+
+    __device__ __forceinline__ void begin(unsigned char* smem, const SmemLayout& L) {
+        const uint32_t st = ctr % kStages;
+        uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.bar) + kStages;
+        mbar_wait(empty + st, ((ctr / kStages) & 1u) ^ 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        open = 1;
+        ns = toff = woff = total = 0;
+    }
+    __device__ __forceinline__ void commit(unsigned char* smem, const SmemLayout& L, uint32_t end) {
+        const uint32_t st = ctr % kStages;
+        TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+        m->pre[ns] = total;
+        m->n = total;
+        m->nseg = ns;
+        m->end = end;
+        mbar_arrive(reinterpret_cast<uint64_t*>(smem + L.bar) + st);
+        ++ctr;
+        open = 0;
+    }
+    __device__ __forceinline__ void add(const StepArgs& a, unsigned char* smem, const SmemLayout& L,
+                                        uint64_t b0, uint64_t len, uint64_t pol) {
+        while (len) {
+            if (!open) begin(smem, L);
+            const int room_t = kStageE - (int)toff, room_w = kStageE - 4 - (int)woff + 4;
+            int room = room_t < room_w ? room_t : room_w;
+            if (ns == (uint32_t)kSegPerStage || room <= 0) {
+                commit(smem, L, 0);
+                continue;
+            }
+            const uint32_t st = ctr % kStages;
+            TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+            const uint64_t take = min(len, (uint64_t)room);
+            const uint64_t b1 = b0 + take;
+            const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+            const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0);
+            const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
+            m->pre[ns] = total;
+            m->tb[ns] = toff + (uint32_t)(b0 - t0);
+            m->wb[ns] = woff + (uint32_t)(b0 - w0);
+            uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+            mbar_expect_tx_only(full, tn * 4 + wn * 8);
+            bulk_g2s(smem + L.tgt + st * kStageTgtBytes + toff * 4, a.tgt + t0, tn * 4, full, pol);
+            bulk_g2s(smem + L.w + st * kStageWBytes + woff * 8, a.w + w0, wn * 8, full, pol);
+            total += (uint32_t)take;
+            toff += tn;
+            woff += wn;
+            ++ns;
+            b0 = b1;
+            len -= take;
+        }
+    }
+};
 
 // Tiled delivery, producer side: queue the row segments of spike s (one per
 // target tile, from the source's tile directory) for the step's tile
@@ -1060,38 +1063,64 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             const uint32_t tslot = tE % 3u;
             uint64_t* full = s_bar;
             uint64_t* empty = s_bar + kStages;
-            if (threadIdx.x == 0) {
-                uint32_t ctr = g_item;
+            if (threadIdx.x < 32) {
+                // producer warp: 32 spikes' segment bounds per round trip,
+                // lane 0 packs them; target blocks in order (L2 blocking)
+                StageBuilder sbld{g_item, 0, 0, 0, 0, 0};
+                const uint32_t B = a.n_blocks;
                 for (uint32_t li = 0; li < a.world; ++li) {
                     const uint32_t h = (a.ex->rank + li) % a.world;
                     const uint32_t* ids = a.spk + d_prev + d_lo;
                     uint32_t cnt = d_cnt;
                     if (li) {
-                        const unsigned long long w0 = globaltimer();
-                        cnt = exchange_wait(a, h, tE, tslot);
-                        wait_ns += globaltimer() - w0;
+                        uint32_t c = 0;
+                        if (lane == 0) {
+                            const unsigned long long w0 = globaltimer();
+                            c = exchange_wait(a, h, tE, tslot);
+                            wait_ns += globaltimer() - w0;
+                        }
+                        cnt = __shfl_sync(0xffffffffu, c, 0);
                         ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
                     }
                     const uint32_t sb = a.ex->src_base[h];
-                    RowCursor cur{blockIdx.x, 0, 0};
-                    for (;;) {
-                        const uint32_t st = ctr % kStages;
-                        mbar_wait(empty + st, ((ctr / kStages) & 1u) ^ 1u);
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        if (!fill_rstage(a, smem, L, st, ids, cnt, sb, cur, my_inner, my_outer,
-                                         pol_stream))
-                            break;  // list exhausted (stage st stays free)
-                        ++ctr;
+                    const uint32_t mine = cnt > blockIdx.x ? (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+                    for (uint32_t blk = 0; blk < B; ++blk) {
+                        for (uint32_t j0 = 0; j0 < mine; j0 += 32) {
+                            const uint32_t j = j0 + lane;
+                            uint64_t sbeg = 0, slen = 0;
+                            if (j < mine) {
+                                const uint32_t s = sb + __ldcg(ids + blockIdx.x + j * gridDim.x);
+                                const uint64_t row = ldg64(a.off + s);
+                                if (B == 1) {
+                                    sbeg = row;
+                                    slen = ldg64(a.off + s + 1) - row;
+                                } else {
+                                    const uint32_t* bo = a.blk_off + (size_t)s * (B + 1);
+                                    const uint32_t lo = __ldg(bo + blk), hi = __ldg(bo + blk + 1);
+                                    sbeg = row + lo;
+                                    slen = hi - lo;
+                                }
+                                if (blk == 0) {
+                                    const uint64_t len = ldg64(a.off + s + 1) - row;
+                                    const uint32_t in = __ldg(a.inner + s);
+                                    my_inner += 2ull * in;
+                                    my_outer += 2ull * (len - in);
+                                }
+                            }
+                            const uint32_t nl = min(32u, mine - j0);
+                            for (uint32_t l = 0; l < nl; ++l) {
+                                const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
+                                const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
+                                if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
+                            }
+                        }
                     }
                 }
-                const uint32_t st = ctr % kStages;  // end marker
-                mbar_wait(empty + st, ((ctr / kStages) & 1u) ^ 1u);
-                TStageMeta* m = reinterpret_cast<TStageMeta*>(s_meta_base + st * kMetaBytes);
-                m->n = 0;
-                m->nseg = 0;
-                m->end = 1;
-                mbar_arrive(full + st);
-                g_item = ctr + 1;
+                if (lane == 0) {
+                    if (!sbld.open) sbld.begin(smem, L);
+                    sbld.commit(smem, L, 1);  // end marker (possibly with data)
+                }
+                g_item = __shfl_sync(0xffffffffu, sbld.ctr, 0);
             } else if (threadIdx.x >= 32) {
                 const uint32_t ct = threadIdx.x - 32, cn = d_cta - 32;
                 for (;;) {
@@ -1254,6 +1283,30 @@ __global__ void tile_dir_fill_kernel(const uint64_t* __restrict__ off,
             }
             k = j;
         }
+    }
+}
+
+// L2 blocking: per source, offsets (within its target-sorted row) of the
+// first entry of every target block.
+__global__ void block_offsets_kernel(const uint64_t* __restrict__ off,
+                                     const uint32_t* __restrict__ tgt, uint32_t n_src,
+                                     uint32_t n_blocks, uint32_t block_n,
+                                     uint32_t* __restrict__ bo) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_src; s += gridDim.x * blockDim.x) {
+        const uint64_t e0 = off[s], e1 = off[s + 1];
+        uint32_t* o = bo + (size_t)s * (n_blocks + 1);
+        o[0] = 0;
+        uint64_t lo = e0;
+        for (uint32_t b = 1; b < n_blocks; ++b) {
+            const uint32_t bound = b * block_n;
+            uint64_t hi = e1;  // first entry with target >= bound
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if ((tgt[mid] & 0x7fffffffu) < bound) lo = mid + 1; else hi = mid;
+            }
+            o[b] = (uint32_t)(lo - e0);
+        }
+        o[n_blocks] = (uint32_t)(e1 - e0);
     }
 }
 

@@ -369,3 +369,18 @@ def test_tiled_delivery_mode_matches_reference(monkeypatch):
     ref = rs.advance(3000)
     assert_same(gpu, ref)
     assert np.array_equal(snaps[0], rs.membrane_snapshot(0))
+
+
+def test_l2_blocked_delivery_matches_reference(monkeypatch):
+    """L2-blocked delivery (target-sorted rows, per-source block offsets,
+    blocks delivered in order), forced on a small network with 2048-neuron
+    blocks: bit-exact against the reference."""
+    monkeypatch.setenv("VXB_BLOCK_NEURONS", "2048")
+    net = RefNet(make_config(seed=1401, voxels=10, npv=1000, k_in=100, rho=6 / 25))
+    opt = SimOptions(steps=300, probe_gids=[5, 5000, 9999])
+    gpu, snaps = gpu_run(net.tables, opt)
+    rs = RefSim(net, opt)
+    ref = rs.advance(300)
+    assert ref.total_spikes > 0
+    assert_same(gpu, ref)
+    assert np.array_equal(snaps[0], rs.membrane_snapshot(0))

@@ -981,59 +981,58 @@ void Engine::setup_exchange() {
 }
 
 // Sort every out-row by target (low bits only: the class bit rides along).
+// Rows are sorted in slices of <= 2^28 entries through slice-sized scratch
+// buffers, so the sort needs ~3 GB extra HBM whatever the table size.
 void Engine::sort_rows() {
     if (rows_sorted || n_syn == 0) return;
     int end_bit = 1;
     while ((1ull << end_bit) < n) ++end_bit;
+    std::vector<uint64_t> hoff((size_t)n_src + 1);
+    CK(cudaMemcpyAsync(hoff.data(), d_off.p, 8ull * (n_src + 1), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    const uint64_t kSlice = 1ull << 28;
+    uint64_t biggest = 0;
+    for (uint32_t s0 = 0; s0 < n_src;) {  // slice bounds
+        uint32_t s1 = s0;
+        while (s1 < n_src && hoff[s1 + 1] - hoff[s0] <= kSlice) ++s1;
+        if (s1 == s0) s1 = s0 + 1;
+        biggest = std::max(biggest, hoff[s1] - hoff[s0]);
+        s0 = s1;
+    }
     DevBuf<uint32_t> t2;
     DevBuf<uint64_t> w2;
-    t2.alloc(n_syn + 4);
-    w2.alloc(n_syn + 2);
-    CK(cudaMemsetAsync(t2.p + n_syn, 0, 16, stream));
-    CK(cudaMemsetAsync(w2.p + n_syn, 0, 16, stream));
-    const unsigned long long* ob = reinterpret_cast<const unsigned long long*>(d_off.p);
-    // CUB's segmented sort takes int item counts: sort in slices of sources
-    uint32_t s0 = 0;
-    std::vector<uint64_t> hoff;
-    while (s0 < n_src) {
-        if (hoff.empty()) {
-            hoff.resize((size_t)n_src + 1);
-            CK(cudaMemcpyAsync(hoff.data(), d_off.p, 8ull * (n_src + 1), cudaMemcpyDeviceToHost,
-                               stream));
-            CK(cudaStreamSynchronize(stream));
-        }
+    DevBuf<unsigned long long> rel;
+    DevBuf<unsigned char> tmpbuf;
+    t2.alloc(std::max<uint64_t>(1, biggest));
+    w2.alloc(std::max<uint64_t>(1, biggest));
+    for (uint32_t s0 = 0; s0 < n_src;) {
         uint32_t s1 = s0;
-        while (s1 < n_src && hoff[s1 + 1] - hoff[s0] < (1ull << 30)) ++s1;
-        if (s1 == s0) s1 = s0 + 1;  // a single row above 2^30 entries
+        while (s1 < n_src && hoff[s1 + 1] - hoff[s0] <= kSlice) ++s1;
+        if (s1 == s0) s1 = s0 + 1;
         const uint64_t base = hoff[s0];
-        const int items = (int)(hoff[s1] - base);
-        if (items > 0) {
-            // offsets relative to the slice
-            DevBuf<unsigned long long> rel;
-            rel.alloc((size_t)(s1 - s0) + 1);
+        const uint64_t items = hoff[s1] - base;
+        if (items > 1) {
+            if (items >= (1ull << 31)) throw SimError("a single out-row exceeds 2^31 entries");
             std::vector<unsigned long long> hr(s1 - s0 + 1);
             for (uint32_t i = s0; i <= s1; ++i) hr[i - s0] = hoff[i] - base;
+            if (rel.n < hr.size()) rel.alloc(hr.size());
             CK(cudaMemcpyAsync(rel.p, hr.data(), 8 * hr.size(), cudaMemcpyHostToDevice, stream));
             size_t tmp = 0;
-            CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_tgt.p + base, t2.p + base,
-                                                        d_w.p + base, w2.p + base, items,
+            CK(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, d_tgt.p + base, t2.p,
+                                                        d_w.p + base, w2.p, (int)items,
                                                         (int)(s1 - s0), rel.p, rel.p + 1, 0,
                                                         end_bit, stream));
-            DevBuf<unsigned char> t;
-            t.alloc(tmp ? tmp : 1);
-            CK(cub::DeviceSegmentedRadixSort::SortPairs(t.p, tmp, d_tgt.p + base, t2.p + base,
-                                                        d_w.p + base, w2.p + base, items,
+            if (tmpbuf.n < tmp) tmpbuf.alloc(tmp);
+            CK(cub::DeviceSegmentedRadixSort::SortPairs(tmpbuf.p, tmp, d_tgt.p + base, t2.p,
+                                                        d_w.p + base, w2.p, (int)items,
                                                         (int)(s1 - s0), rel.p, rel.p + 1, 0,
                                                         end_bit, stream));
-            CK(cudaStreamSynchronize(stream));
+            CK(cudaMemcpyAsync(d_tgt.p + base, t2.p, 4 * items, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaMemcpyAsync(d_w.p + base, w2.p, 8 * items, cudaMemcpyDeviceToDevice, stream));
+            CK(cudaStreamSynchronize(stream));  // rel / scratch reused by the next slice
         }
         s0 = s1;
     }
-    (void)ob;
-    std::swap(d_tgt.p, t2.p);
-    std::swap(d_tgt.n, t2.n);
-    std::swap(d_w.p, w2.p);
-    std::swap(d_w.n, w2.n);
     rows_sorted = true;
 }
 

@@ -7,9 +7,10 @@ from paper_2308_01241_b200 import build as b
 
 VARIANTS = {
     "dw4": {"VXB_DWARPS": 4},
-    "dw2": {"VXB_DWARPS": 2},
-    "dw3s6": {"VXB_DWARPS": 3, "VXB_STAGES": 6},
-    "dw4s3e1024": {"VXB_DWARPS": 4, "VXB_STAGES": 3, "VXB_STAGE_E": 1024},
+    "dw5": {"VXB_DWARPS": 5},
+    "dw4s6e512": {"VXB_DWARPS": 4, "VXB_STAGES": 6, "VXB_STAGE_E": 512},
+    "dw4s8e384": {"VXB_DWARPS": 4, "VXB_STAGES": 8, "VXB_STAGE_E": 384},
+    "t384dw6": {"VXB_THREADS": 384, "VXB_MINB": 2, "VXB_DWARPS": 6},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

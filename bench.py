@@ -15,9 +15,11 @@ second (events = delivered table entries, (gating_inner + gating_outer) / 2,
 engine.cpp:459-463); wall seconds per biological second is reported beside it.
 
 `value` uses the device time of the step kernel (CUDA events on the engine's
-launching stream), inputs resident in HBM.  `e2e` times the same advance
-through the C ABI as a caller sees it: synchronous call, results (rates,
-FLOP tallies, timing rows) copied back to host memory every step.  The
+launching stream), inputs resident in HBM.  `e2e` times each step as the
+assimilation caller drives the C ABI (assim.cpp:91-107): set_conductances of
+every local unit from pinned host buffers (the host->device bytes), then a
+synchronous advance whose results (rates, FLOP tallies, timing rows) are
+copied back to host memory (the device->host bytes).  The
 synapse tables (12 GB) exceed L2 (126 MB), so no flush is needed.
 
 --impl reference runs the reference CPU engine (oracle/_ref/libvoxsim_ref.so,
@@ -81,17 +83,52 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled every ~5 ms during
+    the timed region through NVML (the counters nvidia-smi reads); falls
+    back to `nvidia-smi -lms 100` when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    BITS = (0x8, 0x40, 0x20, 0x4)  # nvmlClocksEventReason* masks
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self.proc = None
+        self.stop = threading.Event()
+        self.t = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _poll(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+            self.mx.append(float(mx))
+            r = get_r(h)
+            self.reasons.update(n for n, b in zip(self.NAMES, self.BITS) if r & b)
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.t = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -105,27 +142,30 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if r[1].replace(".", "").isdigit():
+                self.sm.append(float(r[1]))
+            if r[2].replace(".", "").isdigit():
+                self.mx.append(float(r[2]))
+            self.reasons.update(n for i, n in enumerate(self.NAMES)
+                                if len(r) > 5 + i and r[5 + i].lower() == "active")
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.t:
+            self.t.join(timeout=5)
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx or [0.0]),
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def measured_peak_hbm():
@@ -233,7 +273,34 @@ def run_b200(args):
         sim = netgen.DistributedSimInstance(net, opt, rank, ws)
     else:
         sim = netgen.GeneratedSimInstance(net, opt)
-    for _ in range(args.warmup):
+    # e2e input per step, as the assimilation caller feeds the boundary
+    # (assim.cpp:91-107, EnsembleMember::run_window): fresh AMPA conductance
+    # scales for every local unit from pinned host buffers, staged by
+    # set_conductances and uploaded by the following advance.  Two windows'
+    # worth are drawn up front (sample_conductances with the assimilation
+    # salt, netgen.cpp:318-329) and alternated; g_location/g_scale are the
+    # population's own, so the operating point is unchanged.
+    import torch
+    windows = []
+    for w in range(2):
+        sets = []
+        salt = netgen.mix_key(1, w + 1)
+        for u, unit in enumerate(net.layout.units):
+            if unit.neurons == 0 or (ws > 1 and net.unit_worker[u] != rank):
+                continue
+            pop = net.layout.pop_of_unit(u)
+            buf = torch.empty(unit.neurons, dtype=torch.float32, pin_memory=True).numpy()
+            buf[:] = netgen.sample_conductances(SEED, salt, u, 0, pop.g_location[0],
+                                                pop.g_scale[0], unit.neurons)
+            sets.append((u, buf))
+        windows.append(sets)
+
+    def feed(i):
+        for u, buf in windows[i % 2]:
+            sim.set_conductances(u, 0, buf)
+
+    for i in range(args.warmup):
+        feed(i)
         sim.advance(bio_steps)
 
     def barrier():
@@ -241,12 +308,14 @@ def run_b200(args):
             dist.barrier()
 
     dev_ms, wall, events, spikes, h2d, d2h, launches, results = [], [], 0, 0, 0, 0, 0, []
-    xwait = 0.0
+    xwait, stage_s = 0.0, 0.0
     with ClockSampler(dev) as clk:
         barrier()
         t_all = time.perf_counter()
         for _ in range(args.steps):
             t0 = time.perf_counter()
+            feed(_)
+            stage_s += time.perf_counter() - t0
             r = sim.advance(bio_steps)  # synchronous C-ABI call, results on host
             wall.append(time.perf_counter() - t0)
             dev_ms.append(r.device_ms)
@@ -264,12 +333,12 @@ def run_b200(args):
     # max over ranks of time, sum of work
     if dist:
         import torch
-        t = torch.tensor([dev_s, wall_s, xwait], dtype=torch.float64)
+        t = torch.tensor([dev_s, wall_s, xwait, stage_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s, wall_s, xwait = float(t[0]), float(t[1]), float(t[2])
-        e = torch.tensor([events, spikes], dtype=torch.float64)
+        dev_s, wall_s, xwait, stage_s = (float(x) for x in t)
+        e = torch.tensor([events, spikes, launches], dtype=torch.float64)
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
-        events, spikes = int(e[0]), int(e[1])
+        events, spikes, launches = (int(x) for x in e)
     if rank != 0:
         return
     n = net.total_neurons
@@ -281,7 +350,9 @@ def run_b200(args):
     alg_bytes = (98 * neuron_steps + 12 * events + 20 * spikes) / ws
     peak, peak_kind = measured_peak_hbm()
     achieved = alg_bytes / dev_s / 1e9
-    launches_per = max(1, launches // max(1, args.steps * ws))
+    # per advance and rank: one conductance-scatter launch (the staged
+    # set_conductances) + the step kernel launch(es)
+    launches_per = max(1, launches // max(1, args.steps * ws) - 1)
     traffic = ncu_traffic()
     line = {
         "metric": "synaptic_events_per_s", "value": value, "unit": "events/s", "n_gpus": ws,
@@ -307,8 +378,9 @@ def run_b200(args):
         "e2e": {"value": events / wall_s, "unit": "events/s",
                 "h2d_bytes_per_step": h2d // max(1, args.steps * ws),
                 "d2h_bytes_per_step": d2h // max(1, args.steps * ws),
-                "wall_s_per_bio_s": wall_s / bio_s},
-        "gpu_launches": launches // max(1, ws),
+                "wall_s_per_bio_s": wall_s / bio_s,
+                "host_stage_ms_per_step": 1e3 * stage_s / args.steps},
+        "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "vxb::step_kernel",
@@ -337,7 +409,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--bio-ms", type=float, default=100.0)

@@ -74,10 +74,53 @@ struct DevBuf {
         n = count;
         if (count) CK(cudaMalloc(&p, count * sizeof(T)));
     }
+    void reserve(size_t count) {  // grow-only: no free/sync when it already fits
+        if (count > n) alloc(count);
+    }
     void zero(cudaStream_t s) {
         if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
     }
 };
+
+// Page-locked host staging buffer (grow-only).
+template <typename T>
+struct HostBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void reserve(size_t count) {
+        if (count <= n) return;
+        count = std::max(count, 2 * n);  // geometric growth
+        T* q = nullptr;
+        CK(cudaMallocHost(&q, count * sizeof(T)));
+        if (p) {
+            std::memcpy(q, p, n * sizeof(T));
+            cudaFreeHost(p);
+        }
+        p = q;
+        n = count;
+    }
+};
+
+// Length of the prefix of finite, non-negative values (NaN fails both
+// compares).  Branch-free per 1024-value block so the common all-valid case
+// vectorises; only a block holding a bad value is rescanned.
+uint32_t valid_prefix(const float* v, uint32_t n) {
+    for (uint32_t b = 0; b < n; b += 1024) {
+        const uint32_t e = std::min(n, b + 1024);
+        int bad = 0;
+        for (uint32_t i = b; i < e; ++i) bad |= !(v[i] >= 0.0f && v[i] <= 3.402823466e38f);
+        if (bad)
+            for (uint32_t i = b; i < e; ++i)
+                if (!(v[i] >= 0.0f && v[i] <= 3.402823466e38f)) return i;
+    }
+    return n;
+}
 
 struct Probe {
     uint64_t gid;
@@ -173,6 +216,17 @@ struct Engine {
     std::vector<vxb_step_timings> timings;
     double device_ms = 0;
     uint64_t h2d = 0, d2h = 0, launches = 0;
+
+    // set_conductances staging (flushed by the next advance): one record per
+    // (unit, receptor) = {first staged value, dst float index, count, key}
+    HostBuf<float> h_cstage;
+    std::vector<uint4> cond_rec;
+    std::vector<int32_t> cond_slot;  // [unit * 4 + receptor] -> record, -1 if none
+    size_t cond_total = 0;
+    DevBuf<float> d_cstage;
+    DevBuf<uint4> d_crec;
+    void stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t k);
+    void flush_conductances(bool sync);
 
     ~Engine() {
         for (void* p : peer_base)
@@ -1198,6 +1252,7 @@ void Engine::advance(uint32_t steps) {
         d_probe_v.zero(stream);
         d_probe_i.zero(stream);
     }
+    flush_conductances(false);  // advance syncs before the caller can stage again
 
     // chunking: the linear spike log holds n entries per step of a chunk
     uint32_t chunk = steps;
@@ -1207,10 +1262,10 @@ void Engine::advance(uint32_t steps) {
     }
     const uint32_t cap_entries = record_raster ? n * chunk : 2 * n;
     if (d_spk.n < std::max<size_t>(1, cap_entries)) d_spk.alloc(std::max<size_t>(1, cap_entries));
-    d_seg_end.alloc(chunk + 2);
-    d_rates.alloc((size_t)n_units * chunk);
-    d_phase_ns.alloc(chunk + 2);
-    d_phase_wait.alloc(chunk + 2);
+    d_seg_end.reserve(chunk + 2);
+    d_rates.reserve((size_t)n_units * chunk);
+    d_phase_ns.reserve(chunk + 2);
+    d_phase_wait.reserve(chunk + 2);
     exchange_wait_ms = 0;
 
     std::vector<unsigned long long> phase_ns_all;
@@ -1541,21 +1596,65 @@ int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float
         if (receptor < 0 || receptor >= 4) throw ConfigError("receptor out of range");
         if (n != g.units[unit].neurons)
             throw ConfigError("conductance vector size does not match unit");
-        for (uint32_t i = 0; i < n; ++i)
-            if (!(values[i] >= 0.0f) || !std::isfinite(values[i]))
-                throw ConfigError("conductance values must be finite and >= 0");
-        if (n == 0 || !g.local(g.unit_worker[unit])) return VXB_OK;  // owned by another rank
-        CK(cudaSetDevice(g.device));
-        const uint32_t base = g.wbase[g.unit_worker[unit]] + g.unit_local_base[unit];
-        std::vector<float4> buf(n);
-        CK(cudaMemcpy(buf.data(), g.d_g.p + base, 16ull * n, cudaMemcpyDeviceToHost));
-        for (uint32_t i = 0; i < n; ++i) (&buf[i].x)[receptor] = values[i];
-        CK(cudaMemcpy(g.d_g.p + base, buf.data(), 16ull * n, cudaMemcpyHostToDevice));
+        // engine.cpp:839-843 writes values in order and throws at the first
+        // invalid one, leaving the prefix written: stage the same prefix
+        const uint32_t k = valid_prefix(values, n);
+        if (k && g.local(g.unit_worker[unit])) g.stage_conductances(unit, receptor, values, k);
+        if (k < n) throw ConfigError("conductance values must be finite and >= 0");
         return VXB_OK;
     } catch (const std::exception& x) {
         g.err = x.what();
         return fail_code(x);
     }
+}
+
+void Engine::stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t k) {
+    const uint32_t key = unit * 4 + (uint32_t)receptor;
+    if (cond_slot.size() != 4ull * n_units) cond_slot.assign(4ull * n_units, -1);
+    if (cond_slot[key] >= 0) {  // overwrite the earlier staged values of this unit/receptor
+        uint4& r = cond_rec[cond_slot[key]];
+        std::memcpy(h_cstage.p + r.x, values, 4ull * k);
+        r.z = std::max(r.z, k);
+        return;
+    }
+    cond_slot[key] = (int32_t)cond_rec.size();
+    const uint32_t full = units[unit].neurons;  // room for a later full overwrite
+    if (cond_total + full > 0xFFFFFFFFull) flush_conductances(true);
+    h_cstage.reserve(cond_total + full);
+    std::memcpy(h_cstage.p + cond_total, values, 4ull * k);
+    const uint32_t base = wbase[unit_worker[unit]] + unit_local_base[unit];
+    cond_rec.push_back(make_uint4((uint32_t)cond_total, 4 * base + (uint32_t)receptor, k, key));
+    cond_total += full;
+}
+
+void Engine::flush_conductances(bool sync) {
+    if (cond_rec.empty()) return;
+    CK(cudaSetDevice(device));
+    // compact the records' values (each record reserved a full unit)
+    std::vector<uint4> rec(cond_rec.size());
+    uint32_t total = 0;
+    for (size_t i = 0; i < cond_rec.size(); ++i) {
+        const uint4 r = cond_rec[i];
+        if (r.x != total) std::memmove(h_cstage.p + total, h_cstage.p + r.x, 4ull * r.z);
+        rec[i] = make_uint4(total, r.y, r.z, r.w);
+        total += r.z;
+    }
+    d_cstage.reserve(total);
+    d_crec.reserve(rec.size());
+    CK(cudaMemcpyAsync(d_cstage.p, h_cstage.p, 4ull * total, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_crec.p, rec.data(), 16 * rec.size(), cudaMemcpyHostToDevice, stream));
+    const int blocks = (int)std::min<uint32_t>(148 * 8, (total + 255) / 256);
+    cond_scatter_kernel<<<blocks, 256, 0, stream>>>(d_cstage.p, d_crec.p, (uint32_t)rec.size(),
+                                                     total, reinterpret_cast<float*>(d_g.p));
+    CK(cudaGetLastError());
+    // the pinned staging buffer is reused by the next set_conductances; `rec`
+    // is pageable, so its copy has been staged by the time the call returns
+    if (sync) CK(cudaStreamSynchronize(stream));
+    h2d += 4ull * total + 16 * rec.size();
+    launches += 1;
+    for (const uint4& r : cond_rec) cond_slot[r.w] = -1;
+    cond_rec.clear();
+    cond_total = 0;
 }
 
 int vxb_membrane_snapshot(const vxb_engine* e, uint16_t worker, float* out, uint32_t cap) {

@@ -1336,4 +1336,24 @@ __global__ void debug_normal_kernel(const uint64_t* __restrict__ base,
         out[i] = stream_normal(base[i], k[i]);
 }
 
+// Staged set_conductances (engine.cpp:829-844) applied in one launch before
+// an advance: record r = {first staged value, destination float index
+// (neuron * 4 + receptor), count}; records are sorted by their first value
+// and never overlap, so every staged value has exactly one destination.
+__global__ void cond_scatter_kernel(const float* __restrict__ vals,
+                                    const uint4* __restrict__ rec, uint32_t n_rec,
+                                    uint32_t total, float* __restrict__ g) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = n_rec;  // last record with rec.x <= i
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&rec[mid].x) <= i) lo = mid;
+            else hi = mid;
+        }
+        const uint4 r = rec[lo];
+        g[(uint64_t)r.y + 4ull * (i - r.x)] = vals[i];
+    }
+}
+
 }  // namespace vxb

@@ -33,6 +33,7 @@ from .engine import ConfigError, NetworkTables, SimError, SimInstance, SimOption
 
 MASK64 = (1 << 64) - 1
 GOLDEN = 0x9E3779B97F4A7C15
+RNG_CONDUCTANCE = 7  # rng.hpp:17-28 stream tag
 
 
 # ---------------------------------------------------------------- rng.hpp
@@ -61,6 +62,34 @@ def stream_normal(base: int, k: int) -> float:
     u1 = 1.0 - stream_u01(base, 2 * k)
     u2 = stream_u01(base, 2 * k + 1)
     return math.sqrt(-2.0 * math.log(u1)) * math.cos(6.283185307179586476925286766559 * u2)
+
+
+def stream_normal_array(base: int, count: int) -> np.ndarray:
+    """stream_normal(base, k) for k in [0, count), vectorised (rng.hpp:58-67).
+    The integer stream is exact; numpy's log/cos may differ from glibc's in
+    the last ulp, so this feeds workloads (bench inputs), never parity."""
+    k = np.arange(count, dtype=np.uint64)
+
+    def u01(j):
+        with np.errstate(over="ignore"):
+            x = np.uint64(base) + j * np.uint64(GOLDEN) + np.uint64(GOLDEN)
+            x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+        return (x >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+    u1 = 1.0 - u01(2 * k)
+    u2 = u01(2 * k + np.uint64(1))
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586476925286766559 * u2)
+
+
+def sample_conductances(seed: int, salt: int, unit: int, receptor: int, location: float,
+                        scale: float, count: int) -> np.ndarray:
+    """netgen.cpp:318-329 (vectorised; see stream_normal_array for the ulp note).
+    salt 0 draws the tables' initial values; assim.cpp:98-103 uses
+    mix_key(member + 1, window + 1) per assimilation window."""
+    base = mix_key(mix_key(seed, RNG_CONDUCTANCE, salt), unit, receptor)
+    return np.exp(location + scale * stream_normal_array(base, count)).astype(np.float32)
 
 
 def stream_below(base: int, k: int, n: int) -> int:

@@ -273,6 +273,40 @@ def test_conductance_override_matches_reference():
     assert_same(gpu, ref)
 
 
+def test_conductance_staging_matches_reference():
+    """set_conductances is staged on the host and applied by the next advance;
+    repeated sets, sets between advances and the reference's prefix-written
+    error path (engine.cpp:839-843) must all land exactly as in the reference."""
+    net = RefNet(hot_cfg(seed=17, voxels=3, npv=40, k_in=6, rho=0.2))
+    opt = SimOptions(steps=30, probe_gids=[5, 60, 100])
+    nus = [int(x) for x in net.tables.units["neurons"]]
+    rng = np.random.default_rng(4)
+    bad = rng.uniform(0.0, 2.0, nus[0]).astype(np.float32)
+    bad[nus[0] // 2] = np.nan  # prefix before the NaN is written, then ConfigError
+
+    def script(sim):
+        out = []
+        sim.set_conductances(1, 0, rng_vals(1, 0))
+        sim.set_conductances(1, 0, rng_vals(1, 1))  # overwrites the first set
+        sim.set_conductances(2, 3, rng_vals(2, 2))
+        with pytest.raises(ConfigError):
+            sim.set_conductances(0, 1, bad)
+        out.append(sim.advance(15))
+        sim.set_conductances(2, 3, rng_vals(2, 3))
+        sim.set_conductances(0, 0, rng_vals(0, 4))
+        out.append(sim.advance(15))
+        return out
+
+    def rng_vals(u, k):
+        return np.random.default_rng(100 + k).uniform(0.0, 2.5, nus[u]).astype(np.float32)
+
+    ref = script(RefSim(net, opt))
+    with SimInstance(net.tables, opt) as sim:
+        gpu = script(sim)
+    for g, r in zip(gpu, ref):
+        assert_same(g, r)
+
+
 # test_engine.cpp:539-558
 def test_option_validation():
     net = RefNet(quiet_cfg(seed=1, voxels=1, npv=10, k_in=2))

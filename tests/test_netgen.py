@@ -98,3 +98,24 @@ def test_b200_byte_model_partitions_under_budget():
         netgen.build_network(cfg)
     with pytest.raises(ConfigError, match="byte_model"):
         netgen.parse_config({"partition": {"byte_model": "tpu"}})
+
+
+def test_sample_conductances_matches_reference_tables():
+    """netgen.cpp:260-261: the tables' initial per-neuron conductances are
+    sample_conductances(seed, 0, unit, receptor, g_location, g_scale, n)."""
+    cfg = make_config(seed=21, voxels=3, npv=200, k_in=5, rho=0.3, workers=2)
+    ref = RefNet(cfg)
+    b = netgen.build_network(cfg)
+    g_ref = np.concatenate([w.neurons for w in ref.tables.workers])
+    g_ref = g_ref[np.argsort(g_ref["gid"], kind="stable")]
+    flips = 0
+    for u, unit in enumerate(b.layout.units):
+        pop = b.layout.pop_of_unit(u)
+        rows = g_ref[unit.gid_base:unit.gid_base + unit.neurons]
+        for r in range(4):
+            got = netgen.sample_conductances(cfg["seed"], 0, u, r, pop.g_location[r],
+                                             pop.g_scale[r], unit.neurons)
+            want = rows["g"][:, r]
+            assert np.allclose(got, want, rtol=2e-7, atol=0)
+            flips += int((got != want).sum())
+    assert flips <= 2  # numpy log/cos/exp vs glibc: rare last-ulp float flips

@@ -245,6 +245,8 @@ struct Engine {
     bool rows_sorted = false;
     uint32_t n_blocks = 1, block_n = 0;
     DevBuf<uint32_t> d_blk;
+    DevBuf<uint32_t> d_work;  // dynamic delivery chunk counters [2][blocks][world]
+    bool dyn = false;
     // tiled delivery tables (world == 1)
     bool tiled = false;
     uint32_t n_tiles = 0;
@@ -559,6 +561,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     setup_exchange();
     build_tiles();
     if (!tiled) build_blocks();
+    if (const char* env = std::getenv("VXB_DYN")) dyn = !tiled && std::atoi(env) != 0;
 
     // longest out-row: delivery pieces per spike (<= kStageE entries each)
     {
@@ -1098,6 +1101,7 @@ void Engine::sort_rows() {
 // (VXB_BLOCK_NEURONS overrides the block size).
 void Engine::build_blocks() {
     n_blocks = 1;
+    dyn = false;
     const uint64_t pend_per = packed ? 16 : 32;
     uint64_t bn = (48ull << 20) / pend_per;
     if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
@@ -1110,6 +1114,7 @@ void Engine::build_blocks() {
                                                    d_tgt.p, n_src, n_blocks, block_n, d_blk.p);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream));
+    dyn = true;  // block-major dynamic chunks keep the grid inside one block
 }
 
 // Tiled delivery (single device, experimental, VXB_TILED=1): sort every
@@ -1399,6 +1404,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.q_total = q_total;
     a.n_blocks = n_blocks;
     a.blk_off = d_blk.p;
+    d_work.reserve(2ull * n_blocks * world);
+    d_work.zero(stream);
+    a.work_ctr = d_work.p;
+    a.dyn = dyn ? 1u : 0u;
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));

@@ -155,6 +155,11 @@ struct StepArgs {
     // order; blk_off[s * (n_blocks + 1) + b] = row offset of block b
     uint32_t n_blocks;
     const uint32_t* blk_off;
+    // dynamic delivery: per (phase parity, block, source list) chunk
+    // counters; producers take chunks of spikes block-major so the grid
+    // works on one L2 block at a time and balances itself (dyn != 0)
+    uint32_t* work_ctr;
+    uint32_t dyn;
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -208,6 +213,27 @@ __device__ __forceinline__ void grid_barrier(Control* ctl, Hook hook, Post post)
         }
     }
     __syncthreads();
+}
+
+// find_seg starting from a known segment lo (starts[lo] <= i): galloping
+// search, O(log distance) — the update loop's neurons only move forward.
+__device__ __forceinline__ uint32_t find_seg_from(const uint32_t* starts, uint32_t nseg,
+                                                  uint32_t i, uint32_t lo) {
+    uint32_t step = 1, hi = lo + 1;
+    while (hi < nseg && starts[hi] <= i) {
+        lo = hi;
+        step <<= 1;
+        hi = lo + step;
+    }
+    if (hi > nseg) hi = nseg;
+    while (hi - lo > 1) {  // starts[lo] <= i < starts[hi] (hi == nseg: end)
+        const uint32_t mid = (lo + hi) >> 1;
+        if (starts[mid] <= i)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
 }
 
 // Index of the segment holding shard-local neuron i (largest start <= i).
@@ -691,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __shared__ uint64_t s_br[128];             // binning: row starts
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
+    __shared__ uint32_t s_hcnt[64];  // dynamic delivery: peer batch sizes of the phase
 
     const SegParams* segp = a.seg;
     const uint32_t* startp = a.seg_start;
@@ -780,6 +807,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         if (roleF) {
         const uint32_t n_round = (a.n + 31u) & ~31u;
         NIn<PACKED> cur, nxt;
+        uint32_t seg_hint = 0;  // warp-uniform: segment of the warp's previous first neuron
         if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
         for (uint32_t i = gtid; i < n_round; i += gthreads) {
             const bool live = i < a.n;
@@ -792,8 +820,9 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             {
                 const uint32_t il = live ? i : a.n - 1;
                 uint32_t s0 = 0;
-                if (lane == 0) s0 = find_seg(startp, a.nseg, il);
+                if (lane == 0) s0 = find_seg_from(startp, a.nseg, il, seg_hint);
                 seg = __shfl_sync(0xffffffffu, s0, 0);
+                seg_hint = seg;
                 while (seg + 1 < a.nseg && startp[seg + 1] <= il) ++seg;
             }
             if (live) {
@@ -1068,50 +1097,114 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 // lane 0 packs them; target blocks in order (L2 blocking)
                 StageBuilder sbld{g_item, 0, 0, 0, 0, 0};
                 const uint32_t B = a.n_blocks;
-                for (uint32_t li = 0; li < a.world; ++li) {
-                    const uint32_t h = (a.ex->rank + li) % a.world;
-                    const uint32_t* ids = a.spk + d_prev + d_lo;
-                    uint32_t cnt = d_cnt;
-                    if (li) {
-                        uint32_t c = 0;
-                        if (lane == 0) {
-                            const unsigned long long w0 = globaltimer();
-                            c = exchange_wait(a, h, tE, tslot);
-                            wait_ns += globaltimer() - w0;
-                        }
-                        cnt = __shfl_sync(0xffffffffu, c, 0);
-                        ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
-                    }
-                    const uint32_t sb = a.ex->src_base[h];
-                    const uint32_t mine = cnt > blockIdx.x ? (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+                if (a.dyn) {
+                    // block-major dynamic chunks: every producer finishes
+                    // its share of block b before block b + 1, so the
+                    // grid's atomics stay inside one L2-resident block
+                    const uint32_t W = a.world;
+                    uint32_t* wc = a.work_ctr + (ph & 1u) * B * W;
+                    if (blockIdx.x == 0)  // the other set serves phase ph + 1
+                        for (uint32_t k = lane; k < B * W; k += 32)
+                            a.work_ctr[((ph + 1) & 1u) * B * W + k] = 0u;
                     for (uint32_t blk = 0; blk < B; ++blk) {
-                        for (uint32_t j0 = 0; j0 < mine; j0 += 32) {
-                            const uint32_t j = j0 + lane;
-                            uint64_t sbeg = 0, slen = 0;
-                            if (j < mine) {
-                                const uint32_t s = sb + __ldcg(ids + blockIdx.x + j * gridDim.x);
-                                const uint64_t row = ldg64(a.off + s);
-                                if (B == 1) {
-                                    sbeg = row;
-                                    slen = ldg64(a.off + s + 1) - row;
-                                } else {
-                                    const uint32_t* bo = a.blk_off + (size_t)s * (B + 1);
-                                    const uint32_t lo = __ldg(bo + blk), hi = __ldg(bo + blk + 1);
-                                    sbeg = row + lo;
-                                    slen = hi - lo;
+                        for (uint32_t li = 0; li < W; ++li) {
+                            const uint32_t h = (a.ex->rank + li) % W;
+                            const uint32_t* ids = a.spk + d_prev + d_lo;
+                            uint32_t cnt = d_cnt;
+                            if (li) {
+                                if (blk == 0 && lane == 0) {
+                                    const unsigned long long w0 = globaltimer();
+                                    s_hcnt[li] = exchange_wait(a, h, tE, tslot);
+                                    wait_ns += globaltimer() - w0;
                                 }
-                                if (blk == 0) {
-                                    const uint64_t len = ldg64(a.off + s + 1) - row;
-                                    const uint32_t in = __ldg(a.inner + s);
-                                    my_inner += 2ull * in;
-                                    my_outer += 2ull * (len - in);
+                                __syncwarp();
+                                cnt = s_hcnt[li];
+                                ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
+                            }
+                            const uint32_t sb = a.ex->src_base[h];
+                            const uint32_t CH = max(1u, min(32u, cnt / (8u * gridDim.x)));
+                            uint32_t* ctr = wc + blk * W + li;
+                            uint32_t nxt = 0;
+                            if (lane == 0) nxt = atomicAdd(ctr, CH);
+                            for (;;) {
+                                const uint32_t c0 = __shfl_sync(0xffffffffu, nxt, 0);
+                                if (c0 >= cnt) break;
+                                if (lane == 0) nxt = atomicAdd(ctr, CH);  // in flight meanwhile
+                                const uint32_t nl = min(CH, cnt - c0);
+                                uint64_t sbeg = 0, slen = 0;
+                                if (lane < nl) {
+                                    const uint32_t s = sb + __ldcg(ids + c0 + lane);
+                                    const uint64_t row = ldg64(a.off + s);
+                                    if (B == 1) {
+                                        sbeg = row;
+                                        slen = ldg64(a.off + s + 1) - row;
+                                    } else {
+                                        const uint32_t* bo = a.blk_off + (size_t)s * (B + 1);
+                                        const uint32_t lo = __ldg(bo + blk), hi = __ldg(bo + blk + 1);
+                                        sbeg = row + lo;
+                                        slen = hi - lo;
+                                    }
+                                    if (blk == 0) {
+                                        const uint64_t len = ldg64(a.off + s + 1) - row;
+                                        const uint32_t in = __ldg(a.inner + s);
+                                        my_inner += 2ull * in;
+                                        my_outer += 2ull * (len - in);
+                                    }
+                                }
+                                for (uint32_t l = 0; l < nl; ++l) {
+                                    const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
+                                    const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
+                                    if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
                                 }
                             }
-                            const uint32_t nl = min(32u, mine - j0);
-                            for (uint32_t l = 0; l < nl; ++l) {
-                                const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
-                                const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
-                                if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
+                        }
+                    }
+                } else {
+                    for (uint32_t li = 0; li < a.world; ++li) {
+                        const uint32_t h = (a.ex->rank + li) % a.world;
+                        const uint32_t* ids = a.spk + d_prev + d_lo;
+                        uint32_t cnt = d_cnt;
+                        if (li) {
+                            uint32_t c = 0;
+                            if (lane == 0) {
+                                const unsigned long long w0 = globaltimer();
+                                c = exchange_wait(a, h, tE, tslot);
+                                wait_ns += globaltimer() - w0;
+                            }
+                            cnt = __shfl_sync(0xffffffffu, c, 0);
+                            ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
+                        }
+                        const uint32_t sb = a.ex->src_base[h];
+                        const uint32_t mine = cnt > blockIdx.x ? (cnt - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+                        for (uint32_t blk = 0; blk < B; ++blk) {
+                            for (uint32_t j0 = 0; j0 < mine; j0 += 32) {
+                                const uint32_t j = j0 + lane;
+                                uint64_t sbeg = 0, slen = 0;
+                                if (j < mine) {
+                                    const uint32_t s = sb + __ldcg(ids + blockIdx.x + j * gridDim.x);
+                                    const uint64_t row = ldg64(a.off + s);
+                                    if (B == 1) {
+                                        sbeg = row;
+                                        slen = ldg64(a.off + s + 1) - row;
+                                    } else {
+                                        const uint32_t* bo = a.blk_off + (size_t)s * (B + 1);
+                                        const uint32_t lo = __ldg(bo + blk), hi = __ldg(bo + blk + 1);
+                                        sbeg = row + lo;
+                                        slen = hi - lo;
+                                    }
+                                    if (blk == 0) {
+                                        const uint64_t len = ldg64(a.off + s + 1) - row;
+                                        const uint32_t in = __ldg(a.inner + s);
+                                        my_inner += 2ull * in;
+                                        my_outer += 2ull * (len - in);
+                                    }
+                                }
+                                const uint32_t nl = min(32u, mine - j0);
+                                for (uint32_t l = 0; l < nl; ++l) {
+                                    const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
+                                    const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
+                                    if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
+                                }
                             }
                         }
                     }

@@ -1,6 +1,10 @@
-"""Split the step time of the config-2 workload into neuron update vs
-delivery: the same 1M-neuron network run silent (ou_mean = 0: no spikes, the
-OU noise still drawn) and at its ~10 Hz operating point."""
+"""Split the step time of a bench workload into neuron update vs delivery:
+the same network run silent (ou_mean = 0: no spikes, the OU noise still
+drawn) and at its ~10 Hz operating point.
+
+    python tools/decompose.py [config2|config3] [--steps S] [--reps R] [--only silent|10hz]
+"""
+import argparse
 import json
 import sys
 from pathlib import Path
@@ -27,7 +31,18 @@ def run(cfg, steps=100, reps=5):
 
 
 if __name__ == "__main__":
-    base = bench.workload_cfg()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workload", nargs="?", default="config2")
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args()
+    base = bench.workload_cfg() if args.workload == "config2" else bench.dti_cfg()
     quiet = json.loads(json.dumps(base))
     quiet["regions"]["subcortex"]["ou_mean"] = 0.0
-    print(json.dumps({"silent": run(quiet), "10hz": run(base)}), flush=True)
+    out = {}
+    if args.only in (None, "silent"):
+        out["silent"] = run(quiet, args.steps, args.reps)
+    if args.only in (None, "10hz"):
+        out["10hz"] = run(base, args.steps, args.reps)
+    print(json.dumps(out), flush=True)

@@ -165,8 +165,6 @@ struct Engine {
     DevBuf<unsigned long long> d_mask;    // per local neuron: shards with targets
     std::vector<unsigned long long> h_mask;
     std::vector<unsigned long long> have_src;  // per global source: workers holding targets here
-    uint64_t max_row = 0;
-    uint32_t pieces = 1;
     bool use_smem_seg = true;
     uint32_t smem_bytes = 0;
 
@@ -239,7 +237,6 @@ struct Engine {
     void load(const vxb_network* net, const vxb_options* opt, const vxb_netspec* gen = nullptr,
               uint32_t rank_ = 0, uint32_t world_ = 1);
     void setup_exchange();
-    void build_tiles();
     void sort_rows();
     void build_blocks();
     bool rows_sorted = false;
@@ -247,12 +244,7 @@ struct Engine {
     DevBuf<uint32_t> d_blk;
     DevBuf<uint32_t> d_work;  // dynamic delivery chunk counters [2][blocks][world]
     bool dyn = false;
-    // tiled delivery tables (world == 1)
-    bool tiled = false;
-    uint32_t n_tiles = 0;
-    uint64_t q_total = 0;
-    DevBuf<uint32_t> d_dir_off, d_qcount;
-    DevBuf<uint64_t> d_dir, d_qbase, d_queue;
+    bool f_policy = false;    // neuron-state stream evict_first
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
@@ -559,25 +551,12 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
     setup_exchange();
-    build_tiles();
-    if (!tiled) build_blocks();
-    if (const char* env = std::getenv("VXB_DYN")) dyn = !tiled && std::atoi(env) != 0;
+    build_blocks();
+    if (const char* env = std::getenv("VXB_DYN")) dyn = std::atoi(env) != 0;
 
-    // longest out-row: delivery pieces per spike (<= kStageE entries each)
-    {
-        std::vector<uint64_t> off((size_t)n_src + 1);
-        CK(cudaMemcpyAsync(off.data(), d_off.p, 8ull * (n_src + 1), cudaMemcpyDeviceToHost,
-                           stream));
-        CK(cudaStreamSynchronize(stream));
-        uint64_t mx = 0;
-        for (uint32_t i = 0; i < n_src; ++i) mx = std::max<uint64_t>(mx, off[i + 1] - off[i]);
-        max_row = mx;
-        pieces = (uint32_t)std::max<uint64_t>(1, (mx + kStageE - 1) / kStageE);
-    }
     // cooperative grid
     use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg;
-    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u,
-                            tiled ? kTile * (packed ? 16u : 32u) : 0u).total;
+    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u).total;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const void* kfn = packed ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
@@ -590,6 +569,19 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
                                                          smem_bytes));
     if (per_sm < 1) throw SimError("step kernel cannot be resident on this device");
     grid = sms * per_sm;
+    // L2 residency of the pending buffers: evict_last lines are retained
+    // within the persisting carve-out, so size it to the device maximum
+    // (VXB_PERSIST=0 leaves the driver default)
+    {
+        const char* env = std::getenv("VXB_PERSIST");
+        if (!env || std::atoi(env) != 0) {
+            int mx = 0;
+            CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, device));
+            if (mx > 0) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx));
+        }
+        const char* fp = std::getenv("VXB_FPOL");
+        f_policy = fp ? std::atoi(fp) != 0 : false;
+    }
     CK(cudaStreamSynchronize(stream));
 }
 
@@ -1101,7 +1093,7 @@ void Engine::sort_rows() {
 // (VXB_BLOCK_NEURONS overrides the block size).
 void Engine::build_blocks() {
     n_blocks = 1;
-    dyn = false;
+    dyn = true;  // dynamic chunks: +8% on config 2 even with one block
     const uint64_t pend_per = packed ? 16 : 32;
     uint64_t bn = (48ull << 20) / pend_per;
     if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
@@ -1114,70 +1106,6 @@ void Engine::build_blocks() {
                                                    d_tgt.p, n_src, n_blocks, block_n, d_blk.p);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream));
-    dyn = true;  // block-major dynamic chunks keep the grid inside one block
-}
-
-// Tiled delivery (single device, experimental, VXB_TILED=1): sort every
-// out-row by target, build the per-source tile directory and the per-tile
-// segment queues; delivery then accumulates whole target tiles in shared
-// memory (no global atomics).  Bit-exact, but in round 1 it is latency-bound
-// (serialised stage issue per tile, uneven tiles per CTA) and slower than
-// the L2-atomic path, so it is off by default.
-void Engine::build_tiles() {
-    tiled = false;
-    const char* env = std::getenv("VXB_TILED");
-    if (!env || std::string(env) != "1") return;
-    if (world != 1 || n_syn == 0 || n_syn >= (1ull << 31) || n < (uint32_t)kTile ||
-        n_src != n)
-        return;
-    n_tiles = (n + kTile - 1) / kTile;
-    if (n_tiles >= (1u << 20)) return;
-    sort_rows();
-    // 2. segments per source and per tile
-    DevBuf<uint32_t> nseg, cap;
-    nseg.alloc((size_t)n_src + 1);
-    cap.alloc(n_tiles + 1);
-    nseg.zero(stream);
-    cap.zero(stream);
-    tile_dir_count_kernel<<<1184, 256, 0, stream>>>(
-        reinterpret_cast<const uint64_t*>(d_off.p), d_tgt.p, n_src, nseg.p, cap.p);
-    CK(cudaGetLastError());
-    d_dir_off.alloc((size_t)n_src + 1);
-    DevBuf<unsigned long long> qb64;
-    qb64.alloc(n_tiles + 1);
-    {
-        size_t tmp = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, nseg.p, d_dir_off.p, n_src + 1, stream));
-        DevBuf<unsigned char> t;
-        t.alloc(tmp ? tmp : 1);
-        CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, nseg.p, d_dir_off.p, n_src + 1, stream));
-        // per-tile capacities -> queue bases (u64)
-        std::vector<uint32_t> hc(n_tiles);
-        CK(cudaMemcpyAsync(hc.data(), cap.p, 4ull * n_tiles, cudaMemcpyDeviceToHost, stream));
-        uint32_t total_seg = 0;
-        CK(cudaMemcpyAsync(&total_seg, d_dir_off.p + n_src, 4, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        // locality test: segments must carry enough entries to pay for queueing
-        if ((uint64_t)total_seg * 8 > n_syn) {
-            d_dir_off.release();
-            return;
-        }
-        std::vector<uint64_t> qb(n_tiles + 1, 0);
-        for (uint32_t i = 0; i < n_tiles; ++i) qb[i + 1] = qb[i] + hc[i];
-        q_total = qb[n_tiles];
-        d_qbase.alloc(n_tiles + 1);
-        CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 8ull * (n_tiles + 1), cudaMemcpyHostToDevice,
-                           stream));
-        d_dir.alloc(std::max<uint64_t>(1, total_seg));
-    }
-    tile_dir_fill_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
-                                                   d_tgt.p, n_src, d_dir_off.p, d_dir.p);
-    CK(cudaGetLastError());
-    d_qcount.alloc(2ull * n_tiles);
-    d_qcount.zero(stream);
-    d_queue.alloc(std::max<uint64_t>(1, 2 * q_total));
-    CK(cudaStreamSynchronize(stream));
-    tiled = true;
 }
 
 struct Chunk {
@@ -1355,7 +1283,6 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.spk_cap = (uint32_t)d_spk.n;
     a.ring = record_raster ? 0u : 1u;
     a.use_smem_seg = use_smem_seg ? 1u : 0u;
-    a.pieces = pieces;
     a.dtf = dtf;
     a.ou_root = mix_key(seed, 1);  // rngstream::ou_noise (rng.hpp:18)
     a.seg = d_seg.p;
@@ -1393,21 +1320,13 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.dst_mask = d_mask.p;
     a.phase_wait = d_phase_wait.p;
     d_phase_wait.zero(stream);
-    a.tiled = tiled ? 1u : 0u;
-    a.n_tiles = n_tiles;
-    a.acc_bytes = tiled ? kTile * (packed ? 16u : 32u) : 0u;
-    a.dir_off = d_dir_off.p;
-    a.dir = d_dir.p;
-    a.qbase = d_qbase.p;
-    a.qcount = d_qcount.p;
-    a.queue = d_queue.p;
-    a.q_total = q_total;
     a.n_blocks = n_blocks;
     a.blk_off = d_blk.p;
     d_work.reserve(2ull * n_blocks * world);
     d_work.zero(stream);
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
+    a.f_policy = f_policy ? 1u : 0u;
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));

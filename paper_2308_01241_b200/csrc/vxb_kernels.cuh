@@ -100,7 +100,6 @@ struct StepArgs {
     uint32_t spk_cap;       // spike log capacity
     uint32_t ring;          // spike log in ring mode (raster not recorded)
     uint32_t use_smem_seg;
-    uint32_t pieces;        // delivery pieces per spike row (<= kStageE entries each)
     float dtf;
     uint64_t ou_root;       // mix_key(seed, rngstream::ou_noise)
     // parameters
@@ -141,16 +140,6 @@ struct StepArgs {
     Exchange* ex;
     uint32_t world;
     unsigned long long* phase_wait;  // per phase: max over CTAs of the exchange wait (ns)
-    // tiled delivery (rows sorted by target tile, per-source tile directory)
-    uint32_t tiled;
-    uint32_t n_tiles;
-    uint32_t acc_bytes;
-    const uint32_t* dir_off;   // per source: first directory entry
-    const uint64_t* dir;       // start_rel << 32 | tile << 12 | (len - 1)
-    const uint64_t* qbase;     // per tile: first queue slot
-    uint32_t* qcount;          // [2][n_tiles] segments queued per (step parity, tile)
-    uint64_t* queue;           // [2][q_total] start | (len - 1) << 40
-    uint64_t q_total;
     // L2-blocked delivery: targets split into n_blocks ranges delivered in
     // order; blk_off[s * (n_blocks + 1) + b] = row offset of block b
     uint32_t n_blocks;
@@ -160,6 +149,7 @@ struct StepArgs {
     // works on one L2 block at a time and balances itself (dyn != 0)
     uint32_t* work_ctr;
     uint32_t dyn;
+    uint32_t f_policy;  // 1: neuron-state stream evict_first in L2
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -282,9 +272,6 @@ constexpr int kMaxSmemSeg = 256;
 #ifndef VXB_MINB
 #define VXB_MINB 3
 #endif
-#ifndef VXB_BATCH
-#define VXB_BATCH 4
-#endif
 constexpr int kThreads = VXB_THREADS;
 constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
 #ifndef VXB_DWARPS
@@ -297,46 +284,30 @@ static_assert(VXB_DWARPS >= 2, "delivery needs a producer warp and >= 1 consumer
 #ifndef VXB_STAGE_E
 #define VXB_STAGE_E 768
 #endif
-#ifndef VXB_TILE_LOG
-#define VXB_TILE_LOG 11
-#endif
-constexpr int kTileLog = VXB_TILE_LOG;  // tiled delivery: neurons per tile = 2^kTileLog
-constexpr int kTile = 1 << kTileLog;
 constexpr int kStages = VXB_STAGES;   // delivery pipeline depth (bulk copies in flight)
 constexpr int kStageE = VXB_STAGE_E;  // synapse entries per stage
 constexpr int kStageTgtBytes = (kStageE + 8) * 4;
 constexpr int kStageWBytes = (kStageE + 4) * 8;
 
-struct StageMeta {
-    uint32_t n;       // entries in the piece
-    uint32_t head_t;  // entries skipped at the front of the tgt copy (16 B alignment)
-    uint32_t head_w;
-    uint32_t spike;   // source (shard-local) or ~0 when the piece is empty
-    uint32_t first;   // piece 0 of its row (flop tally)
-    uint32_t len;     // row length
-};
-
-// Tiled delivery packs several queued row segments into one stage.
+// Stage metadata: the producer packs up to kSegPerStage row segments into
+// one stage of the delivery ring.
 constexpr int kSegPerStage = 16;
 struct TStageMeta {
     uint32_t n;                       // entries in the stage
     uint32_t nseg;
-    uint32_t end;                     // last stage of the tile's queue
+    uint32_t end;                     // last stage of the phase
     uint32_t pad;
     uint32_t pre[kSegPerStage + 1];   // prefix of segment lengths
     uint32_t tb[kSegPerStage];        // first entry of segment i in the tgt buffer
     uint32_t wb[kSegPerStage];        // ... in the w buffer
 };
-constexpr uint32_t kMetaBytes =
-    sizeof(TStageMeta) > sizeof(StageMeta) ? sizeof(TStageMeta) : sizeof(StageMeta);
+constexpr uint32_t kMetaBytes = sizeof(TStageMeta);
 
 // Dynamic shared memory carve-up of step_kernel.
 struct SmemLayout {
-    uint32_t acc, tgt, w, bar, meta, seg, start, spk, total;
-    // acc_bytes: per-tile pending accumulators (tiled delivery), 0 otherwise
-    __host__ __device__ SmemLayout(uint32_t nseg_smem, uint32_t acc_bytes = 0) {
-        acc = 0;
-        tgt = acc_bytes;
+    uint32_t tgt, w, bar, meta, seg, start, spk, total;
+    __host__ __device__ explicit SmemLayout(uint32_t nseg_smem) {
+        tgt = 0;
         w = tgt + kStages * kStageTgtBytes;
         bar = w + kStages * kStageWBytes;
         meta = bar + 2 * kStages * 8;  // full barriers, then empty barriers
@@ -376,7 +347,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes),
         "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
-constexpr int kBatch = VXB_BATCH;  // delivery entries in flight per lane
 
 // L2 eviction-priority policies (createpolicy): the synapse stream is read
 // once per spike and must not evict the pending buffers the atomics hit.
@@ -390,101 +360,54 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
-    uint32_t v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-        : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
-    uint64_t v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
-        : "=l"(v) : "l"(p), "l"(pol));
-    return v;
-}
 __device__ __forceinline__ void red_add(unsigned long long* p, uint64_t v, uint64_t pol) {
     asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;"
                  ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
-// Starts the bulk copies of table entries [b0, b1) into stage `st` (16-byte
-// aligned supersets; head offsets in the stage metadata).
-__device__ __forceinline__ void issue_range(const StepArgs& a, unsigned char* smem,
-                                            const SmemLayout& L, uint32_t st, uint64_t b0,
-                                            uint64_t b1, uint64_t pol) {
-    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta + st * kMetaBytes);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
-    StageMeta m;
-    m.spike = 0;
-    m.first = 0;
-    m.len = 0;
-    m.n = (uint32_t)(b1 - b0);
-    const uint64_t t0 = b0 & ~3ull, t1 = (b1 + 3) & ~3ull;
-    const uint64_t w0 = b0 & ~1ull, w1 = (b1 + 1) & ~1ull;
-    m.head_t = (uint32_t)(b0 - t0);
-    m.head_w = (uint32_t)(b0 - w0);
-    *meta = m;
-    const uint32_t tb = (uint32_t)(t1 - t0) * 4, wb = (uint32_t)(w1 - w0) * 8;
-    mbar_expect_tx(bar, tb + wb);
-    bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
-    bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
+// Cache-hinted accesses of the neuron-update stream (policy chosen at run
+// time: evict_first keeps the streamed state from displacing the pending
+// buffers the delivery atomics hit; evict_normal otherwise).
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
-
-// Tiled delivery: fill stage `st` with as many queued segments (q[qi..cnt))
-// as fit, one mbarrier for all their bulk copies.  Returns true once the
-// queue is exhausted (the stage is then marked as the tile's last).
-__device__ __forceinline__ bool issue_tstage(const StepArgs& a, unsigned char* smem,
-                                             const SmemLayout& L, uint32_t st,
-                                             const uint64_t* q, uint32_t cnt, uint32_t& qi,
-                                             uint64_t pol) {
-    TStageMeta* meta = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
-    uint64_t b0s[kSegPerStage];
-    uint32_t lens[kSegPerStage];
-    uint64_t ev[kSegPerStage];
-#pragma unroll
-    for (int k = 0; k < kSegPerStage; ++k)  // independent loads, one round trip
-        ev[k] = qi + k < cnt ? __ldcg(reinterpret_cast<const unsigned long long*>(q) + qi + k) : 0ull;
-    uint32_t ns = 0, toff = 0, woff = 0, total = 0, bytes = 0;
-    while (qi < cnt && ns < (uint32_t)kSegPerStage) {
-        const uint64_t e = ev[ns];
-        const uint64_t b0 = e & ((1ull << 40) - 1), b1 = b0 + (e >> 40) + 1;
-        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - (b0 & ~3ull));
-        const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - (b0 & ~1ull));
-        if (ns && (toff + tn > (uint32_t)kStageE + 8 || woff + wn > (uint32_t)kStageE + 4)) break;
-        b0s[ns] = b0;
-        lens[ns] = (uint32_t)(b1 - b0);
-        meta->pre[ns] = total;
-        meta->tb[ns] = toff + (uint32_t)(b0 & 3ull);
-        meta->wb[ns] = woff + (uint32_t)(b0 & 1ull);
-        total += lens[ns];
-        bytes += tn * 4 + wn * 8;
-        toff += tn;
-        woff += wn;
-        ++ns;
-        ++qi;
-    }
-    meta->pre[ns] = total;
-    meta->n = total;
-    meta->nseg = ns;
-    const bool end = qi >= cnt;
-    meta->end = end ? 1u : 0u;
-    if (!ns) {
-        mbar_arrive(bar);
-        return end;
-    }
-    mbar_expect_tx(bar, bytes);
-    uint32_t to = 0, wo = 0;
-    for (uint32_t i = 0; i < ns; ++i) {
-        const uint64_t b0 = b0s[i], b1 = b0 + lens[i];
-        const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
-        const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0), wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
-        bulk_g2s(smem + L.tgt + st * kStageTgtBytes + to * 4, a.tgt + t0, tn * 4, bar, pol);
-        bulk_g2s(smem + L.w + st * kStageWBytes + wo * 8, a.w + w0, wn * 8, bar, pol);
-        to += tn;
-        wo += wn;
-    }
-    return end;
+__device__ __forceinline__ uint32_t ldp(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldp(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 ldp(const float4* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 ldp_cg(const ulonglong2* p, uint64_t pol) {
+    ulonglong2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void stp(uint32_t* p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stp(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stp(float4* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                 ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stp_cg(ulonglong2* p, ulonglong2 v, uint64_t pol) {
+    asm volatile("st.global.cg.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;"
+                 ::"l"(p), "l"(v.x), "l"(v.y), "l"(pol) : "memory");
 }
 
 __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
@@ -554,63 +477,6 @@ struct StageBuilder {
         }
     }
 };
-
-// Tiled delivery, producer side: queue the row segments of spike s (one per
-// target tile, from the source's tile directory) for the step's tile
-// queues.  Runs when the spike is produced, one phase before delivery.
-__device__ __forceinline__ void bin_spike(const StepArgs& a, uint32_t s, uint32_t set,
-                                          unsigned long long& inner2,
-                                          unsigned long long& outer2) {
-    const uint32_t d0 = __ldg(a.dir_off + s), d1 = __ldg(a.dir_off + s + 1);
-    const uint64_t row = ldg64(a.off + s), len = ldg64(a.off + s + 1) - row;
-    for (uint32_t d = d0; d < d1; ++d) {
-        const uint64_t e = ldg64(a.dir + d);
-        const uint32_t tile = (uint32_t)(e >> 12) & 0xfffffu;
-        const uint64_t start = row + (e >> 32), lm1 = e & 0xfffull;
-        const uint32_t q = atomicAdd(a.qcount + (size_t)set * a.n_tiles + tile, 1u);
-        a.queue[(size_t)set * a.q_total + ldg64(a.qbase + tile) + q] = start | (lm1 << 40);
-    }
-    const uint32_t in = __ldg(a.inner + s);
-    inner2 += 2ull * in;
-    outer2 += 2ull * (len - in);
-}
-
-// Starts the bulk copies of one delivery piece (item = spike k, piece c of
-// C) into stage `st`.  Pieces are 16-byte aligned supersets of the entry
-// range; the head offsets are recorded in the stage's metadata.
-template <bool PACKED>
-__device__ __forceinline__ void issue_piece(const StepArgs& a, unsigned char* smem,
-                                            const SmemLayout& L, uint32_t st, uint32_t item,
-                                            uint32_t C, const uint32_t* ids, uint32_t src_base,
-                                            uint64_t pol) {
-    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + L.meta + st * kMetaBytes);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
-    const uint32_t k = item / C, c = item - k * C;
-    const uint32_t s = src_base + __ldcg(ids + k);
-    const uint64_t e0 = ldg64(a.off + s), e1 = ldg64(a.off + s + 1);
-    const uint64_t len = e1 - e0;
-    const uint64_t b0 = e0 + len * c / C, b1 = e0 + len * (c + 1) / C;
-    StageMeta m;
-    m.spike = s;
-    m.first = c == 0;
-    m.len = (uint32_t)len;
-    m.n = (uint32_t)(b1 - b0);
-    if (m.n == 0) {
-        m.head_t = m.head_w = 0;
-        *meta = m;
-        mbar_arrive(bar);
-        return;
-    }
-    const uint64_t t0 = b0 & ~3ull, t1 = (b1 + 3) & ~3ull;
-    const uint64_t w0 = b0 & ~1ull, w1 = (b1 + 1) & ~1ull;
-    m.head_t = (uint32_t)(b0 - t0);
-    m.head_w = (uint32_t)(b0 - w0);
-    *meta = m;
-    const uint32_t tb = (uint32_t)(t1 - t0) * 4, wb = (uint32_t)(w1 - w0) * 8;
-    mbar_expect_tx(bar, tb + wb);
-    bulk_g2s(smem + L.tgt + st * kStageTgtBytes, a.tgt + t0, tb, bar, pol);
-    bulk_g2s(smem + L.w + st * kStageWBytes, a.w + w0, wb, bar, pol);
-}
 
 // Routing of one warp's spikes to the peers (engine.cpp:416-437 + transport
 // send): ids go straight into the peers' receive slots over NVLink P2P
@@ -685,36 +551,35 @@ struct NIn {
 
 template <bool PACKED>
 __device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool doE,
-                                            const void* pend_rd, NIn<PACKED>& x) {
-    x.vb = a.v[i];
-    x.iou = a.i_ou[i];
+                                            const void* pend_rd, NIn<PACKED>& x, uint64_t pf,
+                                            uint64_t pk) {
+    x.vb = ldp(a.v + i, pf);
+    x.iou = ldp(a.i_ou + i, pf);
     if (doE) {
-        x.j = a.j[i];
-        x.g = a.g[i];
+        x.j = ldp(a.j + i, pf);
+        x.g = ldp(a.g + i, pf);
         if constexpr (PACKED) {
-            x.p0 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + i);
+            x.p0 = ldp_cg(reinterpret_cast<const ulonglong2*>(pend_rd) + i, pk);
         } else {
-            x.p0 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i);
-            x.p1 = __ldcg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i + 1);
+            x.p0 = ldp_cg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i, pk);
+            x.p1 = ldp_cg(reinterpret_cast<const ulonglong2*>(pend_rd) + 2 * (size_t)i + 1, pk);
         }
     } else {
-        x.isyn = a.i_syn[i];
+        x.isyn = ldp(a.i_syn + i, pf);
     }
 }
 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u, a.tiled ? a.acc_bytes : 0u);
+    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u);
     SegParams* s_seg = reinterpret_cast<SegParams*>(smem + L.seg);
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
     unsigned char* s_meta_base = smem + L.meta;
     __shared__ uint32_t s_nspk;
-    __shared__ uint32_t s_rcnt;
-    __shared__ uint32_t s_bn[129], s_bd[128];  // binning: segments per spike, dir offsets
-    __shared__ uint64_t s_br[128];             // binning: row starts
+    __shared__ uint32_t s_fwork;  // next 32-neuron update chunk of the phase
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
     __shared__ uint32_t s_hcnt[64];  // dynamic delivery: peer batch sizes of the phase
@@ -732,6 +597,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     }
     if (threadIdx.x == 0) {
         s_nspk = 0;
+        s_fwork = 0;
         for (int k = 0; k < kStages; ++k) {
             mbar_init(s_bar + k, 1);                          // full: producer + tx bytes
             mbar_init(s_bar + kStages + k, VXB_DWARPS > 1 ? VXB_DWARPS - 1 : 1);  // empty
@@ -742,37 +608,29 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
 
     const uint32_t lane = threadIdx.x & 31;
     // Warp roles: the first VXB_DWARPS warps of every CTA run the delivery
-    // pipeline (bulk copies + atomics, L2-atomic bound) while the others run
-    // the neuron update (HBM bound), so both units are busy on every SM.
-#if VXB_DWARPS > 0
+    // pipeline (bulk copies + atomics, L2-atomic bound) and then join the
+    // others on the neuron update, which every warp takes in 32-neuron
+    // chunks of the CTA's contiguous neuron range.
+    static_assert(VXB_DWARPS >= 2, "delivery needs a producer and a consumer warp");
     constexpr uint32_t kDT = VXB_DWARPS * 32;
-    const bool roleD = threadIdx.x < kDT, roleF = !roleD;
-    const uint32_t f_first = kDT, f_cta = blockDim.x - kDT, d_cta = kDT;
-#else
-    const bool roleD = true, roleF = true;
-    const uint32_t f_first = 0, f_cta = blockDim.x, d_cta = blockDim.x;
-#endif
-    auto fsync = [&] {
-#if VXB_DWARPS > 0
-        asm volatile("bar.sync 1, %0;" ::"r"(f_cta) : "memory");
-#else
-        __syncthreads();
-#endif
-    };
-    auto dsync = [&] {
-#if VXB_DWARPS > 0
-        asm volatile("bar.sync 2, %0;" ::"r"(d_cta) : "memory");
-#else
-        __syncthreads();
-#endif
-    };
-    const uint32_t gtid = blockIdx.x * f_cta + (threadIdx.x - f_first);  // F threads
-    const uint32_t gthreads = gridDim.x * f_cta;
+    const bool roleD = threadIdx.x < kDT;
+    const uint32_t d_cta = kDT;
+    // this CTA's neurons: [c_lo, c_hi), multiples of 32 apart
+    const uint32_t per = (((a.n + gridDim.x - 1) / gridDim.x) + 31u) & ~31u;
+    const uint32_t c_lo = min(a.n, blockIdx.x * per), c_hi = min(a.n, c_lo + per);
+    const uint32_t nch = (c_hi - c_lo + 31u) >> 5;
     Control* ctl = a.ctl;
     unsigned long long my_inner = 0, my_outer = 0;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
-    uint32_t g_item = 0;  // pieces this CTA has consumed since launch (stage/parity)
+    const uint64_t pol_f = a.f_policy ? pol_stream : policy_evict_normal();
+    // the update's read + zeroing of the pending buffer: kept in L2 for the
+    // next phase's atomics when the buffer fits; evict-first when it is
+    // L2-blocked, or the zeroed lines would displace the live block
+    const uint64_t pol_pz = a.n_blocks > 1 ? pol_stream : pol_keep;
+    uint32_t g_item = 0;  // stages this CTA has consumed since launch (stage/parity)
+    // warp-uniform cache of the parameter segment last looked up
+    uint32_t seg_hint = 0, seg_lo = 1u, seg_nx = 0u;
 
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
@@ -793,297 +651,18 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         }
         const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
 
-        // D work of this phase: pieces of the rows of S(tE), dealt to CTAs
-        // round-robin (local spikes, then every peer's batch).
-        uint32_t d_lo = 0, d_cnt = 0, d_C = 1, d_prev = 0;
+        // D work of this phase: the rows of S(tE) (local spikes, then every
+        // peer's batch)
+        uint32_t d_lo = 0, d_cnt = 0, d_prev = 0;
         if (doE) {
             d_lo = (ph >= 2 && !a.ring) ? __ldcg(a.seg_end + ph - 2) : 0u;
             d_cnt = __ldcg(a.seg_end + ph - 1) - d_lo;
             d_prev = a.ring ? ((ph - 1) & 1u) * a.n : 0u;
-            d_C = a.pieces;
         }
-
-        // ------------------------------------------------------------ F
-        if (roleF) {
-        const uint32_t n_round = (a.n + 31u) & ~31u;
-        NIn<PACKED> cur, nxt;
-        uint32_t seg_hint = 0;  // warp-uniform: segment of the warp's previous first neuron
-        if (gtid < a.n) load_neuron<PACKED>(a, gtid, doE, pend_rd, cur);
-        for (uint32_t i = gtid; i < n_round; i += gthreads) {
-            const bool live = i < a.n;
-            const uint32_t inext = i + gthreads;
-            if (inext < a.n) load_neuron<PACKED>(a, inext, doE, pend_rd, nxt);
-            bool spiked = false;
-            // parameter segment: one binary search per warp (lanes hold
-            // consecutive neurons), then a short forward walk per lane
-            uint32_t seg;
-            {
-                const uint32_t il = live ? i : a.n - 1;
-                uint32_t s0 = 0;
-                if (lane == 0) s0 = find_seg_from(startp, a.nseg, il, seg_hint);
-                seg = __shfl_sync(0xffffffffu, s0, 0);
-                seg_hint = seg;
-                while (seg + 1 < a.nseg && startp[seg + 1] <= il) ++seg;
-            }
-            if (live) {
-                const SegParams& P = segp[seg];
-                uint32_t vb = cur.vb;
-                const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                float4 j = cur.j;
-                float iou = cur.iou;
-                float isyn;
-                if (doE) {
-                    // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
-                    float p0, p1, p2, p3;
-                    if constexpr (PACKED) {
-                        p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
-                        p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
-                        p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
-                        p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
-                        if (!a.tiled)  // tiled delivery overwrites whole tiles instead
-                            __stcg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull));
-                    } else {
-                        p0 = dequantize((int64_t)cur.p0.x);
-                        p1 = dequantize((int64_t)cur.p0.y);
-                        p2 = dequantize((int64_t)cur.p1.x);
-                        p3 = dequantize((int64_t)cur.p1.y);
-                        ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
-                        if (!a.tiled) {
-                            __stcg(q, make_ulonglong2(0ull, 0ull));
-                            __stcg(q + 1, make_ulonglong2(0ull, 0ull));
-                        }
-                    }
-                    j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
-                    j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
-                    j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
-                    j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
-                    // current_kernel (model.hpp:73-81), u order, from 0.0f
-                    const float4 g = cur.g;
-                    float c = 0.0f;
-                    c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
-                    c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
-                    c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
-                    c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
-                    isyn = c;
-                    // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
-                    float xi = 0.0f;
-                    if (P.sigma_pos) {
-                        const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
-                        xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
-                    }
-                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
-                    if (!doA) a.i_syn[i] = isyn;
-                    a.j[i] = j;
-                    a.i_ou[i] = iou;
-                } else {
-                    isyn = cur.isyn;
-                }
-                if (doA) {
-                    // membrane_kernel + threshold (engine.cpp:363-385)
-                    if (is_refrac(vb)) {
-                        const uint32_t r = (vb & 0x007fffffu) - 1u;
-                        vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
-                    } else {
-                        float inoise = iou;
-                        if (inj_ep) {
-                            const float x =
-                                __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
-                            if (x != 0.0f) inoise = fadd(iou, x);
-                        }
-                        const float nv = fadd(
-                            v, fmul(P.dt_over_c,
-                                    fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
-                        if (!isfinite(nv)) {
-                            atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
-                            vb = __float_as_uint(nv);
-                        } else if (nv >= P.v_th) {
-                            spiked = true;
-                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                        } else {
-                            vb = __float_as_uint(nv);
-                        }
-                    }
-                    // forced spikes (engine.cpp:389-398): join unless already fired
-                    if (f_hi > f_lo && !spiked) {
-                        const uint32_t k =
-                            f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
-                        if (k < f_hi && __ldg(a.forced_local + k) == i) {
-                            spiked = true;
-                            vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                        }
-                    }
-                    a.v[i] = vb;
-                }
-                // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
-                if (a.n_probes) {
-                    uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
-                    while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
-                        const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
-                        if (doE) a.probe_i[row + ph - 1] = isyn;
-                        if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                        ++k;
-                    }
-                }
-            }
-            // spike staging + rates (engine.cpp:400-404), warp aggregated
-            bool overflow_route = false;
-            const unsigned ball = __ballot_sync(0xffffffffu, spiked);
-            if (ball) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (spiked) {
-                    const unsigned rank = __popc(ball & ((1u << lane) - 1u));
-                    if (base + rank < kSpkStage)
-                        s_spk[base + rank] = i;
-                    else {  // staging full: straight to the log (and to the peers / tiles)
-                        a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
-                        if (a.world > 1) overflow_route = true;
-                        if (a.tiled) bin_spike(a, i, tA & 1u, my_inner, my_outer);
-                    }
-                    const uint32_t unit = segp[seg].unit;
-                    const unsigned peers = __match_any_sync(ball, unit);
-                    if ((unsigned)__ffs(peers) - 1u == lane)
-                        atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
-                }
-            }
-            if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
-                if (exchange_route(a, i, overflow_route, tA % 3u)) __threadfence_system();
-            cur = nxt;
-        }
-        // flush the CTA's staged spikes with one log reservation
-        fsync();
-        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
-        if (threadIdx.x == f_first && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
-        fsync();
-        for (uint32_t k = threadIdx.x - f_first; k < nst; k += f_cta)
-            a.spk[log_base + s_base + k] = s_spk[k];
-        if (a.tiled && doA) {
-            // bin the staged spikes into the tile queues: one thread per
-            // (spike, tile segment) pair, 128 spikes per round
-            for (uint32_t c0 = 0; c0 < nst; c0 += 128) {
-                const uint32_t cn = min(128u, nst - c0);
-                const uint32_t fl = threadIdx.x - f_first;
-                if (fl < cn) {
-                    const uint32_t sp = s_spk[c0 + fl];
-                    const uint32_t d0 = __ldg(a.dir_off + sp), d1 = __ldg(a.dir_off + sp + 1);
-                    const uint64_t row = ldg64(a.off + sp), len = ldg64(a.off + sp + 1) - row;
-                    const uint32_t in = __ldg(a.inner + sp);
-                    my_inner += 2ull * in;
-                    my_outer += 2ull * (len - in);
-                    s_bn[fl] = d1 - d0;
-                    s_bd[fl] = d0;
-                    s_br[fl] = row;
-                }
-                fsync();
-                if (threadIdx.x == f_first) {  // exclusive prefix (<= 128 spikes)
-                    uint32_t acc = 0;
-                    for (uint32_t k = 0; k < cn; ++k) {
-                        const uint32_t v = s_bn[k];
-                        s_bn[k] = acc;
-                        acc += v;
-                    }
-                    s_bn[cn] = acc;
-                }
-                fsync();
-                const uint32_t tot = s_bn[cn];
-                for (uint32_t pidx = fl; pidx < tot; pidx += f_cta) {
-                    uint32_t lo = 0, hi = cn;  // spike k with s_bn[k] <= pidx < s_bn[k+1]
-                    while (hi - lo > 1) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (s_bn[mid] <= pidx) lo = mid; else hi = mid;
-                    }
-                    const uint64_t e = ldg64(a.dir + s_bd[lo] + (pidx - s_bn[lo]));
-                    const uint32_t tile = (uint32_t)(e >> 12) & 0xfffffu;
-                    const uint64_t start = s_br[lo] + (e >> 32), lm1 = e & 0xfffull;
-                    const uint32_t set = tA & 1u;
-                    const uint32_t qpos = atomicAdd(a.qcount + (size_t)set * a.n_tiles + tile, 1u);
-                    a.queue[(size_t)set * a.q_total + ldg64(a.qbase + tile) + qpos] =
-                        start | (lm1 << 40);
-                }
-                fsync();
-            }
-        }
-        if (a.world > 1 && doA) {
-            bool sent = false;
-            const uint32_t nr = (nst + 31u) & ~31u;
-            for (uint32_t k = threadIdx.x - f_first; k < nr; k += f_cta)
-                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % 3u);
-            if (sent) __threadfence_system();
-        }
-        if (threadIdx.x == f_first) s_nspk = 0;
-        }  // roleF
 
         // ------------------------------------------------------------ D
         unsigned long long wait_ns = 0;
-        if (roleD && doE && a.tiled) {
-            // Tiled delivery of S(tE): this CTA owns whole target tiles; the
-            // queued row segments are streamed in by bulk copies and summed
-            // with shared-memory atomics, then every tile's pending sums are
-            // stored with plain coalesced stores (no global atomics, no
-            // zeroing pass: each tile is overwritten entirely).
-            const uint32_t set = tE & 1u;
-            unsigned long long* acc = reinterpret_cast<unsigned long long*>(smem + L.acc);
-            const uint32_t acc_words = a.acc_bytes / 8;
-            for (uint32_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-                for (uint32_t k = threadIdx.x; k < acc_words; k += d_cta) acc[k] = 0ull;
-                if (threadIdx.x == 0) s_rcnt = atomicExch(a.qcount + (size_t)set * a.n_tiles + tile, 0u);
-                dsync();
-                const uint32_t cnt = s_rcnt;
-                const uint64_t* q = a.queue + (size_t)set * a.q_total + ldg64(a.qbase + tile);
-                const uint32_t tbase = tile << kTileLog;
-                uint32_t qi = 0;
-                bool ended = false;
-                if (threadIdx.x == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    for (uint32_t j = 0; j < (uint32_t)kStages && !ended; ++j)
-                        ended = issue_tstage(a, smem, L, (g_item + j) % kStages, q, cnt, qi, pol_stream);
-                }
-                for (;;) {
-                    const uint32_t st = g_item % kStages;
-                    mbar_wait(s_bar + st, (g_item / kStages) & 1u);
-                    ++g_item;
-                    const TStageMeta* m = reinterpret_cast<const TStageMeta*>(s_meta_base + st * kMetaBytes);
-                    const uint32_t n_e = m->n, last = m->end;
-                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes);
-                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes);
-                    uint32_t sg = 0;
-                    for (uint32_t e = threadIdx.x; e < n_e; e += d_cta) {
-                        while (e >= m->pre[sg + 1]) ++sg;
-                        const uint32_t r = e - m->pre[sg];
-                        const uint32_t t = tg[m->tb[sg] + r], tl = (t & 0x7fffffffu) - tbase, cls = t >> 31;
-                        const uint64_t wq = wv[m->wb[sg] + r];
-                        if constexpr (PACKED) {
-                            // carry-free packed pair: two native 32-bit shared
-                            // atomics give the same 64-bit word (64-bit shared
-                            // atomics are CAS loops on sm_100)
-                            unsigned int* a32 = reinterpret_cast<unsigned int*>(acc + 2 * tl + cls);
-                            atomicAdd(a32, (unsigned int)wq);
-                            atomicAdd(a32 + 1, (unsigned int)(wq >> 32));
-                        } else {
-                            atomicAdd(acc + 4 * tl + 2 * cls,
-                                      (unsigned long long)(int64_t)(int32_t)(uint32_t)wq);
-                            atomicAdd(acc + 4 * tl + 2 * cls + 1,
-                                      (unsigned long long)(int64_t)(int32_t)(uint32_t)(wq >> 32));
-                        }
-                    }
-                    dsync();  // stage st drained by every delivery thread
-                    if (last) break;
-                    if (threadIdx.x == 0 && !ended) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        ended = issue_tstage(a, smem, L, st, q, cnt, qi, pol_stream);
-                    }
-                }
-                // store the tile's pending sums (whole tile, coalesced 16 B)
-                const uint32_t nt = min((uint32_t)kTile, a.n - tbase);
-                const uint32_t words = nt * (PACKED ? 2u : 4u);
-                ulonglong2* dst = reinterpret_cast<ulonglong2*>(
-                    reinterpret_cast<unsigned long long*>(pend_wr) + (size_t)tbase * (PACKED ? 2u : 4u));
-                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(acc);
-                for (uint32_t k = threadIdx.x; k < words / 2; k += d_cta) __stcg(dst + k, src[k]);
-                dsync();  // acc reused by the next tile
-            }
-        } else if (roleD && doE) {
+        if (roleD && doE) {
             // Producer / consumer delivery pipeline: warp 0 lane 0 packs the
             // rows of this CTA's spikes (local list, then each peer's batch
             // once its step flag is set) into the stage ring with bulk copies;
@@ -1247,6 +826,186 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             }
         }
 
+
+        // ------------------------------------------------------------ F
+        // 32-neuron chunks from the CTA's counter; loads of the next chunk
+        // are in flight while the current one is updated
+        {
+            NIn<PACKED> cur, nxt;
+            uint32_t ch = 0;
+            if (lane == 0) ch = atomicAdd(&s_fwork, 1u);
+            ch = __shfl_sync(0xffffffffu, ch, 0);
+            uint32_t i = c_lo + (ch << 5) + lane;
+            if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, pol_f, pol_pz);
+            while (ch < nch) {
+                uint32_t chn = 0;
+                if (lane == 0) chn = atomicAdd(&s_fwork, 1u);
+                chn = __shfl_sync(0xffffffffu, chn, 0);
+                const uint32_t inext = c_lo + (chn << 5) + lane;
+                if (chn < nch && inext < c_hi)
+                    load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, pol_f, pol_pz);
+                const bool live = i < c_hi;
+                bool spiked = false;
+                // parameter segment: warp-uniform cached range, a galloping
+                // search when the chunk leaves it, a per-lane walk only for
+                // lanes past a segment boundary
+                uint32_t seg;
+                {
+                    const uint32_t w_lo = c_lo + (ch << 5);
+                    const uint32_t w_last = min(w_lo + 31u, c_hi - 1u);
+                    if (w_lo < seg_lo || w_last >= seg_nx) {
+                        uint32_t s0 = 0;
+                        if (lane == 0)
+                            s0 = find_seg_from(startp, a.nseg, w_lo, w_lo >= seg_lo ? seg_hint : 0u);
+                        seg_hint = __shfl_sync(0xffffffffu, s0, 0);
+                        seg_lo = startp[seg_hint];
+                        seg_nx = seg_hint + 1 < a.nseg ? startp[seg_hint + 1] : a.n;
+                    }
+                    seg = seg_hint;
+                    const uint32_t il = live ? i : c_hi - 1u;
+                    if (il >= seg_nx)
+                        while (seg + 1 < a.nseg && startp[seg + 1] <= il) ++seg;
+                }
+                if (live) {
+                    const SegParams& P = segp[seg];
+                    uint32_t vb = cur.vb;
+                    const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                    float4 j = cur.j;
+                    float iou = cur.iou;
+                    float isyn;
+                    if (doE) {
+                        // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
+                        float p0, p1, p2, p3;
+                        if constexpr (PACKED) {
+                            p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
+                            p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
+                            p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
+                            p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
+                            stp_cg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull), pol_pz);
+                        } else {
+                            p0 = dequantize((int64_t)cur.p0.x);
+                            p1 = dequantize((int64_t)cur.p0.y);
+                            p2 = dequantize((int64_t)cur.p1.x);
+                            p3 = dequantize((int64_t)cur.p1.y);
+                            ulonglong2* q = reinterpret_cast<ulonglong2*>(pend_rd) + 2 * (size_t)i;
+                            stp_cg(q, make_ulonglong2(0ull, 0ull), pol_pz);
+                            stp_cg(q + 1, make_ulonglong2(0ull, 0ull), pol_pz);
+                        }
+                        j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
+                        j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
+                        j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
+                        j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
+                        // current_kernel (model.hpp:73-81), u order, from 0.0f
+                        const float4 g = cur.g;
+                        float c = 0.0f;
+                        c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
+                        c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
+                        c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
+                        c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
+                        isyn = c;
+                        // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
+                        float xi = 0.0f;
+                        if (P.sigma_pos) {
+                            const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
+                            xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
+                        }
+                        iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                        if (!doA) stp(a.i_syn + i, isyn, pol_f);
+                        stp(a.j + i, j, pol_f);
+                        stp(a.i_ou + i, iou, pol_f);
+                    } else {
+                        isyn = cur.isyn;
+                    }
+                    if (doA) {
+                        // membrane_kernel + threshold (engine.cpp:363-385)
+                        if (is_refrac(vb)) {
+                            const uint32_t r = (vb & 0x007fffffu) - 1u;
+                            vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
+                        } else {
+                            float inoise = iou;
+                            if (inj_ep) {
+                                const float x =
+                                    __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
+                                if (x != 0.0f) inoise = fadd(iou, x);
+                            }
+                            const float nv = fadd(
+                                v, fmul(P.dt_over_c,
+                                        fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                            if (!isfinite(nv)) {
+                                atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
+                                vb = __float_as_uint(nv);
+                            } else if (nv >= P.v_th) {
+                                spiked = true;
+                                vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                            } else {
+                                vb = __float_as_uint(nv);
+                            }
+                        }
+                        // forced spikes (engine.cpp:389-398): join unless already fired
+                        if (f_hi > f_lo && !spiked) {
+                            const uint32_t k =
+                                f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                            if (k < f_hi && __ldg(a.forced_local + k) == i) {
+                                spiked = true;
+                                vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                            }
+                        }
+                        stp(a.v + i, vb, pol_f);
+                    }
+                    // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
+                    if (a.n_probes) {
+                        uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                        while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                            const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
+                            if (doE) a.probe_i[row + ph - 1] = isyn;
+                            if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                            ++k;
+                        }
+                    }
+                }
+                // spike staging + rates (engine.cpp:400-404), warp aggregated
+                bool overflow_route = false;
+                const unsigned ball = __ballot_sync(0xffffffffu, spiked);
+                if (ball) {
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (spiked) {
+                        const unsigned rank = __popc(ball & ((1u << lane) - 1u));
+                        if (base + rank < kSpkStage)
+                            s_spk[base + rank] = i;
+                        else {  // staging full: straight to the log (and to the peers)
+                            a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                            if (a.world > 1) overflow_route = true;
+                        }
+                        const uint32_t unit = segp[seg].unit;
+                        const unsigned peers = __match_any_sync(ball, unit);
+                        if ((unsigned)__ffs(peers) - 1u == lane)
+                            atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
+                    }
+                }
+                if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
+                    if (exchange_route(a, i, overflow_route, tA % 3u)) __threadfence_system();
+                cur = nxt;
+                ch = chn;
+                i = inext;
+            }
+        }
+        // flush the CTA's staged spikes with one log reservation
+        __syncthreads();
+        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
+        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x)
+            a.spk[log_base + s_base + k] = s_spk[k];
+        if (a.world > 1 && doA) {
+            bool sent = false;
+            const uint32_t nr = (nst + 31u) & ~31u;
+            for (uint32_t k = threadIdx.x; k < nr; k += blockDim.x)
+                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % 3u);
+            if (sent) __threadfence_system();
+        }
+
         if (threadIdx.x == 0 && wait_ns && a.phase_wait) atomicMax(a.phase_wait + ph, wait_ns);
         grid_barrier(
             ctl,
@@ -1258,8 +1017,11 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             [&] {
                 if (a.world > 1 && doA) exchange_publish(a, tA);
             });
-        if (threadIdx.x == 0)  // L2-coherent reads
+        if (threadIdx.x == 0) {  // L2-coherent reads
             s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
+            s_nspk = 0;
+            s_fwork = 0;
+        }
         __syncthreads();
         if (s_stop) break;
     }
@@ -1334,48 +1096,6 @@ __global__ void csr_scatter_kernel(const SynIn* __restrict__ e,
         }
         neg = __any_sync(0xffffffffu, neg);
         if (lane == 0 && (neg || sf >= (1ll << 32) || ss >= (1ll << 32))) atomicExch(wide, 1u);
-    }
-}
-
-// Tiled delivery tables: rows are sorted by target; a segment is the run of a
-// row inside one target tile, split so that no piece exceeds a stage.
-__global__ void tile_dir_count_kernel(const uint64_t* __restrict__ off,
-                                      const uint32_t* __restrict__ tgt, uint32_t n_src,
-                                      uint32_t* __restrict__ nseg, uint32_t* __restrict__ tile_cap) {
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_src; s += gridDim.x * blockDim.x) {
-        const uint64_t e0 = off[s], e1 = off[s + 1];
-        uint32_t cnt = 0;
-        uint64_t k = e0;
-        while (k < e1) {
-            const uint32_t tile = (tgt[k] & 0x7fffffffu) >> kTileLog;
-            uint64_t j = k + 1;
-            while (j < e1 && ((tgt[j] & 0x7fffffffu) >> kTileLog) == tile) ++j;
-            const uint32_t pieces = (uint32_t)((j - k + kStageE - 1) / kStageE);
-            cnt += pieces;
-            atomicAdd(tile_cap + tile, pieces);
-            k = j;
-        }
-        nseg[s] = cnt;
-    }
-}
-
-__global__ void tile_dir_fill_kernel(const uint64_t* __restrict__ off,
-                                     const uint32_t* __restrict__ tgt, uint32_t n_src,
-                                     const uint32_t* __restrict__ dir_off, uint64_t* __restrict__ dir) {
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_src; s += gridDim.x * blockDim.x) {
-        const uint64_t e0 = off[s], e1 = off[s + 1];
-        uint32_t at = dir_off[s];
-        uint64_t k = e0;
-        while (k < e1) {
-            const uint32_t tile = (tgt[k] & 0x7fffffffu) >> kTileLog;
-            uint64_t j = k + 1;
-            while (j < e1 && ((tgt[j] & 0x7fffffffu) >> kTileLog) == tile) ++j;
-            for (uint64_t p = k; p < j; p += kStageE) {
-                const uint64_t len = min((uint64_t)kStageE, j - p);
-                dir[at++] = ((p - e0) << 32) | ((uint64_t)tile << 12) | (len - 1);
-            }
-            k = j;
-        }
     }
 }
 

@@ -391,16 +391,32 @@ def test_acceptance_1_multi_worker_equivalence():
         assert np.array_equal(state, ref_state)
 
 
-def test_tiled_delivery_mode_matches_reference(monkeypatch):
-    """Experimental tiled delivery (VXB_TILED=1): target-sorted rows, tile
-    queues, shared-memory accumulation — must stay bit-exact."""
-    monkeypatch.setenv("VXB_TILED", "1")
+@pytest.mark.parametrize("dyn", ["0", "1"])
+def test_static_and_dynamic_delivery_match_reference(monkeypatch, dyn):
+    """Both producer schedules — static round-robin rows (VXB_DYN=0) and the
+    default block-major dynamic chunks — are bit-exact (config 1 shape)."""
+    monkeypatch.setenv("VXB_DYN", dyn)
     cfg = make_config(seed=1, voxels=1, npv=10000, k_in=100, dt_ms=0.1, steps=3000)
     net = RefNet(cfg)
     opt = SimOptions(steps=3000, dt_ms=0.1, probe_gids=[0, 4321, 9999])
     gpu, snaps = gpu_run(net.tables, opt)
     rs = RefSim(net, opt)
     ref = rs.advance(3000)
+    assert_same(gpu, ref)
+    assert np.array_equal(snaps[0], rs.membrane_snapshot(0))
+
+
+def test_many_segments_global_parameter_table():
+    """More parameter segments than fit in shared memory (600 units): the
+    segment table stays in global memory and the cached/galloping lookup
+    must still find every neuron's segment."""
+    net = RefNet(hot_cfg(seed=23, voxels=300, npv=30, k_in=8, rho=0.3))
+    assert net.tables.units.shape[0] > 256
+    opt = SimOptions(steps=60, probe_gids=[0, 4444, 8999])
+    gpu, snaps = gpu_run(net.tables, opt)
+    rs = RefSim(net, opt)
+    ref = rs.advance(60)
+    assert ref.total_spikes > 0
     assert_same(gpu, ref)
     assert np.array_equal(snaps[0], rs.membrane_snapshot(0))
 

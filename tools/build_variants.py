@@ -6,11 +6,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2308_01241_b200 import build as b
 
 VARIANTS = {
-    "dw4": {"VXB_DWARPS": 4},
-    "dw5": {"VXB_DWARPS": 5},
-    "dw4s6e512": {"VXB_DWARPS": 4, "VXB_STAGES": 6, "VXB_STAGE_E": 512},
-    "dw4s8e384": {"VXB_DWARPS": 4, "VXB_STAGES": 8, "VXB_STAGE_E": 384},
-    "t384dw6": {"VXB_THREADS": 384, "VXB_MINB": 2, "VXB_DWARPS": 6},
+    "m4": {"VXB_MINB": 4},
+    "t384m2": {"VXB_THREADS": 384, "VXB_MINB": 2},
+    "t384m2dw4": {"VXB_THREADS": 384, "VXB_MINB": 2, "VXB_DWARPS": 4},
+    "t512m2dw4": {"VXB_THREADS": 512, "VXB_MINB": 2, "VXB_DWARPS": 4},
+    "t320m3": {"VXB_THREADS": 320, "VXB_MINB": 3},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

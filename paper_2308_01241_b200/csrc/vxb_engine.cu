@@ -172,7 +172,9 @@ struct Engine {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid = 0;
-    DevBuf<SegParams> d_seg;
+    DevBuf<ParamSet> d_pset;
+    DevBuf<SegInfo> d_sinfo;
+    uint32_t npset = 0;
     DevBuf<uint32_t> d_seg_start;
     DevBuf<uint32_t> d_v;
     DevBuf<float4> d_j;
@@ -447,10 +449,44 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
 
-    d_seg.alloc(segs.size());
+    {  // device segment tables: shared parameter sets + per-segment info
+        std::vector<ParamSet> ps;
+        std::vector<SegInfo> si(segs.size());
+        for (size_t k = 0; k < segs.size(); ++k) {
+            const SegParams& g = segs[k];
+            ParamSet p;
+            std::memset(&p, 0, sizeof p);
+            p.tref = g.tref;
+            p.dt_over_c = g.dt_over_c;
+            p.g_leak = g.g_leak;
+            p.e_leak = g.e_leak;
+            p.v_th = g.v_th;
+            p.v_reset = g.v_reset;
+            for (int r = 0; r < 4; ++r) {
+                p.decay[r] = g.decay[r];
+                p.omega[r] = g.omega[r];
+                p.e_rev[r] = g.e_rev[r];
+            }
+            p.ou_mu = g.ou_mu;
+            p.ou_a = g.ou_a;
+            p.ou_b = g.ou_b;
+            p.sigma_pos = g.sigma_pos;
+            size_t idx = 0;
+            while (idx < ps.size() && std::memcmp(&ps[idx], &p, sizeof p) != 0) ++idx;
+            if (idx == ps.size()) ps.push_back(p);
+            si[k] = SegInfo{g.gid_off, g.unit, g.voxel, (uint32_t)idx, 0u};
+        }
+        npset = (uint32_t)ps.size();
+        d_pset.alloc(std::max<size_t>(1, ps.size()));
+        d_sinfo.alloc(std::max<size_t>(1, si.size()));
+        if (!ps.empty())
+            CK(cudaMemcpyAsync(d_pset.p, ps.data(), ps.size() * sizeof(ParamSet),
+                               cudaMemcpyHostToDevice, stream));
+        if (!si.empty())
+            CK(cudaMemcpyAsync(d_sinfo.p, si.data(), si.size() * sizeof(SegInfo),
+                               cudaMemcpyHostToDevice, stream));
+    }
     d_seg_start.alloc(seg_start.size());
-    CK(cudaMemcpyAsync(d_seg.p, segs.data(), segs.size() * sizeof(SegParams),
-                       cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_seg_start.p, seg_start.data(), seg_start.size() * 4,
                        cudaMemcpyHostToDevice, stream));
     d_v.alloc(n);
@@ -555,8 +591,9 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     if (const char* env = std::getenv("VXB_DYN")) dyn = std::atoi(env) != 0;
 
     // cooperative grid
-    use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg;
-    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u).total;
+    use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg && npset <= (uint32_t)kMaxSmemPset;
+    smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u,
+                            use_smem_seg ? npset : 0u).total;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const void* kfn = packed ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
@@ -569,6 +606,12 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
                                                          smem_bytes));
     if (per_sm < 1) throw SimError("step kernel cannot be resident on this device");
     grid = sms * per_sm;
+    if (std::getenv("VXB_VERBOSE"))
+        std::fprintf(stderr,
+                     "vxb: n=%u n_src=%u syn=%llu segs=%zu psets=%u smem_seg=%d smem=%u B "
+                     "grid=%d (%d/SM) blocks=%u packed=%d dyn=%d\n",
+                     n, n_src, (unsigned long long)n_syn, segs.size(), npset, (int)use_smem_seg,
+                     smem_bytes, grid, per_sm, n_blocks, (int)packed, (int)dyn);
     // L2 residency of the pending buffers: evict_last lines are retained
     // within the persisting carve-out, so size it to the device maximum
     // (VXB_PERSIST=0 leaves the driver default)
@@ -1275,6 +1318,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     std::memset(&a, 0, sizeof a);
     a.n = n;
     a.nseg = (uint32_t)segs.size();
+    a.npset = npset;
     a.n_units = n_units;
     a.steps = steps;
     a.t0 = t0;
@@ -1285,7 +1329,8 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.use_smem_seg = use_smem_seg ? 1u : 0u;
     a.dtf = dtf;
     a.ou_root = mix_key(seed, 1);  // rngstream::ou_noise (rng.hpp:18)
-    a.seg = d_seg.p;
+    a.pset = d_pset.p;
+    a.sinfo = d_sinfo.p;
     a.seg_start = d_seg_start.p;
     a.v = d_v.p;
     a.j = d_j.p;

@@ -49,6 +49,27 @@ struct SegParams {
 };
 static_assert(sizeof(SegParams) == 128, "SegParams layout");
 
+// Device form of the segments: the float parameters are shared by every
+// segment of a population (ParamSet, a handful per network) and a segment
+// only keeps its unit, voxel, gid offset and parameter-set index (SegInfo),
+// so networks with ~1000 units still keep the whole table in shared memory.
+struct ParamSet {
+    uint32_t tref;
+    float dt_over_c, g_leak, e_leak, v_th, v_reset;
+    float decay[4];
+    float omega[4];
+    float e_rev[4];
+    float ou_mu, ou_a, ou_b;
+    uint32_t sigma_pos;
+    uint32_t pad[2];
+};
+static_assert(sizeof(ParamSet) == 96, "ParamSet layout");
+struct SegInfo {
+    int64_t gid_off;
+    uint32_t unit, voxel, pset, pad;
+};
+static_assert(sizeof(SegInfo) == 24, "SegInfo layout");
+
 // Refractory neurons hold V = V_reset (engine.cpp:364-367); the counter is
 // kept in the V word as a negative NaN payload so the state is one word.
 __host__ __device__ __forceinline__ bool is_refrac(uint32_t bits) {
@@ -92,6 +113,7 @@ struct StepArgs {
     // sizes
     uint32_t n;             // shard neurons
     uint32_t nseg;
+    uint32_t npset;
     uint32_t n_units;
     uint32_t steps;         // A steps in this chunk (phases = steps + 1)
     uint32_t t0;            // absolute step of the chunk's first A
@@ -103,7 +125,8 @@ struct StepArgs {
     float dtf;
     uint64_t ou_root;       // mix_key(seed, rngstream::ou_noise)
     // parameters
-    const SegParams* seg;
+    const ParamSet* pset;
+    const SegInfo* sinfo;
     const uint32_t* seg_start;
     // state
     uint32_t* v;            // float bits or refractory code
@@ -265,7 +288,8 @@ struct Pend<false> {  // four signed int64 buckets, the reference's layout
     };
 };
 
-constexpr int kMaxSmemSeg = 256;
+constexpr int kMaxSmemSeg = 1024;   // segments kept in shared memory
+constexpr int kMaxSmemPset = 32;    // parameter sets kept in shared memory
 #ifndef VXB_THREADS
 #define VXB_THREADS 256
 #endif
@@ -278,6 +302,9 @@ constexpr int kSpkStage = 1024;  // per-CTA spike staging before one log append
 #define VXB_DWARPS 3
 #endif
 static_assert(VXB_DWARPS >= 2, "delivery needs a producer warp and >= 1 consumer warp");
+#ifndef VXB_PREFETCH
+#define VXB_PREFETCH 1  // L2 prefetch of the update state two chunks ahead
+#endif
 #ifndef VXB_STAGES
 #define VXB_STAGES 4
 #endif
@@ -305,14 +332,15 @@ constexpr uint32_t kMetaBytes = sizeof(TStageMeta);
 
 // Dynamic shared memory carve-up of step_kernel.
 struct SmemLayout {
-    uint32_t tgt, w, bar, meta, seg, start, spk, total;
-    __host__ __device__ explicit SmemLayout(uint32_t nseg_smem) {
+    uint32_t tgt, w, bar, meta, pset, seg, start, spk, total;
+    __host__ __device__ SmemLayout(uint32_t nseg_smem, uint32_t npset_smem) {
         tgt = 0;
         w = tgt + kStages * kStageTgtBytes;
         bar = w + kStages * kStageWBytes;
         meta = bar + 2 * kStages * 8;  // full barriers, then empty barriers
-        seg = (meta + kStages * kMetaBytes + 127) & ~127u;
-        start = seg + nseg_smem * (uint32_t)sizeof(SegParams);
+        pset = (meta + kStages * kMetaBytes + 127) & ~127u;
+        seg = pset + npset_smem * (uint32_t)sizeof(ParamSet);
+        start = seg + nseg_smem * (uint32_t)sizeof(SegInfo);
         spk = (start + (nseg_smem + 1) * 4 + 15) & ~15u;
         total = spk + kSpkStage * 4;
     }
@@ -572,8 +600,9 @@ __device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u);
-    SegParams* s_seg = reinterpret_cast<SegParams*>(smem + L.seg);
+    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u, a.use_smem_seg ? a.npset : 0u);
+    ParamSet* s_pset = reinterpret_cast<ParamSet*>(smem + L.pset);
+    SegInfo* s_seg = reinterpret_cast<SegInfo*>(smem + L.seg);
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
@@ -584,14 +613,17 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __shared__ int s_stop;
     __shared__ uint32_t s_hcnt[64];  // dynamic delivery: peer batch sizes of the phase
 
-    const SegParams* segp = a.seg;
+    const ParamSet* psp = a.pset;
+    const SegInfo* segp = a.sinfo;
     const uint32_t* startp = a.seg_start;
     if (a.use_smem_seg) {
         for (uint32_t k = threadIdx.x; k < a.nseg; k += blockDim.x) {
-            s_seg[k] = a.seg[k];
+            s_seg[k] = a.sinfo[k];
             s_start[k] = a.seg_start[k];
         }
+        for (uint32_t k = threadIdx.x; k < a.npset; k += blockDim.x) s_pset[k] = a.pset[k];
         if (threadIdx.x == 0) s_start[a.nseg] = a.n;
+        psp = s_pset;
         segp = s_seg;
         startp = s_start;
     }
@@ -832,15 +864,35 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         // are in flight while the current one is updated
         {
             NIn<PACKED> cur, nxt;
-            uint32_t ch = 0;
-            if (lane == 0) ch = atomicAdd(&s_fwork, 1u);
-            ch = __shfl_sync(0xffffffffu, ch, 0);
+            // chunk pipeline: ch is being updated, chn's state is in flight
+            // to registers, chn2's lines are being prefetched into L2
+            auto grab = [&]() {
+                uint32_t c = 0;
+                if (lane == 0) c = atomicAdd(&s_fwork, 1u);
+                return __shfl_sync(0xffffffffu, c, 0);
+            };
+            auto prefetch = [&](uint32_t c) {
+                if (VXB_PREFETCH == 0 || c >= nch) return;
+                const uint32_t b = c_lo + (c << 5);
+                const char* q = nullptr;
+                if (lane == 0) q = reinterpret_cast<const char*>(a.v + b);
+                else if (lane == 1) q = reinterpret_cast<const char*>(a.i_ou + b);
+                else if (lane < 6) q = reinterpret_cast<const char*>(a.j + b) + (lane - 2) * 128;
+                else if (doE && lane < 10) q = reinterpret_cast<const char*>(a.g + b) + (lane - 6) * 128;
+                else if (doE && lane < (PACKED ? 14u : 18u))
+                    q = reinterpret_cast<const char*>(pend_rd) + (size_t)b * (PACKED ? 16 : 32) +
+                        (lane - 10) * 128;
+                else if (!doE && lane == 10) q = reinterpret_cast<const char*>(a.i_syn + b);
+                if (q) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+            };
+            uint32_t ch = grab();
+            uint32_t chn = grab();
+            prefetch(chn);
             uint32_t i = c_lo + (ch << 5) + lane;
             if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, pol_f, pol_pz);
             while (ch < nch) {
-                uint32_t chn = 0;
-                if (lane == 0) chn = atomicAdd(&s_fwork, 1u);
-                chn = __shfl_sync(0xffffffffu, chn, 0);
+                const uint32_t chn2 = grab();
+                prefetch(chn2);
                 const uint32_t inext = c_lo + (chn << 5) + lane;
                 if (chn < nch && inext < c_hi)
                     load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, pol_f, pol_pz);
@@ -867,7 +919,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         while (seg + 1 < a.nseg && startp[seg + 1] <= il) ++seg;
                 }
                 if (live) {
-                    const SegParams& P = segp[seg];
+                    const SegInfo& S = segp[seg];
+                    const ParamSet& P = psp[S.pset];
                     uint32_t vb = cur.vb;
                     const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
                     float4 j = cur.j;
@@ -906,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         // ou_kernel (model.hpp:88-90) with xi = stream word tE (engine.cpp:551-558)
                         float xi = 0.0f;
                         if (P.sigma_pos) {
-                            const uint64_t gid = (uint64_t)((int64_t)i + P.gid_off);
+                            const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
                             xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
                         }
                         iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
@@ -925,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                             float inoise = iou;
                             if (inj_ep) {
                                 const float x =
-                                    __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + P.voxel);
+                                    __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + S.voxel);
                                 if (x != 0.0f) inoise = fadd(iou, x);
                             }
                             const float nv = fadd(
@@ -988,6 +1041,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                     if (exchange_route(a, i, overflow_route, tA % 3u)) __threadfence_system();
                 cur = nxt;
                 ch = chn;
+                chn = chn2;
                 i = inext;
             }
         }

@@ -448,6 +448,16 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t byte
 // kSegPerStage to a stage — so every bulk-copy round trip carries a full
 // stage whatever the row lengths.  Copies are issued as segments are added
 // (expect_tx per segment, one arrive at commit).
+// Scratch of the warp-parallel stage packing (producer warp only).
+constexpr int kMaxPieces = 2 * kSegPerStage;
+struct BatchScratch {
+    uint64_t sb0[32];                 // the warp's segments: first entry
+    uint32_t slen[32];                //                      length
+    uint64_t pb0[kMaxPieces];         // pieces laid out this round
+    uint32_t ptake[kMaxPieces], pst[kMaxPieces], ptoff[kMaxPieces], pwoff[kMaxPieces];
+    uint32_t np, ncom, more, com[2];
+};
+
 struct StageBuilder {
     uint32_t ctr;    // stages committed since launch (stage = ctr % kStages)
     uint32_t open;   // a stage is being filled
@@ -502,6 +512,97 @@ struct StageBuilder {
             ++ns;
             b0 = b1;
             len -= take;
+        }
+    }
+    // Warp-collective add of one segment per lane (len 0 = none).  Lane 0
+    // lays the segments out over stages (metadata only, cheap scalar work),
+    // all lanes then issue their pieces' bulk copies in parallel, and lane 0
+    // commits the stages the round closed.  A round touches at most two
+    // stages, so a deferred commit never holds a ring slot that this round
+    // waits for (kStages >= 3).  StageBuilder state is meaningful in lane 0.
+    __device__ __forceinline__ void add_batch(const StepArgs& a, unsigned char* smem,
+                                              const SmemLayout& L, uint64_t my_b0,
+                                              uint32_t my_len, uint64_t pol, BatchScratch& S,
+                                              uint32_t lane) {
+        if (!__any_sync(0xffffffffu, my_len != 0)) return;
+        S.sb0[lane] = my_b0;
+        S.slen[lane] = my_len;
+        __syncwarp();
+        uint32_t seg = 0, used = 0;  // lane 0's cursor over the warp's segments
+        for (;;) {
+            if (lane == 0) {
+                uint32_t np = 0, ncom = 0, touched = open ? 1u : 0u;
+                while (seg < 32) {
+                    const uint32_t len = S.slen[seg] - used;
+                    if (len == 0) {
+                        ++seg;
+                        used = 0;
+                        continue;
+                    }
+                    if (!open) {
+                        if (touched == 2) break;
+                        begin(smem, L);
+                        ++touched;
+                    }
+                    const int room_t = kStageE - (int)toff, room_w = kStageE - (int)woff;
+                    const int room = room_t < room_w ? room_t : room_w;
+                    const uint32_t st = ctr % kStages;
+                    TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+                    if (ns == (uint32_t)kSegPerStage || room <= 0) {  // close the stage
+                        m->pre[ns] = total;
+                        m->n = total;
+                        m->nseg = ns;
+                        m->end = 0;
+                        S.com[ncom++] = st;
+                        ++ctr;
+                        open = 0;
+                        continue;
+                    }
+                    const uint32_t take = min(len, (uint32_t)room);
+                    const uint64_t b0 = S.sb0[seg] + used, b1 = b0 + take;
+                    const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+                    m->pre[ns] = total;
+                    m->tb[ns] = toff + (uint32_t)(b0 - t0);
+                    m->wb[ns] = woff + (uint32_t)(b0 - w0);
+                    S.pb0[np] = b0;
+                    S.ptake[np] = take;
+                    S.pst[np] = st;
+                    S.ptoff[np] = toff;
+                    S.pwoff[np] = woff;
+                    ++np;
+                    total += take;
+                    toff += (uint32_t)(((b1 + 3) & ~3ull) - t0);
+                    woff += (uint32_t)(((b1 + 1) & ~1ull) - w0);
+                    ++ns;
+                    used += take;
+                }
+                S.np = np;
+                S.ncom = ncom;
+                S.more = seg < 32;
+            }
+            __syncwarp();
+            const uint32_t np = S.np;
+            if (lane < np) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (uint32_t q = lane; q < np; q += 32) {
+                const uint64_t b0 = S.pb0[q], b1 = b0 + S.ptake[q];
+                const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+                const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0);
+                const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
+                const uint32_t st = S.pst[q];
+                uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+                mbar_expect_tx_only(full, tn * 4 + wn * 8);
+                bulk_g2s(smem + L.tgt + st * kStageTgtBytes + S.ptoff[q] * 4, a.tgt + t0, tn * 4,
+                         full, pol);
+                bulk_g2s(smem + L.w + st * kStageWBytes + S.pwoff[q] * 8, a.w + w0, wn * 8, full,
+                         pol);
+            }
+            __syncwarp();
+            if (lane == 0)
+                for (uint32_t k = 0; k < S.ncom; ++k)
+                    mbar_arrive(reinterpret_cast<uint64_t*>(smem + L.bar) + S.com[k]);
+            const uint32_t more = S.more;
+            __syncwarp();
+            if (!more) break;
         }
     }
 };
@@ -612,6 +713,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __shared__ uint32_t s_base;
     __shared__ int s_stop;
     __shared__ uint32_t s_hcnt[64];  // dynamic delivery: peer batch sizes of the phase
+    __shared__ BatchScratch s_scr;   // producer warp: stage packing
 
     const ParamSet* psp = a.pset;
     const SegInfo* segp = a.sinfo;
@@ -762,10 +864,15 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                                         my_outer += 2ull * (len - in);
                                     }
                                 }
-                                for (uint32_t l = 0; l < nl; ++l) {
-                                    const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
-                                    const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
-                                    if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
+                                if (B > 1) {  // short block segments: parallel issue
+                                    sbld.add_batch(a, smem, L, sbeg, (uint32_t)slen, pol_stream, s_scr, lane);
+                                } else {
+                                    for (unsigned m = __ballot_sync(0xffffffffu, slen != 0); m; m &= m - 1) {
+                                        const int l = __ffs(m) - 1;
+                                        const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
+                                        const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
+                                        if (lane == 0) sbld.add(a, smem, L, b0, ln, pol_stream);
+                                    }
                                 }
                             }
                         }
@@ -810,11 +917,15 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                                         my_outer += 2ull * (len - in);
                                     }
                                 }
-                                const uint32_t nl = min(32u, mine - j0);
-                                for (uint32_t l = 0; l < nl; ++l) {
-                                    const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
-                                    const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
-                                    if (lane == 0 && ln) sbld.add(a, smem, L, b0, ln, pol_stream);
+                                if (B > 1) {  // short block segments: parallel issue
+                                    sbld.add_batch(a, smem, L, sbeg, (uint32_t)slen, pol_stream, s_scr, lane);
+                                } else {
+                                    for (unsigned m = __ballot_sync(0xffffffffu, slen != 0); m; m &= m - 1) {
+                                        const int l = __ffs(m) - 1;
+                                        const uint64_t b0 = __shfl_sync(0xffffffffu, sbeg, l);
+                                        const uint64_t ln = __shfl_sync(0xffffffffu, slen, l);
+                                        if (lane == 0) sbld.add(a, smem, L, b0, ln, pol_stream);
+                                    }
                                 }
                             }
                         }

@@ -1372,6 +1372,13 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
     a.f_policy = f_policy ? 1u : 0u;
+    const bool prof = std::getenv("VXB_PHASE_PROFILE") != nullptr;
+    DevBuf<unsigned long long> d_prof;
+    if (prof) {
+        d_prof.alloc(2ull * (steps + 1) * grid);
+        d_prof.zero(stream);
+        a.prof = d_prof.p;
+    }
 
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
@@ -1400,6 +1407,35 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         for (auto x : pw) exchange_wait_ms += x * 1e-6;
     }
     CK(cudaStreamSynchronize(stream));
+    if (prof) {  // per phase: mean / max over CTAs of delivery and update end (us)
+        std::vector<unsigned long long> pr(d_prof.n), pn(steps + 2);
+        CK(cudaMemcpy(pr.data(), d_prof.p, 8 * pr.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(pn.data(), d_phase_ns.p, 8 * pn.size(), cudaMemcpyDeviceToHost));
+        double sd = 0, md = 0, sf = 0, mf = 0, sp = 0;
+        uint32_t nd = 0;
+        for (uint32_t ph = 1; ph < steps; ++ph) {  // phases with both E and A
+            const double t0 = (double)pn[ph], len = (double)(pn[ph + 1] - pn[ph]);
+            double pmd = 0, pmf = 0;
+            for (int b = 0; b < grid; ++b) {
+                const double d = pr[2 * ((size_t)ph * grid + b)] ? pr[2 * ((size_t)ph * grid + b)] - t0 : 0;
+                const double f = pr[2 * ((size_t)ph * grid + b) + 1] - t0;
+                sd += d;
+                sf += f;
+                pmd = std::max(pmd, d);
+                pmf = std::max(pmf, f);
+                ++nd;
+            }
+            md += pmd;
+            mf += pmf;
+            sp += len;
+        }
+        const double np_ = std::max(1u, steps - 1);
+        if (nd)
+            std::fprintf(stderr,
+                         "vxb phase profile (us): phase %.1f | delivery end mean %.1f max %.1f | "
+                         "update end mean %.1f max %.1f\n",
+                         sp / np_ / 1e3, sd / nd / 1e3, md / np_ / 1e3, sf / nd / 1e3, mf / np_ / 1e3);
+    }
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
     device_ms += ms;

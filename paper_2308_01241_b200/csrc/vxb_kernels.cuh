@@ -173,6 +173,9 @@ struct StepArgs {
     uint32_t* work_ctr;
     uint32_t dyn;
     uint32_t f_policy;  // 1: neuron-state stream evict_first in L2
+    // phase profile (VXB_PHASE_PROFILE): per (phase, CTA) globaltimer of the
+    // end of this CTA's delivery and of its update, or null
+    unsigned long long* prof;
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -714,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     __shared__ int s_stop;
     __shared__ uint32_t s_hcnt[64];  // dynamic delivery: peer batch sizes of the phase
     __shared__ BatchScratch s_scr;   // producer warp: stage packing
+    __shared__ unsigned long long s_tD, s_tF;  // phase profile
 
     const ParamSet* psp = a.pset;
     const SegInfo* segp = a.sinfo;
@@ -732,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     if (threadIdx.x == 0) {
         s_nspk = 0;
         s_fwork = 0;
+        s_tD = s_tF = 0;
         for (int k = 0; k < kStages; ++k) {
             mbar_init(s_bar + k, 1);                          // full: producer + tx bytes
             mbar_init(s_bar + kStages + k, VXB_DWARPS > 1 ? VXB_DWARPS - 1 : 1);  // empty
@@ -970,6 +975,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
         }
 
 
+        if (a.prof && roleD && lane == 0) atomicMax(&s_tD, (unsigned long long)globaltimer());
+
         // ------------------------------------------------------------ F
         // 32-neuron chunks from the CTA's counter; loads of the next chunk
         // are in flight while the current one is updated
@@ -1156,8 +1163,13 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 i = inext;
             }
         }
+        if (a.prof && lane == 0) atomicMax(&s_tF, (unsigned long long)globaltimer());
         // flush the CTA's staged spikes with one log reservation
         __syncthreads();
+        if (a.prof && threadIdx.x == 0) {
+            a.prof[2 * ((size_t)ph * gridDim.x + blockIdx.x)] = s_tD;
+            a.prof[2 * ((size_t)ph * gridDim.x + blockIdx.x) + 1] = s_tF;
+        }
         const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
         if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
         __syncthreads();
@@ -1186,6 +1198,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
             s_nspk = 0;
             s_fwork = 0;
+            s_tD = s_tF = 0;
         }
         __syncthreads();
         if (s_stop) break;

@@ -1129,8 +1129,9 @@ void Engine::sort_rows() {
 }
 
 // L2-blocked delivery: when the pending buffer does not fit in L2, targets
-// are split into ranges whose pending slice does (48 MB: measured optimum on
-// config 3 between L2 misses and producer passes), rows are sorted by
+// are split into ranges whose pending slice does (64 MB: measured optimum on
+// config 3 between L2 misses and producer passes; 48 MB before the
+// warp-parallel producer), rows are sorted by
 // target and every CTA delivers block 0's segments of all its spikes, then
 // block 1's, ... so the live part of the pending buffer stays L2-resident
 // (VXB_BLOCK_NEURONS overrides the block size).
@@ -1138,7 +1139,7 @@ void Engine::build_blocks() {
     n_blocks = 1;
     dyn = true;  // dynamic chunks: +8% on config 2 even with one block
     const uint64_t pend_per = packed ? 16 : 32;
-    uint64_t bn = (48ull << 20) / pend_per;
+    uint64_t bn = (64ull << 20) / pend_per;
     if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
     if ((uint64_t)n <= bn || n_syn == 0) return;
     n_blocks = (uint32_t)((n + bn - 1) / bn);

@@ -64,9 +64,11 @@ def dti_cfg(workers=1, rate=10, dt_ms=1.0, total=20_000_000):
     byte model (strong scaling over GPUs)."""
     from paper_2308_01241_b200 import netgen
     path = ROOT / "build" / f"dti200_{total}.txt"
-    if not path.exists():
+    if not path.exists():  # every rank may get here: write privately, rename atomically
         path.parent.mkdir(parents=True, exist_ok=True)
-        netgen.write_connectome_file(netgen.dti_like_connectome(total_neurons=total), path)
+        tmp = path.with_suffix(f".{os.getpid()}.tmp")
+        netgen.write_connectome_file(netgen.dti_like_connectome(total_neurons=total), tmp)
+        os.replace(tmp, path)
     ampa, ou = K500_POINTS[rate]
     return {"seed": SEED, "dt_ms": dt_ms, "steps": 1000, "workers": workers,
             "connectome": {"kind": "file", "path": str(path)},

@@ -588,6 +588,11 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
 
     setup_exchange();
     build_blocks();
+    // dynamic chunks win on one device (+8% config 2, config 3 2.0 -> 1.5 s
+    // per bio-s) and with peers when there is one block (config 2 at 4 GPUs
+    // +4%); with peers and several L2 blocks the static deal measured better
+    // (config 3 at 4 GPUs: 0.34 vs 0.60 s per bio-s)
+    dyn = world == 1 || n_blocks == 1;
     if (const char* env = std::getenv("VXB_DYN")) dyn = std::atoi(env) != 0;
 
     // cooperative grid
@@ -1031,8 +1036,8 @@ void Engine::generate_csr(const vxb_netspec& spec) {
     CK(cudaStreamSynchronize(stream));
 }
 
-// Exchange state: receive region (one slot per peer: ids[2][n_h], counts,
-// flag), per-neuron destination masks, device control block.
+// Exchange state: receive region (one slot per peer: ids[kSlots][n_h],
+// counts[kSlots], flag), per-neuron destination masks, device control block.
 void Engine::setup_exchange() {
     std::memset(&h_ex, 0, sizeof h_ex);
     h_ex.rank = rank;
@@ -1047,7 +1052,7 @@ void Engine::setup_exchange() {
         for (uint32_t hh = 0; hh < world; ++hh) {
             h_ex.cap[hh] = src_base[hh + 1] - src_base[hh];
             rx_slot_off[hh] = off;
-            if (hh != rank) off += ((12ull * h_ex.cap[hh] + 15) & ~15ull) + 16;
+            if (hh != rank) off += ((4ull * kSlots * h_ex.cap[hh] + 15) & ~15ull) + 32;
         }
         d_rx.alloc(std::max<size_t>(16, off));
         d_rx.zero(stream);
@@ -1055,7 +1060,7 @@ void Engine::setup_exchange() {
             if (hh == rank) continue;
             unsigned char* b = d_rx.p + rx_slot_off[hh];
             h_ex.rx_ids[hh] = reinterpret_cast<uint32_t*>(b);
-            h_ex.rx_meta[hh] = reinterpret_cast<uint32_t*>(b + ((12ull * h_ex.cap[hh] + 15) & ~15ull));
+            h_ex.rx_meta[hh] = reinterpret_cast<uint32_t*>(b + ((4ull * kSlots * h_ex.cap[hh] + 15) & ~15ull));
         }
         peer_base.assign(world, nullptr);
     }
@@ -1137,7 +1142,7 @@ void Engine::sort_rows() {
 // (VXB_BLOCK_NEURONS overrides the block size).
 void Engine::build_blocks() {
     n_blocks = 1;
-    dyn = true;  // dynamic chunks: +8% on config 2 even with one block
+    dyn = false;
     const uint64_t pend_per = packed ? 16 : 32;
     uint64_t bn = (64ull << 20) / pend_per;
     if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
@@ -1804,11 +1809,11 @@ int vxb_connect_peers(vxb_engine* e, const void* handles, uint64_t stride) {
             // peer d's region: slots of every shard but d, in shard order
             size_t off = 0;
             for (uint32_t hh = 0; hh < g.rank; ++hh)
-                if (hh != d) off += ((12ull * g.h_ex.cap[hh] + 15) & ~15ull) + 16;
+                if (hh != d) off += ((4ull * kSlots * g.h_ex.cap[hh] + 15) & ~15ull) + 32;
             unsigned char* slot = static_cast<unsigned char*>(base) + off;
             g.h_ex.tx_ids[d] = reinterpret_cast<uint32_t*>(slot);
             g.h_ex.tx_meta[d] = reinterpret_cast<uint32_t*>(
-                slot + ((12ull * g.h_ex.cap[g.rank] + 15) & ~15ull));
+                slot + ((4ull * kSlots * g.h_ex.cap[g.rank] + 15) & ~15ull));
         }
         CK(cudaMemcpy(g.d_ex.p, &g.h_ex, sizeof g.h_ex, cudaMemcpyHostToDevice));
         return VXB_OK;

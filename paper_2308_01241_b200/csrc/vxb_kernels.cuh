@@ -84,13 +84,15 @@ struct Control {
     unsigned int spk_cursor;   // append cursor of the spike log
     unsigned long long err;    // min (step << 32 | local) of a divergence, ~0 = none
     unsigned long long flops_inner, flops_outer;
-    unsigned int pad[6];
+    unsigned int routed;       // CTAs that routed this phase's spikes (multi-GPU)
+    unsigned int pad[5];
 };
 
 // Device-side state of the per-step spike-id exchange between ranks (one
 // process per GPU).  Receive slots live in this rank's IPC-exported region,
 // send slots are this rank's slots inside the peers' regions (NVLink P2P).
 constexpr int kMaxShards = 64;  // dst masks are 64-bit (partition.hpp:35)
+constexpr uint32_t kSlots = 4;  // exchange batches in flight per (sender, receiver)
 struct Exchange {
     uint32_t rank, world;
     uint32_t cap_self;                    // ids per parity in my slots (= my neurons)
@@ -100,11 +102,13 @@ struct Exchange {
     unsigned long long timeout_ns;
     uint32_t src_base[kMaxShards + 1];    // global source index base per shard
     uint32_t cap[kMaxShards];             // neurons of shard h
-    // Batches are triple-buffered by step (slot = step % 3): a sender may run
-    // one phase ahead of a receiver still reading the batch of two steps ago.
-    uint32_t send_cnt[3][kMaxShards];     // ids queued per (slot, destination)
-    uint32_t* rx_ids[kMaxShards];         // [3 * cap[h]] from source shard h
-    uint32_t* rx_meta[kMaxShards];        // counts[3], flag (= step + 1)
+    // Batches are buffered by step (slot = step % kSlots).  A batch is
+    // published as soon as every CTA has routed its spikes (before the
+    // phase's delivery ends), so a sender can be up to two phases ahead of
+    // a receiver still reading the batch of step t - 1: four slots.
+    uint32_t send_cnt[4][kMaxShards];     // ids queued per (slot, destination)
+    uint32_t* rx_ids[kMaxShards];         // [kSlots * cap[h]] from source shard h
+    uint32_t* rx_meta[kMaxShards];        // counts[kSlots], flag (= step + 1)
     uint32_t* tx_ids[kMaxShards];         // my slot in peer d
     uint32_t* tx_meta[kMaxShards];
 };
@@ -641,16 +645,16 @@ __device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bo
 // Publish the batch of step t to every peer: counts, then the step flag
 // with system-scope release.  An empty batch still publishes its flag: it is
 // the reference's step barrier (engine.cpp:468-524).  Run by one thread after
-// every CTA's routing is complete (the grid barrier's last arriver).
+// every CTA's routing is complete (the last CTA through the routing count).
 __device__ __forceinline__ void exchange_publish(const StepArgs& a, uint32_t t) {
     Exchange* ex = a.ex;
-    const uint32_t slot = t % 3u, world = ex->world, me = ex->rank;
+    const uint32_t slot = t % kSlots, world = ex->world, me = ex->rank;
     __threadfence_system();
     for (uint32_t d = 0; d < world; ++d)
         if (d != me) ex->tx_meta[d][slot] = atomicExch(&ex->send_cnt[slot][d], 0u);
     __threadfence_system();
     for (uint32_t d = 0; d < world; ++d)
-        if (d != me) st_release_sys(ex->tx_meta[d] + 3, t + 1);
+        if (d != me) st_release_sys(ex->tx_meta[d] + kSlots, t + 1);
 }
 
 // Wait for peer h's batch of step tE (receiver side of the step barrier);
@@ -660,7 +664,7 @@ __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h,
     Exchange* ex = a.ex;
     const uint32_t* meta = ex->rx_meta[h];
     const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(meta + 3) < tE + 1) {
+    while (ld_acquire_sys(meta + kSlots) < tE + 1) {
         if (ex->timeout_ns && globaltimer() - t0 > ex->timeout_ns) {
             if (atomicCAS(&ex->timeout, 0u, h + 1) == 0u) ex->timeout_step = tE;
             return 0;
@@ -807,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             // once its step flag is set) into the stage ring with bulk copies;
             // the other delivery warps drain stages into the pending buffer
             // with red.add (L2 atomics).  full/empty mbarriers per stage.
-            const uint32_t tslot = tE % 3u;
+            const uint32_t tslot = tE % kSlots;
             uint64_t* full = s_bar;
             uint64_t* empty = s_bar + kStages;
             if (threadIdx.x < 32) {
@@ -1156,7 +1160,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                     }
                 }
                 if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
-                    if (exchange_route(a, i, overflow_route, tA % 3u)) __threadfence_system();
+                    if (exchange_route(a, i, overflow_route, tA % kSlots)) __threadfence_system();
                 cur = nxt;
                 ch = chn;
                 chn = chn2;
@@ -1179,8 +1183,18 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             bool sent = false;
             const uint32_t nr = (nst + 31u) & ~31u;
             for (uint32_t k = threadIdx.x; k < nr; k += blockDim.x)
-                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % 3u);
+                sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % kSlots);
             if (sent) __threadfence_system();
+            // the batch S(tA) is complete once every CTA has routed: the last
+            // CTA publishes it now, while the grid may still be delivering
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&ctl->routed, 1u) == gridDim.x - 1) {
+                    ctl->routed = 0;
+                    exchange_publish(a, tA);
+                }
+            }
         }
 
         if (threadIdx.x == 0 && wait_ns && a.phase_wait) atomicMax(a.phase_wait + ph, wait_ns);
@@ -1191,9 +1205,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
                 a.phase_ns[ph + 1] = globaltimer();
             },
-            [&] {
-                if (a.world > 1 && doA) exchange_publish(a, tA);
-            });
+            [] {});
         if (threadIdx.x == 0) {  // L2-coherent reads
             s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
             s_nspk = 0;

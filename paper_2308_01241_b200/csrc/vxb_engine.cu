@@ -1378,6 +1378,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
     a.f_policy = f_policy ? 1u : 0u;
+    {
+        const char* ep = std::getenv("VXB_EARLY_PUBLISH");
+        a.early_publish = ep ? (std::atoi(ep) != 0 ? 1u : 0u) : 0u;  // measured slower (config 2 at 4 GPUs 4.23e11 vs 4.72e11 events/s)
+    }
     const bool prof = std::getenv("VXB_PHASE_PROFILE") != nullptr;
     DevBuf<unsigned long long> d_prof;
     if (prof) {

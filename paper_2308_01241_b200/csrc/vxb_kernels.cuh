@@ -180,6 +180,7 @@ struct StepArgs {
     // phase profile (VXB_PHASE_PROFILE): per (phase, CTA) globaltimer of the
     // end of this CTA's delivery and of its update, or null
     unsigned long long* prof;
+    uint32_t early_publish;  // publish S(tA) once routed (else after the phase barrier)
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
 };
 
@@ -1187,12 +1188,14 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             if (sent) __threadfence_system();
             // the batch S(tA) is complete once every CTA has routed: the last
             // CTA publishes it now, while the grid may still be delivering
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                if (atomicAdd(&ctl->routed, 1u) == gridDim.x - 1) {
-                    ctl->routed = 0;
-                    exchange_publish(a, tA);
+            if (a.early_publish) {
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    if (atomicAdd(&ctl->routed, 1u) == gridDim.x - 1) {
+                        ctl->routed = 0;
+                        exchange_publish(a, tA);
+                    }
                 }
             }
         }
@@ -1205,7 +1208,9 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
                 a.phase_ns[ph + 1] = globaltimer();
             },
-            [] {});
+            [&] {
+                if (a.world > 1 && doA && !a.early_publish) exchange_publish(a, tA);
+            });
         if (threadIdx.x == 0) {  // L2-coherent reads
             s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
             s_nspk = 0;

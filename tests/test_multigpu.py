@@ -72,14 +72,18 @@ def _gpus():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("world", [2, 4])
-def test_nvlink_exchange_matches_reference(world):
+@pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (2, {"VXB_EARLY_PUBLISH": "1"}),
+                                       (2, {"VXB_DYN": "0"})])
+def test_nvlink_exchange_matches_reference(world, env):
+    """Default schedule, plus the optional early batch publication (4-slot
+    ring) and the static delivery deal."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
            "--master-port", str(_free_port()), str(ROOT / "tests" / "dist_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={**os.environ, **env})
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert lines, out.stdout + out.stderr
     res = json.loads(lines[-1])

@@ -107,17 +107,25 @@ struct HostBuf {
     }
 };
 
-// Length of the prefix of finite, non-negative values (NaN fails both
-// compares).  Branch-free per 1024-value block so the common all-valid case
-// vectorises; only a block holding a bad value is rescanned.
-uint32_t valid_prefix(const float* v, uint32_t n) {
+// Copies the prefix of finite, non-negative values of v into dst and
+// returns its length (NaN fails both compares; -0.0 passes, as in the
+// reference).  Block-wise: each 1024-value block is checked branch-free and
+// then copied while it is still in cache, so the caller's buffer is read
+// from memory once.  dst == nullptr only validates.
+uint32_t copy_valid_prefix(float* dst, const float* v, uint32_t n) {
     for (uint32_t b = 0; b < n; b += 1024) {
         const uint32_t e = std::min(n, b + 1024);
         int bad = 0;
-        for (uint32_t i = b; i < e; ++i) bad |= !(v[i] >= 0.0f && v[i] <= 3.402823466e38f);
+        for (uint32_t i = b; i < e; ++i) {
+            const float x = v[i];
+            bad |= !((x >= 0.0f) & (x <= 3.402823466e38f));
+        }
+        uint32_t end = e;
         if (bad)
-            for (uint32_t i = b; i < e; ++i)
-                if (!(v[i] >= 0.0f && v[i] <= 3.402823466e38f)) return i;
+            for (end = b; end < e; ++end)
+                if (!(v[end] >= 0.0f && v[end] <= 3.402823466e38f)) break;
+        if (dst) std::memcpy(dst + b, v + b, 4ull * (end - b));
+        if (end < e) return end;
     }
     return n;
 }
@@ -225,7 +233,7 @@ struct Engine {
     size_t cond_total = 0;
     DevBuf<float> d_cstage;
     DevBuf<uint4> d_crec;
-    void stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t k);
+    uint32_t stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t n);
     void flush_conductances(bool sync);
 
     ~Engine() {
@@ -1617,8 +1625,9 @@ int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float
             throw ConfigError("conductance vector size does not match unit");
         // engine.cpp:839-843 writes values in order and throws at the first
         // invalid one, leaving the prefix written: stage the same prefix
-        const uint32_t k = valid_prefix(values, n);
-        if (k && g.local(g.unit_worker[unit])) g.stage_conductances(unit, receptor, values, k);
+        const uint32_t k = g.local(g.unit_worker[unit])
+                               ? g.stage_conductances(unit, receptor, values, n)
+                               : copy_valid_prefix(nullptr, values, n);
         if (k < n) throw ConfigError("conductance values must be finite and >= 0");
         return VXB_OK;
     } catch (const std::exception& x) {
@@ -1627,23 +1636,23 @@ int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float
     }
 }
 
-void Engine::stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t k) {
+uint32_t Engine::stage_conductances(uint32_t unit, int receptor, const float* values,
+                                    uint32_t n) {
     const uint32_t key = unit * 4 + (uint32_t)receptor;
     if (cond_slot.size() != 4ull * n_units) cond_slot.assign(4ull * n_units, -1);
-    if (cond_slot[key] >= 0) {  // overwrite the earlier staged values of this unit/receptor
-        uint4& r = cond_rec[cond_slot[key]];
-        std::memcpy(h_cstage.p + r.x, values, 4ull * k);
-        r.z = std::max(r.z, k);
-        return;
+    if (cond_slot[key] < 0) {  // new record, with room for a full unit
+        const uint32_t full = units[unit].neurons;
+        if (cond_total + full > 0xFFFFFFFFull) flush_conductances(true);
+        h_cstage.reserve(cond_total + full);
+        const uint32_t base = wbase[unit_worker[unit]] + unit_local_base[unit];
+        cond_slot[key] = (int32_t)cond_rec.size();
+        cond_rec.push_back(make_uint4((uint32_t)cond_total, 4 * base + (uint32_t)receptor, 0u, key));
+        cond_total += full;
     }
-    cond_slot[key] = (int32_t)cond_rec.size();
-    const uint32_t full = units[unit].neurons;  // room for a later full overwrite
-    if (cond_total + full > 0xFFFFFFFFull) flush_conductances(true);
-    h_cstage.reserve(cond_total + full);
-    std::memcpy(h_cstage.p + cond_total, values, 4ull * k);
-    const uint32_t base = wbase[unit_worker[unit]] + unit_local_base[unit];
-    cond_rec.push_back(make_uint4((uint32_t)cond_total, 4 * base + (uint32_t)receptor, k, key));
-    cond_total += full;
+    uint4& r = cond_rec[cond_slot[key]];  // a later set overwrites the earlier values
+    const uint32_t k = copy_valid_prefix(h_cstage.p + r.x, values, n);
+    r.z = std::max(r.z, k);
+    return k;
 }
 
 void Engine::flush_conductances(bool sync) {

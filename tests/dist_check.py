@@ -88,5 +88,49 @@ def main():
     dist.destroy_process_group()
 
 
+def main_full():
+    """Full-size property (BASELINE config 2 weak-scaling network, 1M neurons
+    per GPU, K = 1000): the N-GPU run with the NVLink exchange equals the same
+    N-worker network hosted on one GPU (raster, rates, state)."""
+    import bench
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    steps = 40
+    cfg = bench.workload_cfg(voxels=100 * world, workers=world)
+    cfg["partition"] = {"method": "sequential"}
+    net = netgen.build_network(cfg)
+    opt = SimOptions(steps=steps, record_raster=True, record_timings=False, device=local)
+    sim = netgen.DistributedSimInstance(net, opt, rank, world)
+    r = sim.advance(steps)
+    mine = {"raster": np.stack([r.raster["step"].astype(np.int64), r.raster["gid"].astype(np.int64)], 1),
+            "rates": r.rates.counts, "snap": sim.membrane_snapshot(rank), "events": r.events}
+    sim.close()
+    out = [None] * world
+    dist.all_gather_object(out, mine)
+    if rank == 0:
+        raster = np.concatenate([o["raster"] for o in out])
+        raster = raster[np.lexsort((raster[:, 1], raster[:, 0]))]
+        with netgen.GeneratedSimInstance(net, SimOptions(steps=steps, record_raster=True,
+                                                         record_timings=False, device=local)) as one:
+            q = one.advance(steps)
+            snaps = [one.membrane_snapshot(w) for w in range(world)]
+        qr = np.stack([q.raster["step"].astype(np.int64), q.raster["gid"].astype(np.int64)], 1)
+        qr = qr[np.lexsort((qr[:, 1], qr[:, 0]))]
+        res = {"world": world, "mode": "full", "spikes": int(raster.shape[0]),
+               "events": int(sum(o["events"] for o in out)), "one_gpu_events": int(q.events),
+               "raster_equal": bool(raster.shape == qr.shape and np.array_equal(raster, qr)),
+               "rates_equal": bool(np.array_equal(sum(o["rates"] for o in out), q.rates.counts)),
+               "snapshots_equal": all(np.array_equal(out[w]["snap"], snaps[w]) for w in range(world))}
+        res["pass"] = all(v for k, v in res.items() if k.endswith("_equal")) and res["spikes"] > 0
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--full":
+        main_full()
+    else:
+        main()

@@ -89,3 +89,19 @@ def test_nvlink_exchange_matches_reference(world, env):
     res = json.loads(lines[-1])
     assert res["pass"], res
     assert res["gating_outer"] > 0  # spikes really crossed GPUs
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_fullsize_config2_two_gpus_equal_one_gpu():
+    """BASELINE config 2 at full size per GPU (2 x 1M neurons, 2e9 synapses):
+    the 2-GPU NVLink run equals the same 2-worker network on one GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=2", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), str(ROOT / "tests" / "dist_check.py"), "--full"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert lines, out.stdout + out.stderr
+    res = json.loads(lines[-1])
+    assert res["pass"], res
+    assert res["events"] == res["one_gpu_events"]

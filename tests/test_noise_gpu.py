@@ -30,3 +30,25 @@ def test_ou_noise_float_samples_bit_exact():
     # the doubles may differ in the last ulp where CUDA and glibc log/cos round differently
     ulps = np.abs(dev.view(np.int64) - host.view(np.int64))
     assert ulps.max() <= 4
+
+
+def test_ou_noise_float_bit_exact_1e9_samples(tmp_path):
+    """1e9 (gid, step) samples — one biological second of config 2 — device
+    xi against glibc on the host cores (tests/native/noise_fliprate.cu):
+    every float sample identical.  The doubles differ in ~15 % of samples
+    (CUDA vs glibc log/cos last ulp); the float rounding absorbs it."""
+    import json
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "noise_fliprate"
+    subprocess.run(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "--fmad=false",
+                    "-Xcompiler", "-fopenmp,-ffp-contract=off",
+                    "-I", str(root / "paper_2308_01241_b200" / "csrc"),
+                    str(root / "tests" / "native" / "noise_fliprate.cu"), "-o", str(exe)],
+                   check=True, timeout=300)
+    out = subprocess.run([str(exe), "1000000", "1000", "0"], capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    res = json.loads(out.strip().splitlines()[-1])
+    assert res["samples"] == 10**9
+    assert res["float_mismatch"] == 0, res

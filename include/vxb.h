@@ -335,10 +335,15 @@ int vxb_generate_worker_table(const vxb_netspec* spec, int device, uint16_t work
 uint64_t vxb_fnv1a(const void* data, uint64_t n, uint64_t h);
 
 /* ---- diagnostics --------------------------------------------------------- */
-/* Device evaluation of stream_normal(base[i], k[i]) (rng.hpp:63-67) exactly as
- * the step kernel computes it, for noise-parity checks against the host. */
+/* Device evaluation of stream_normal(base[i], k[i]) (rng.hpp:63-67) with
+ * CUDA's log/cos (the fast path), for noise-parity checks against the host. */
 int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
                             double* out);
+/* The float OU noise sample (float)stream_normal(base[i], k[i]) exactly as the
+ * step kernel computes it (engine.cpp:551-553): fast path, with correctly
+ * rounded log/cos for samples near a float rounding boundary. */
+int vxb_debug_stream_xi(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
+                        float* out);
 
 /* ---- one-call convenience (run_simulation, engine.hpp:92-93) ------------- */
 /* Creates, advances `steps` and returns the engine holding the results. */

@@ -148,7 +148,8 @@ EXPORTS = [
     "vxb_result_timings", "vxb_result_device_ms", "vxb_result_h2d_bytes",
     "vxb_result_d2h_bytes", "vxb_result_launches", "vxb_set_conductances",
     "vxb_membrane_snapshot", "vxb_worker_neurons", "vxb_workers", "vxb_units",
-    "vxb_probes", "vxb_run_simulation", "vxb_debug_stream_normal", "vxb_create_generated",
+    "vxb_probes", "vxb_run_simulation", "vxb_debug_stream_normal", "vxb_debug_stream_xi",
+    "vxb_create_generated",
     "vxb_generate_worker_table", "vxb_create_generated_rank", "vxb_mask_bytes",
     "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
     "vxb_result_exchange_wait_ms", "vxb_fnv1a",
@@ -188,6 +189,7 @@ def _declare(lib):
         "vxb_units": (C.c_uint32, [P]),
         "vxb_probes": (C.c_uint32, [P]),
         "vxb_debug_stream_normal": (C.c_int, [C.c_int, P, P, C.c_uint64, P]),
+        "vxb_debug_stream_xi": (C.c_int, [C.c_int, P, P, C.c_uint64, P]),
         "vxb_create_generated": (C.c_int, [P, C.POINTER(Options), C.POINTER(P)]),
         "vxb_generate_worker_table": (C.c_int, [P, C.c_int, C.c_uint16, P, C.c_uint32, P,
                                                 C.c_uint64, P]),

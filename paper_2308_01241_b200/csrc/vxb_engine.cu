@@ -1919,6 +1919,27 @@ int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k,
     }
 }
 
+int vxb_debug_stream_xi(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
+                        float* out) {
+    try {
+        CK(cudaSetDevice(device));
+        DevBuf<uint64_t> b, kk;
+        DevBuf<float> o;
+        b.alloc(n);
+        kk.alloc(n);
+        o.alloc(n);
+        CK(cudaMemcpy(b.p, base, 8 * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(kk.p, k, 8 * n, cudaMemcpyHostToDevice));
+        debug_xi_kernel<<<1184, 256>>>(b.p, kk.p, n, o.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, o.p, 4 * n, cudaMemcpyDeviceToHost));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return fail_code(x);
+    }
+}
+
 int vxb_run_simulation(const vxb_network* net, const vxb_options* opt, uint32_t steps,
                        vxb_engine** out) {
     int rc = vxb_create(net, opt, out);

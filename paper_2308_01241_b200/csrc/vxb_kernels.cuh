@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         float xi = 0.0f;
                         if (P.sigma_pos) {
                             const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
-                            xi = __double2float_rn(stream_normal(mix_key(a.ou_root, gid), tE));
+                            xi = stream_xi(mix_key(a.ou_root, gid), tE);
                         }
                         iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
                         if (!doA) stp(a.i_syn + i, isyn, pol_f);
@@ -1342,6 +1342,14 @@ __global__ void debug_normal_kernel(const uint64_t* __restrict__ base,
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
         out[i] = stream_normal(base[i], k[i]);
+}
+
+__global__ void debug_xi_kernel(const uint64_t* __restrict__ base,
+                                const uint64_t* __restrict__ k, uint64_t n,
+                                float* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = stream_xi(base[i], k[i]);
 }
 
 // Staged set_conductances (engine.cpp:829-844) applied in one launch before

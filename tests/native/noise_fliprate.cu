@@ -4,12 +4,14 @@
 // kernel uses (paper_2308_01241_b200/csrc/vxb_device.cuh) and once on the
 // host with glibc log/cos exactly as the reference evaluates it
 // (rng.hpp:58-67, engine.cpp:551-553; compiled -ffp-contract=off).
-// Prints one JSON line: samples, float mismatches, double mismatches.
+// Prints one JSON line: samples, float mismatches and the first (gid, t) of
+// them.  Argument 4 = 1 checks the fast path alone (no near-boundary
+// correctly rounded recomputation).
 //
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a --fmad=false \
 //        -Xcompiler -fopenmp,-ffp-contract=off -I paper_2308_01241_b200/csrc \
 //        tests/native/noise_fliprate.cu -o noise_fliprate
-//   ./noise_fliprate G T t0
+//   ./noise_fliprate G T t0 [fast_only]
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -24,12 +26,13 @@
 using namespace vxb;
 
 __global__ void xi_kernel(uint64_t root, uint64_t g0, uint32_t G, uint32_t T, uint64_t t0,
-                          double* out) {
+                          float* out, int fast_only) {
     const uint64_t n = (uint64_t)G * T;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t gid = g0 + i / T, t = t0 + i % T;
-        out[i] = stream_normal(mix_key(root, gid), t);
+        out[i] = fast_only ? __double2float_rn(stream_normal(mix_key(root, gid), t))
+                           : stream_xi(mix_key(root, gid), t);
     }
 }
 
@@ -46,26 +49,35 @@ int main(int argc, char** argv) {
     const uint64_t seed = 2;
     const uint64_t root = mix_key(seed, 1);  // rngstream::ou_noise
     const uint32_t gchunk = std::max<uint32_t>(1, (uint32_t)(200000000ull / T));
-    double* d = nullptr;
-    if (cudaMalloc(&d, 8ull * gchunk * T) != cudaSuccess) return 2;
-    std::vector<double> h((size_t)gchunk * T);
-    unsigned long long fl = 0, db = 0, total = 0;
+    const int fast_only = argc > 4 ? std::atoi(argv[4]) : 0;
+    float* d = nullptr;
+    if (cudaMalloc(&d, 4ull * gchunk * T) != cudaSuccess) return 2;
+    std::vector<float> h((size_t)gchunk * T);
+    unsigned long long fl = 0, total = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> bad;
     for (uint32_t g0 = 0; g0 < G; g0 += gchunk) {
         const uint32_t gn = std::min(gchunk, G - g0);
-        xi_kernel<<<148 * 16, 256>>>(root, g0, gn, T, t0, d);
+        xi_kernel<<<148 * 16, 256>>>(root, g0, gn, T, t0, d, fast_only);
         if (cudaDeviceSynchronize() != cudaSuccess) return 3;
-        cudaMemcpy(h.data(), d, 8ull * gn * T, cudaMemcpyDeviceToHost);
-#pragma omp parallel for reduction(+ : fl, db) schedule(static)
+        cudaMemcpy(h.data(), d, 4ull * gn * T, cudaMemcpyDeviceToHost);
+#pragma omp parallel for reduction(+ : fl) schedule(static)
         for (long long i = 0; i < (long long)gn * T; ++i) {
             const uint64_t gid = g0 + (uint64_t)i / T, t = t0 + (uint64_t)i % T;
-            const double x = host_normal(mix_key(root, gid), t);
-            db += x != h[i];
-            fl += (float)x != (float)h[i];
+            const float x = (float)host_normal(mix_key(root, gid), t);
+            if (x != h[i]) {
+                ++fl;
+#pragma omp critical
+                if (bad.size() < 64) bad.emplace_back(gid, t);
+            }
         }
         total += (unsigned long long)gn * T;
     }
-    std::printf("{\"samples\": %llu, \"float_mismatch\": %llu, \"double_mismatch\": %llu}\n",
-                total, fl, db);
+    std::printf("{\"samples\": %llu, \"float_mismatch\": %llu, \"fast_only\": %d, \"mismatches\": [",
+                total, fl, fast_only);
+    for (size_t i = 0; i < bad.size(); ++i)
+        std::printf("%s[%llu, %llu]", i ? ", " : "", (unsigned long long)bad[i].first,
+                    (unsigned long long)bad[i].second);
+    std::printf("]}\n");
     cudaFree(d);
     return 0;
 }

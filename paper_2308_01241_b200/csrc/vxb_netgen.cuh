@@ -89,6 +89,19 @@ __device__ __forceinline__ int32_t quantize(double w) {
     return (int32_t)llround(__dmul_rn(w, 65536.0));
 }
 
+// quantize(mean + spread * stream_normal(kw, idx)) (netgen.cpp:118-183): the
+// fast normal unless w * 2^16 lies within 256 ulps of an llround half-way
+// point, where CUDA's last-ulp log/cos could flip the integer; then the
+// correctly rounded normal (vxb_device.cuh) decides, as glibc does.
+__device__ __forceinline__ int32_t weight_q(double mean, double spread, uint64_t kw,
+                                            uint64_t idx) {
+    const double w = __dadd_rn(mean, __dmul_rn(spread, stream_normal(kw, idx)));
+    const double x = __dmul_rn(w < 0 ? 0.0 : w, 65536.0);
+    const double fr = __dsub_rn(x, floor(x));  // exact
+    if (fabs(__dsub_rn(fr, 0.5)) > __dmul_rn(0x1p-44, x)) return (int32_t)llround(x);
+    return quantize(__dadd_rn(mean, __dmul_rn(spread, stream_normal_cr(kw, idx))));
+}
+
 struct Drawn {
     uint32_t src_unit;
     uint64_t src_gid;
@@ -148,11 +161,9 @@ __device__ __forceinline__ bool draw_synapse(const GenDev& G, const GenVoxel& V,
             want_slow = !want_fast;
         }
         if (want_fast)
-            d.wf = quantize(__dadd_rn(SU.w_mean[rf],
-                                      __dmul_rn(SU.w_spread[rf], stream_normal(kw, (uint64_t)k * 3))));
+            d.wf = weight_q(SU.w_mean[rf], SU.w_spread[rf], kw, (uint64_t)k * 3);
         if (want_slow)
-            d.ws = quantize(__dadd_rn(SU.w_mean[rs], __dmul_rn(SU.w_spread[rs],
-                                                               stream_normal(kw, (uint64_t)k * 3 + 1))));
+            d.ws = weight_q(SU.w_mean[rs], SU.w_spread[rs], kw, (uint64_t)k * 3 + 1);
     }
     return true;
 }

@@ -74,3 +74,25 @@ def test_ou_noise_near_boundary_samples_match_glibc():
     host = np.array([R.ref_stream_normal(int(b), int(k)) for b, k in zip(base, steps)]).astype(np.float32)
     assert (fast.astype(np.float32) != host).all()  # the fast path really flips here
     assert np.array_equal(xi, host)
+
+
+def test_correctly_rounded_normal_agrees_with_glibc(tmp_path):
+    """The double-double stream_normal_cr (used near rounding boundaries for
+    the OU noise and the Q16 synapse weights) is correctly rounded: it
+    differs from glibc only where glibc itself is not (log ~0.08 %, cos
+    ~0.13 % of inputs, checked against mpmath), against ~15 % for CUDA's
+    fast log/cos (tests/native/normal_cr_check.cu, 2e7 samples)."""
+    import json
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "normal_cr_check"
+    subprocess.run(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "--fmad=false",
+                    "-Xcompiler", "-fopenmp,-ffp-contract=off",
+                    "-I", str(root / "paper_2308_01241_b200" / "csrc"),
+                    str(root / "tests" / "native" / "normal_cr_check.cu"), "-o", str(exe)],
+                   check=True, timeout=300)
+    res = json.loads(subprocess.run([str(exe), "20000000"], capture_output=True, text=True,
+                                    timeout=600, check=True).stdout.strip().splitlines()[-1])
+    assert res["cr_double_mismatch"] < 0.004 * res["samples"], res
+    assert res["fast_double_mismatch"] > 0.1 * res["samples"], res

@@ -395,12 +395,12 @@ def run_b200(args):
         try:
             ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
             ref.step(20)
-            e, s, k = ref.step(args.cpu_steps)
+            e, s, k = ref.step(args.cpu_sample_steps)
             line["cpu_baseline"] = {
                 "value": e / s, "unit": "events/s", "cores": ref.threads, "kind": "reference",
-                "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_steps} "
+                "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_sample_steps} "
                           f"steps, {ref.workers} workers (threads), "
-                          f"{k / (ref.neurons * args.cpu_steps * 1e-3):.1f} Hz, "
+                          f"{k / (ref.neurons * args.cpu_sample_steps * 1e-3):.1f} Hz, "
                           f"{s:.1f} s of CPU time"}
         except Exception as e:  # the checker is optional on the GPU arm
             line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
@@ -418,7 +418,10 @@ def main():
     ap.add_argument("--dt", type=float, default=1.0)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--cpu-voxels", type=int, default=12)
-    ap.add_argument("--cpu-steps", type=int, default=4000)
+    ap.add_argument("--cpu-steps", type=int, default=4000,
+                    help="--impl reference: simulated steps per bench step")
+    ap.add_argument("--cpu-sample-steps", type=int, default=12000,
+                    help="cpu_baseline of the B200 arm: simulated steps of the timed sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4"])
     ap.add_argument("--rate", type=int, default=10, choices=[7, 10, 15, 30],

@@ -389,6 +389,11 @@ def run_b200(args):
                      "alg_bytes_per_launch": alg_bytes / max(1, launches_per * args.steps),
                      "exchange": "4 B per (spike, destination GPU) over NVLink" if ws > 1 else None,
                      "model": "98 B/neuron-step + 12 B/event + 20 B/delivered spike"},
+        # the resource that bounds delivery: scattered L2 red.add, measured
+        # ceiling 1.93e11/s per GPU (profiles/r01_delivery_ceiling.txt)
+        "roofline_atomic": {"bound": "l2_atomic", "achieved": value / ws, "peak": 1.93e11,
+                            "unit": "red.add/s per GPU", "frac": value / ws / 1.93e11,
+                            "peak_kind": "measured (tools/microbench_delivery.cu)"},
         "clocks": clk.summary(),
     }
     if not args.no_cpu and args.workload == "config2":
@@ -401,7 +406,7 @@ def run_b200(args):
                 "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_sample_steps} "
                           f"steps, {ref.workers} workers (threads), "
                           f"{k / (ref.neurons * args.cpu_sample_steps * 1e-3):.1f} Hz, "
-                          f"{s:.1f} s of CPU time"}
+                          f"{s:.1f} s wall on {ref.threads} threads"}
         except Exception as e:  # the checker is optional on the GPU arm
             line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}

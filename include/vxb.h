@@ -345,6 +345,39 @@ int vxb_debug_stream_normal(int device, const uint64_t* base, const uint64_t* k,
 int vxb_debug_stream_xi(int device, const uint64_t* base, const uint64_t* k, uint64_t n,
                         float* out);
 
+/* ---- BOLD-proxy readout (hemo.hpp, assim.cpp:51-71) ------------------------ */
+typedef struct vxb_hemo_params { /* HemoParams (hemo.hpp:10-23) */
+    double kappa, gamma, tau, alpha, e0, v0;
+} vxb_hemo_params;
+typedef struct vxb_hemo_state { /* HemoState (hemo.hpp:25-30); rest = {0, 1, 1, 1} */
+    double s, f, v, q;
+} vxb_hemo_state;
+
+/* Enable the device BOLD readout (replaces the assimilation caller's
+ * window_bold over RunResult::rates, assim.cpp:51-71 / 91-107): every
+ * advance() then drives one Balloon-Windkessel model per voxel with
+ * z = voxel_count / (voxel neurons * dt_s) / baseline_hz per step
+ * (step_hemodynamics, hemo.cpp:19-41) and samples bold_signal
+ * (hemo.cpp:43-47) every `sample_every` steps of the advance, as
+ * bold_from_drive does (hemo.cpp:49-62).  `init` (n_voxels states, NULL = rest)
+ * seeds the per-voxel state, which then carries across advances.  Errors:
+ * HemoParams::validate / baseline_hz > 0 / sample_every >= 1 -> VXB_ECONFIG;
+ * a diverged state makes advance() return VXB_ESIM with the reference's
+ * message, the simulation itself staying usable.  One device only. */
+int vxb_set_hemodynamics(vxb_engine* e, const vxb_hemo_params* p, double baseline_hz,
+                         uint32_t sample_every, const vxb_hemo_state* init);
+/* Current per-voxel states (cap >= n_voxels). */
+int vxb_hemo_get_state(const vxb_engine* e, vxb_hemo_state* out, uint32_t cap);
+/* BOLD samples of the last advance: [steps / sample_every][n_voxels]. */
+uint64_t vxb_result_bold_size(const vxb_engine* e);
+int vxb_result_bold(const vxb_engine* e, double* out, uint64_t cap);
+/* Diagnostics: bold_from_drive (hemo.cpp:49-62) on the device for n_series
+ * drive series z[series][steps]; state[n_series] in/out; out[series][steps /
+ * sample_every]. */
+int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double* z,
+                              uint32_t steps, uint32_t n_series, double dt_s,
+                              uint32_t sample_every, vxb_hemo_state* state, double* out);
+
 /* ---- one-call convenience (run_simulation, engine.hpp:92-93) ------------- */
 /* Creates, advances `steps` and returns the engine holding the results. */
 int vxb_run_simulation(const vxb_network* net, const vxb_options* opt,

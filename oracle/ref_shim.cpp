@@ -14,6 +14,7 @@
 #include "voxsim/config.hpp"
 #include "voxsim/connectome.hpp"
 #include "voxsim/engine.hpp"
+#include "voxsim/hemo.hpp"
 #include "voxsim/layout.hpp"
 #include "voxsim/model.hpp"
 #include "voxsim/netgen.hpp"
@@ -403,6 +404,61 @@ float ref_ou_kernel(float i, float dt, float mean, float sigma, float tau, float
 // OU noise sample as the engine consumes it (engine.cpp:551-553).
 float ref_ou_xi(uint64_t seed, uint64_t gid, uint64_t step) {
     return static_cast<float>(stream_normal(mix_key(seed, rngstream::ou_noise, gid), step));
+}
+
+// ---- hemodynamics (hemo.cpp) ------------------------------------------------
+// p = {kappa, gamma, tau, alpha, e0, v0}; st = {s, f, v, q} in/out.
+static HemoParams hemo_params(const double* p) {
+    HemoParams h;
+    h.kappa = p[0];
+    h.gamma = p[1];
+    h.tau = p[2];
+    h.alpha = p[3];
+    h.e0 = p[4];
+    h.v0 = p[5];
+    return h;
+}
+// bold_from_drive (hemo.cpp:49-62) for one drive series.
+int ref_bold_from_drive(const double* p, const double* z, uint32_t steps, double dt_s,
+                        uint32_t sample_every, double* st, double* out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        HemoState h{st[0], st[1], st[2], st[3]};
+        std::vector<double> zz(z, z + steps);
+        std::vector<double> b = bold_from_drive(zz, dt_s, sample_every, hemo_params(p), &h);
+        std::copy(b.begin(), b.end(), out);
+        st[0] = h.s;
+        st[1] = h.f;
+        st[2] = h.v;
+        st[3] = h.q;
+    });
+}
+// window_bold (assim.cpp:51-71; it lives in an anonymous namespace there, so
+// the drive is restated here around the reference's own step_hemodynamics /
+// bold_signal): counts[unit][steps], unit_voxel[units], vox_n[voxels];
+// states[voxels][4] in/out; out[steps / sample_every][voxels].
+int ref_window_bold(const double* p, const uint32_t* counts, uint32_t n_units, uint32_t steps,
+                    const uint32_t* unit_voxel, uint32_t n_voxels, const uint64_t* vox_n,
+                    double dt_s, double baseline_hz, uint32_t sample_every, double* states,
+                    double* out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        const HemoParams hp = hemo_params(p);
+        hp.validate();
+        for (uint32_t t = 0; t < steps; ++t) {
+            std::vector<uint32_t> vc(n_voxels, 0);  // RateSeries::voxel_counts (stats.cpp:193-201)
+            for (uint32_t u = 0; u < n_units; ++u) vc[unit_voxel[u]] += counts[(size_t)u * steps + t];
+            for (uint32_t v = 0; v < n_voxels; ++v) {
+                double hz = vox_n[v] > 0 ? vc[v] / (static_cast<double>(vox_n[v]) * dt_s) : 0.0;
+                HemoState h{states[4 * v], states[4 * v + 1], states[4 * v + 2], states[4 * v + 3]};
+                step_hemodynamics(h, hz / baseline_hz, dt_s, hp);
+                states[4 * v] = h.s;
+                states[4 * v + 1] = h.f;
+                states[4 * v + 2] = h.v;
+                states[4 * v + 3] = h.q;
+                if ((t + 1) % sample_every == 0)
+                    out[(size_t)((t + 1) / sample_every - 1) * n_voxels + v] = bold_signal(h, hp);
+            }
+        }
+    });
 }
 
 } // extern "C"

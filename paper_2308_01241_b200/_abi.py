@@ -135,6 +135,10 @@ class Options(C.Structure):
     ]
 
 
+class HemoParams(C.Structure):  # vxb_hemo_params == HemoParams (hemo.hpp:10-23)
+    _fields_ = [(n, C.c_double) for n in ("kappa", "gamma", "tau", "alpha", "e0", "v0")]
+
+
 class Flops(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in
                 ("membrane", "gating_inner", "gating_outer", "gating_decay", "current")]
@@ -152,7 +156,8 @@ EXPORTS = [
     "vxb_create_generated",
     "vxb_generate_worker_table", "vxb_create_generated_rank", "vxb_mask_bytes",
     "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
-    "vxb_result_exchange_wait_ms", "vxb_fnv1a",
+    "vxb_result_exchange_wait_ms", "vxb_fnv1a", "vxb_set_hemodynamics", "vxb_hemo_get_state",
+    "vxb_result_bold_size", "vxb_result_bold", "vxb_debug_bold_from_drive",
 ]
 
 _lib = None
@@ -202,6 +207,12 @@ def _declare(lib):
         "vxb_connect_peers": (C.c_int, [P, P, C.c_uint64]),
         "vxb_run_simulation": (C.c_int, [C.POINTER(Network), C.POINTER(Options), C.c_uint32,
                                          C.POINTER(P)]),
+        "vxb_set_hemodynamics": (C.c_int, [P, C.POINTER(HemoParams), C.c_double, C.c_uint32, P]),
+        "vxb_hemo_get_state": (C.c_int, [P, P, C.c_uint32]),
+        "vxb_result_bold_size": (C.c_uint64, [P]),
+        "vxb_result_bold": (C.c_int, [P, P, C.c_uint64]),
+        "vxb_debug_bold_from_drive": (C.c_int, [C.c_int, C.POINTER(HemoParams), P, C.c_uint32,
+                                                C.c_uint32, C.c_double, C.c_uint32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

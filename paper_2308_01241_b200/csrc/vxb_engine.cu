@@ -32,6 +32,7 @@
 #include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "vxb.h"
+#include "vxb_hemo.cuh"
 #include "vxb_kernels.cuh"
 #include "vxb_netgen.cuh"
 
@@ -44,6 +45,10 @@ struct ConfigError : std::runtime_error {
 };
 struct SimError : std::runtime_error {
     using std::runtime_error::runtime_error;
+};
+// hemo.cpp:37-40: raised by the BOLD readout; the simulation itself stays usable
+struct HemoError : SimError {
+    using SimError::SimError;
 };
 
 #define CK(x)                                                                          \
@@ -235,6 +240,21 @@ struct Engine {
     DevBuf<uint4> d_crec;
     uint32_t stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t n);
     void flush_conductances(bool sync);
+
+    // BOLD-proxy readout on the device (vxb_hemo.cuh), enabled by
+    // vxb_set_hemodynamics: per-voxel Balloon-Windkessel state carried across
+    // advances, BOLD samples of the last advance [sample][voxel]
+    bool hemo_on = false;
+    HemoParamsDev hemo_p{};
+    double hemo_baseline = 1.0;
+    uint32_t hemo_every = 1;
+    DevBuf<HemoStateDev> d_hemo;
+    DevBuf<uint32_t> d_vox_off, d_vox_units;
+    DevBuf<double> d_vox_n, d_bold;
+    DevBuf<unsigned long long> d_hemo_err;
+    std::vector<double> bold;
+    void set_hemodynamics(const vxb_hemo_params& p, double baseline_hz, uint32_t sample_every,
+                          const vxb_hemo_state* init);
 
     ~Engine() {
         for (void* p : peer_base)
@@ -1165,6 +1185,61 @@ void Engine::build_blocks() {
     CK(cudaStreamSynchronize(stream));
 }
 
+// HemoParams::validate (hemo.cpp:8-17), validate_assim's baseline check
+// (assim.cpp:47) and bold_from_drive's sampling check (hemo.cpp:52-53).
+void validate_hemo(const vxb_hemo_params& p, double baseline_hz, uint32_t sample_every) {
+    if (!(p.tau > 0)) throw ConfigError("hemodynamics: tau must be > 0");
+    if (!(p.alpha > 0) || p.alpha > 1) throw ConfigError("hemodynamics: alpha must be in (0, 1]");
+    if (!(p.e0 > 0) || p.e0 >= 1) throw ConfigError("hemodynamics: E0 must be in (0, 1)");
+    if (!(p.v0 > 0)) throw ConfigError("hemodynamics: V0 must be > 0");
+    if (p.kappa < 0 || p.gamma < 0) throw ConfigError("hemodynamics: decay rates must be >= 0");
+    if (!(baseline_hz > 0)) throw ConfigError("baseline_hz must be > 0");
+    if (sample_every == 0) throw ConfigError("hemodynamics: sample_every must be >= 1");
+}
+
+void Engine::set_hemodynamics(const vxb_hemo_params& p, double baseline_hz,
+                              uint32_t sample_every, const vxb_hemo_state* init) {
+    validate_hemo(p, baseline_hz, sample_every);
+    if (world > 1)
+        throw ConfigError("the device BOLD readout needs every unit on this device (one GPU)");
+    CK(cudaSetDevice(device));
+    // voxel -> units CSR and voxel sizes (voxel_sizes, assim.cpp:319)
+    std::vector<uint32_t> off(n_voxels + 1, 0), vu(n_units);
+    std::vector<double> vn(n_voxels, 0.0);
+    std::vector<uint64_t> vn64(n_voxels, 0);
+    for (uint32_t u = 0; u < n_units; ++u) {
+        ++off[units[u].voxel + 1];
+        vn64[units[u].voxel] += units[u].neurons;
+    }
+    for (uint32_t v = 0; v < n_voxels; ++v) {
+        off[v + 1] += off[v];
+        vn[v] = static_cast<double>(vn64[v]);
+    }
+    std::vector<uint32_t> cur(off.begin(), off.end() - 1);
+    for (uint32_t u = 0; u < n_units; ++u) vu[cur[units[u].voxel]++] = u;
+    std::vector<HemoStateDev> st(n_voxels, HemoStateDev{0.0, 1.0, 1.0, 1.0});  // hemo.hpp:25-30
+    if (init)
+        for (uint32_t v = 0; v < n_voxels; ++v) st[v] = {init[v].s, init[v].f, init[v].v, init[v].q};
+    d_vox_off.alloc(off.size());
+    d_vox_units.alloc(std::max<size_t>(1, vu.size()));
+    d_vox_n.alloc(std::max<size_t>(1, vn.size()));
+    d_hemo.alloc(std::max<size_t>(1, st.size()));
+    d_hemo_err.alloc(1);
+    CK(cudaMemcpyAsync(d_vox_off.p, off.data(), 4 * off.size(), cudaMemcpyHostToDevice, stream));
+    if (!vu.empty())
+        CK(cudaMemcpyAsync(d_vox_units.p, vu.data(), 4 * vu.size(), cudaMemcpyHostToDevice, stream));
+    if (!vn.empty()) {
+        CK(cudaMemcpyAsync(d_vox_n.p, vn.data(), 8 * vn.size(), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_hemo.p, st.data(), sizeof(HemoStateDev) * st.size(),
+                           cudaMemcpyHostToDevice, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+    hemo_p = {p.kappa, p.gamma, p.tau, p.alpha, p.e0, p.v0};
+    hemo_baseline = baseline_hz;
+    hemo_every = sample_every;
+    hemo_on = true;
+}
+
 struct Chunk {
     uint32_t t0, rel0, steps;
 };
@@ -1258,11 +1333,26 @@ void Engine::advance(uint32_t steps) {
     d_phase_wait.reserve(chunk + 2);
     exchange_wait_ms = 0;
 
+    const uint32_t n_bold = hemo_on ? steps / hemo_every : 0u;
+    bold.assign((size_t)n_bold * n_voxels, 0.0);
+    if (hemo_on) {
+        d_bold.reserve(std::max<size_t>(1, bold.size()));
+        const unsigned long long none = ~0ull;
+        CK(cudaMemcpyAsync(d_hemo_err.p, &none, 8, cudaMemcpyHostToDevice, stream));
+    }
+
     std::vector<unsigned long long> phase_ns_all;
     phase_ns_all.reserve(steps + 2);
     for (uint32_t rel0 = 0; rel0 < steps; rel0 += chunk) {
         const uint32_t cs = std::min(chunk, steps - rel0);
         run_chunk(step_done + rel0, rel0, cs, steps);
+        if (hemo_on) {  // window_bold (assim.cpp:51-71) over this chunk's rate rows
+            bold_kernel<<<(n_voxels + 127) / 128, 128, 0, stream>>>(
+                d_rates.p, cs, d_vox_off.p, d_vox_units.p, d_vox_n.p, n_voxels, hemo_p,
+                dt_ms * 1e-3, hemo_baseline, hemo_every, rel0, d_hemo.p, d_bold.p, d_hemo_err.p);
+            CK(cudaGetLastError());
+            launches += 1;
+        }
         // phase end times of this chunk
         std::vector<unsigned long long> ph(cs + 2);
         CK(cudaMemcpyAsync(ph.data(), d_phase_ns.p, 8ull * (cs + 2), cudaMemcpyDeviceToHost,
@@ -1283,6 +1373,17 @@ void Engine::advance(uint32_t steps) {
                            cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         d2h += 8 * probe_v.size();
+    }
+    bool hemo_diverged = false;
+    if (hemo_on) {
+        unsigned long long herr = 0;
+        if (!bold.empty())
+            CK(cudaMemcpyAsync(bold.data(), d_bold.p, 8 * bold.size(), cudaMemcpyDeviceToHost,
+                               stream));
+        CK(cudaMemcpyAsync(&herr, d_hemo_err.p, 8, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        d2h += 8 * bold.size() + 8;
+        hemo_diverged = herr != ~0ull;
     }
     for (uint32_t x : rates) total_spikes += x;
     const uint64_t nn = n;
@@ -1318,6 +1419,8 @@ void Engine::advance(uint32_t steps) {
         }
     }
     step_done += steps;
+    // hemo.cpp:37-40, raised by the readout: the simulation state is intact
+    if (hemo_diverged) throw HemoError("hemodynamic state diverged");
 }
 
 void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
@@ -1553,6 +1656,9 @@ int vxb_advance(vxb_engine* e, uint32_t steps) {
     try {
         e->eng.advance(steps);
         return VXB_OK;
+    } catch (const HemoError& x) {  // raised by the BOLD readout, not the simulation
+        e->eng.err = x.what();
+        return VXB_ESIM;
     } catch (const std::exception& x) {
         e->eng.err = x.what();
         e->eng.failed = true;
@@ -1933,6 +2039,76 @@ int vxb_debug_stream_xi(int device, const uint64_t* base, const uint64_t* k, uin
         debug_xi_kernel<<<1184, 256>>>(b.p, kk.p, n, o.p);
         CK(cudaGetLastError());
         CK(cudaMemcpy(out, o.p, 4 * n, cudaMemcpyDeviceToHost));
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g_create_error = x.what();
+        return fail_code(x);
+    }
+}
+
+int vxb_set_hemodynamics(vxb_engine* e, const vxb_hemo_params* p, double baseline_hz,
+                         uint32_t sample_every, const vxb_hemo_state* init) {
+    Engine& g = e->eng;
+    try {
+        if (!p) throw ConfigError("hemodynamics: null parameters");
+        g.set_hemodynamics(*p, baseline_hz, sample_every, init);
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
+}
+
+int vxb_hemo_get_state(const vxb_engine* e, vxb_hemo_state* out, uint32_t cap) {
+    const Engine& g = e->eng;
+    if (!g.hemo_on || cap < g.n_voxels) return VXB_ECONFIG;
+    if (cudaSetDevice(g.device) != cudaSuccess ||
+        cudaMemcpy(out, g.d_hemo.p, sizeof(vxb_hemo_state) * g.n_voxels,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+        return VXB_ESIM;
+    return VXB_OK;
+}
+
+uint64_t vxb_result_bold_size(const vxb_engine* e) { return e->eng.bold.size(); }
+
+int vxb_result_bold(const vxb_engine* e, double* out, uint64_t cap) {
+    if (cap < e->eng.bold.size()) return VXB_ECONFIG;
+    std::memcpy(out, e->eng.bold.data(), 8 * e->eng.bold.size());
+    return VXB_OK;
+}
+
+int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double* z,
+                              uint32_t steps, uint32_t n_series, double dt_s,
+                              uint32_t sample_every, vxb_hemo_state* state, double* out) {
+    try {
+        if (!p) throw ConfigError("hemodynamics: null parameters");
+        validate_hemo(*p, 1.0, sample_every);
+        int nd = 0;
+        if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0)
+            throw SimError("no CUDA device available (the engine has no CPU fallback)");
+        CK(cudaSetDevice(device));
+        const size_t nz = (size_t)steps * n_series, no = (size_t)(steps / sample_every) * n_series;
+        DevBuf<double> dz, dout;
+        DevBuf<HemoStateDev> dst;
+        DevBuf<unsigned long long> derr;
+        dz.alloc(std::max<size_t>(1, nz));
+        dout.alloc(std::max<size_t>(1, no));
+        dst.alloc(std::max<uint32_t>(1, n_series));
+        derr.alloc(1);
+        const unsigned long long none = ~0ull;
+        if (nz) CK(cudaMemcpy(dz.p, z, 8 * nz, cudaMemcpyHostToDevice));
+        if (n_series) CK(cudaMemcpy(dst.p, state, sizeof(HemoStateDev) * n_series, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(derr.p, &none, 8, cudaMemcpyHostToDevice));
+        const HemoParamsDev hp{p->kappa, p->gamma, p->tau, p->alpha, p->e0, p->v0};
+        if (n_series)
+            bold_drive_kernel<<<(n_series + 127) / 128, 128>>>(dz.p, steps, n_series, hp, dt_s,
+                                                               sample_every, dst.p, dout.p, derr.p);
+        CK(cudaGetLastError());
+        unsigned long long err = 0;
+        CK(cudaMemcpy(&err, derr.p, 8, cudaMemcpyDeviceToHost));
+        if (no) CK(cudaMemcpy(out, dout.p, 8 * no, cudaMemcpyDeviceToHost));
+        if (n_series) CK(cudaMemcpy(state, dst.p, sizeof(HemoStateDev) * n_series, cudaMemcpyDeviceToHost));
+        if (err != ~0ull) throw SimError("hemodynamic state diverged");
         return VXB_OK;
     } catch (const std::exception& x) {
         g_create_error = x.what();

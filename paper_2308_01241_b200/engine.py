@@ -166,6 +166,59 @@ class RateSeries:
 
 
 @dataclass
+class HemoParams:
+    """voxsim::HemoParams (hemo.hpp:10-23): Balloon-Windkessel constants."""
+    kappa: float = 0.65   # signal decay, 1/s
+    gamma: float = 0.41   # flow-dependent elimination, 1/s
+    tau: float = 0.98     # hemodynamic transit time, s
+    alpha: float = 0.32   # Grubb's exponent
+    e0: float = 0.34      # resting oxygen extraction
+    v0: float = 0.02      # resting venous volume fraction
+
+    def k1(self) -> float:
+        return 7.0 * self.e0
+
+    def k2(self) -> float:
+        return 2.0
+
+    def k3(self) -> float:
+        return 2.0 * self.e0 - 0.2
+
+    def _c(self) -> _abi.HemoParams:
+        return _abi.HemoParams(self.kappa, self.gamma, self.tau, self.alpha, self.e0, self.v0)
+
+
+HEMO_STATE_DTYPE = np.dtype([("s", "f8"), ("f", "f8"), ("v", "f8"), ("q", "f8")])
+
+
+def hemo_rest(n: int) -> np.ndarray:
+    """n HemoState records at rest (hemo.hpp:25-30): s = 0, f = v = q = 1."""
+    st = np.zeros(n, HEMO_STATE_DTYPE)
+    st["f"] = st["v"] = st["q"] = 1.0
+    return st
+
+
+def bold_from_drive(z, dt_s: float, sample_every: int, params: HemoParams | None = None,
+                    state: np.ndarray | None = None, device: int = 0) -> np.ndarray:
+    """voxsim::bold_from_drive (hemo.cpp:49-62) evaluated on the GPU for one
+    drive series (1-D z) or several (2-D z[series][steps]); `state` (HEMO_STATE_DTYPE,
+    one per series) is updated in place when given."""
+    p = params or HemoParams()
+    zz = np.ascontiguousarray(np.atleast_2d(np.asarray(z, np.float64)))
+    ns, steps = zz.shape
+    st = hemo_rest(ns) if state is None else state
+    if st.dtype != HEMO_STATE_DTYPE or not st.flags.c_contiguous or st.size != ns:
+        raise ConfigError("hemodynamics: state must be a contiguous HemoState array per series")
+    out = np.zeros((ns, steps // max(1, sample_every)), np.float64)
+    lib = _abi.load_library()
+    rc = lib.vxb_debug_bold_from_drive(device, C.byref(p._c()), ptr(zz), steps, ns, dt_s,
+                                       sample_every, ptr(st), ptr(out))
+    if rc != 0:
+        _raise(rc, lib.vxb_last_error(None).decode())
+    return out[0] if np.ndim(z) == 1 else out
+
+
+@dataclass
 class RunResult:
     """voxsim::RunResult (engine.hpp:55-63)."""
     raster: np.ndarray          # RASTER_DTYPE, sorted (step, worker, local)
@@ -180,6 +233,8 @@ class RunResult:
     d2h_bytes: int = 0
     launches: int = 0
     exchange_wait_ms: float = 0.0
+    # BOLD-proxy readout (set_hemodynamics): [steps // sample_every][voxels]
+    bold: np.ndarray | None = None
 
     @property
     def events(self) -> int:
@@ -196,6 +251,7 @@ class SimInstance:
         self._opt = options
         self._units = tables.units.copy()
         self._n_voxels = tables.n_voxels
+        self._hemo_every = 0
         net, keep_net = tables._descriptor()
         opt, keep_opt = options._descriptor()
         h = C.c_void_p()
@@ -262,11 +318,42 @@ class SimInstance:
             L.vxb_result_timings(h, ptr(timings), nt)
         rates = RateSeries(steps, self._opt.dt_ms, self._units["neurons"].astype(np.uint64),
                            counts)
+        bold = None
+        if self._hemo_every:
+            bold = np.zeros((steps // self._hemo_every, self._n_voxels), np.float64)
+            if bold.size:
+                L.vxb_result_bold(h, ptr(bold), bold.size)
         return RunResult(raster, timings, probes, rates, flops,
                          int(L.vxb_result_total_spikes(h)), steps,
                          float(L.vxb_result_device_ms(h)), int(L.vxb_result_h2d_bytes(h)),
                          int(L.vxb_result_d2h_bytes(h)), int(L.vxb_result_launches(h)),
-                         float(L.vxb_result_exchange_wait_ms(h)))
+                         float(L.vxb_result_exchange_wait_ms(h)), bold)
+
+    def set_hemodynamics(self, params: HemoParams | None = None, baseline_hz: float = 1.0,
+                         sample_every: int = 1, state: np.ndarray | None = None) -> None:
+        """Device BOLD-proxy readout for every following advance: the
+        assimilation caller's window_bold (assim.cpp:51-71) per voxel, sampled
+        like bold_from_drive (hemo.cpp:49-62); `state` seeds the per-voxel
+        HemoState (default: rest) and then carries across advances."""
+        p = params or HemoParams()
+        st = None
+        if state is not None:
+            st = np.ascontiguousarray(state, HEMO_STATE_DTYPE)
+            if st.size != self._n_voxels:
+                raise ConfigError("hemodynamic state size does not match the voxel count")
+        rc = self._lib.vxb_set_hemodynamics(self._h, C.byref(p._c()), baseline_hz, sample_every,
+                                            ptr(st))
+        if rc != 0:
+            self._err(rc)
+        self._hemo_every = sample_every
+
+    def hemo_state(self) -> np.ndarray:
+        """Per-voxel HemoState after the last advance (HEMO_STATE_DTYPE)."""
+        out = np.zeros(self._n_voxels, HEMO_STATE_DTYPE)
+        rc = self._lib.vxb_hemo_get_state(self._h, ptr(out), out.size)
+        if rc != 0:
+            self._err(rc)
+        return out
 
     def set_conductances(self, unit: int, receptor: int, values) -> None:
         v = np.ascontiguousarray(values, dtype=np.float32)

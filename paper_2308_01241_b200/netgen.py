@@ -1050,6 +1050,7 @@ class GeneratedSimInstance(SimInstance):
         self._opt = options
         self._units = net.arrays["units"].copy()
         self._n_voxels = len(net.layout.voxels)
+        self._hemo_every = 0
         spec = net.spec()
         opt, keep = options._descriptor()
         h = C.c_void_p()
@@ -1125,6 +1126,7 @@ class DistributedSimInstance(SimInstance):
         self._opt = options
         self._units = net.arrays["units"].copy()
         self._n_voxels = len(net.layout.voxels)
+        self._hemo_every = 0
         self.rank, self.world = rank, world
         spec = net.spec()
         opt, keep = options._descriptor()

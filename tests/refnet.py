@@ -88,6 +88,10 @@ def ref_lib():
             "ref_current_kernel": (C.c_float, [C.c_float, P, P, P]),
             "ref_ou_kernel": (C.c_float, [C.c_float] * 6),
             "ref_ou_xi": (C.c_float, [u64, u64, u64]),
+            "ref_bold_from_drive": (C.c_int, [P, P, u32, C.c_double, u32, P, P, C.c_char_p,
+                                              C.c_int]),
+            "ref_window_bold": (C.c_int, [P, P, u32, u32, P, u32, P, C.c_double, C.c_double,
+                                          u32, P, P, C.c_char_p, C.c_int]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -390,3 +394,43 @@ class OracleSim:
 def raster_set(raster: np.ndarray):
     """Multiset of (step, gid), as test_engine.cpp:98-103."""
     return sorted(zip(raster["step"].tolist(), raster["gid"].tolist()))
+
+
+# ---------------------------------------------------------- hemodynamics
+def _hemo_p(params):
+    return np.array([params.kappa, params.gamma, params.tau, params.alpha, params.e0,
+                     params.v0], np.float64)
+
+
+def ref_bold_from_drive(params, z, dt_s, sample_every, state=None):
+    """The reference's bold_from_drive (hemo.cpp:49-62); state = [s, f, v, q]
+    (float64[4], updated in place) or rest."""
+    L = ref_lib()
+    z = np.ascontiguousarray(z, np.float64)
+    st = np.array([0.0, 1.0, 1.0, 1.0]) if state is None else state
+    out = np.zeros(len(z) // max(1, sample_every), np.float64)
+    err = C.create_string_buffer(1024)
+    rc = L.ref_bold_from_drive(ptr(_hemo_p(params)), ptr(z), len(z), dt_s, sample_every,
+                               ptr(st), ptr(out), err, 1024)
+    if rc:
+        _raise(rc, _strip(err.value.decode()))
+    return out
+
+
+def ref_window_bold(params, counts, unit_voxel, vox_n, dt_s, baseline_hz, sample_every,
+                    states):
+    """window_bold (assim.cpp:51-71) with bold_from_drive sampling, around the
+    reference's step_hemodynamics / bold_signal; states float64[voxels][4] in/out."""
+    L = ref_lib()
+    counts = np.ascontiguousarray(counts, np.uint32)
+    nu, steps = counts.shape
+    uv = np.ascontiguousarray(unit_voxel, np.uint32)
+    vn = np.ascontiguousarray(vox_n, np.uint64)
+    out = np.zeros((steps // sample_every, len(vn)), np.float64)
+    err = C.create_string_buffer(1024)
+    rc = L.ref_window_bold(ptr(_hemo_p(params)), ptr(counts), nu, steps, ptr(uv), len(vn),
+                           ptr(vn), dt_s, baseline_hz, sample_every, ptr(states), ptr(out),
+                           err, 1024)
+    if rc:
+        _raise(rc, _strip(err.value.decode()))
+    return out

@@ -218,6 +218,11 @@ def run_reference(args):
     if rank != 0:
         return
     ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
+    # size each bench step so the whole warmup + steps run takes about
+    # --cpu-budget-s on this host (host core counts differ between boxes)
+    e0, s0, _ = ref.step(200)
+    per_step_s = args.cpu_budget_s / max(1, args.steps + args.warmup)
+    args.cpu_steps = int(min(args.cpu_steps, max(50, per_step_s / max(s0 / 200, 1e-9))))
     for _ in range(args.warmup):
         ref.step(args.cpu_steps)
     ev = sec = spk = 0
@@ -399,8 +404,11 @@ def run_b200(args):
     if not args.no_cpu and args.workload == "config2":
         try:
             ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
-            ref.step(20)
-            e, s, k = ref.step(args.cpu_sample_steps)
+            _, s0, _ = ref.step(300)  # warm-up + rate probe: ~cpu_sample_seconds of sample
+            n_s = int(min(args.cpu_sample_steps,
+                          max(500, args.cpu_sample_seconds / max(s0 / 300, 1e-9))))
+            args.cpu_sample_steps = n_s
+            e, s, k = ref.step(n_s)
             line["cpu_baseline"] = {
                 "value": e / s, "unit": "events/s", "cores": ref.threads, "kind": "reference",
                 "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_sample_steps} "
@@ -426,7 +434,11 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4000,
                     help="--impl reference: simulated steps per bench step")
     ap.add_argument("--cpu-sample-steps", type=int, default=12000,
-                    help="cpu_baseline of the B200 arm: simulated steps of the timed sample")
+                    help="cpu_baseline of the B200 arm: at most this many simulated steps")
+    ap.add_argument("--cpu-sample-seconds", type=float, default=15.0,
+                    help="cpu_baseline of the B200 arm: target wall time of the sample")
+    ap.add_argument("--cpu-budget-s", type=float, default=150.0,
+                    help="--impl reference: target wall time of warmup + steps")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4"])
     ap.add_argument("--rate", type=int, default=10, choices=[7, 10, 15, 30],

@@ -357,7 +357,13 @@ class SimInstance:
 
     def set_conductances(self, unit: int, receptor: int, values) -> None:
         v = np.ascontiguousarray(values, dtype=np.float32)
-        rc = self._lib.vxb_set_conductances(self._h, unit, receptor, ptr(v), v.size)
+        # (per-window hot call of the assimilation caller: from_buffer is ~2x
+        # cheaper than ndarray.ctypes for the address of a writable buffer)
+        try:
+            addr = C.addressof(C.c_char.from_buffer(v)) if v.size else None
+        except (TypeError, ValueError):
+            addr = ptr(v)
+        rc = self._lib.vxb_set_conductances(self._h, unit, receptor, addr, v.size)
         if rc != 0:
             self._err(rc)
 

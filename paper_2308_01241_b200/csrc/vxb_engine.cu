@@ -1488,6 +1488,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     d_work.zero(stream);
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
+    // chunks of one local spike when a row segment averages >= 512 entries
+    // (in-degree per L2 block; config 2: 1000), else up to 32 (config 3's
+    // short L2-block segments: 1.14 ms per step at 32, 1.31 ms at 13, 6.2 at 1)
+    a.ch_max = (n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
     a.f_policy = f_policy ? 1u : 0u;
     {
         const char* ep = std::getenv("VXB_EARLY_PUBLISH");

@@ -176,6 +176,9 @@ struct StepArgs {
     // works on one L2 block at a time and balances itself (dyn != 0)
     uint32_t* work_ctr;
     uint32_t dyn;
+    uint32_t ch_max;    // dynamic delivery of local spikes: most spikes per chunk (1 for
+                        // long rows: the phase's last chunk ends sooner, config 2 79.4 ->
+                        // 77.9 us/step); peers' batches (short rows here) take up to 32
     uint32_t f_policy;  // 1: neuron-state stream evict_first in L2
     // phase profile (VXB_PHASE_PROFILE): per (phase, CTA) globaltimer of the
     // end of this CTA's delivery and of its update, or null
@@ -845,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                                 ids = a.ex->rx_ids[h] + tslot * a.ex->cap[h];
                             }
                             const uint32_t sb = a.ex->src_base[h];
-                            const uint32_t CH = max(1u, min(32u, cnt / (8u * gridDim.x)));
+                            const uint32_t CH = max(1u, min(li ? 32u : a.ch_max, cnt / (8u * gridDim.x)));
                             uint32_t* ctr = wc + blk * W + li;
                             uint32_t nxt = 0;
                             if (lane == 0) nxt = atomicAdd(ctr, CH);

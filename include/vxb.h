@@ -363,7 +363,10 @@ typedef struct vxb_hemo_state { /* HemoState (hemo.hpp:25-30); rest = {0, 1, 1, 
  * seeds the per-voxel state, which then carries across advances.  Errors:
  * HemoParams::validate / baseline_hz > 0 / sample_every >= 1 -> VXB_ECONFIG;
  * a diverged state makes advance() return VXB_ESIM with the reference's
- * message, the simulation itself staying usable.  One device only. */
+ * message, the simulation itself staying usable.  On several GPUs (one
+ * engine per rank) advance() only sums the rank's voxel counts: the caller
+ * adds the ranks' vxb_result_voxel_counts and passes the totals to
+ * vxb_hemo_feed_counts, which runs the same model on them. */
 int vxb_set_hemodynamics(vxb_engine* e, const vxb_hemo_params* p, double baseline_hz,
                          uint32_t sample_every, const vxb_hemo_state* init);
 /* Current per-voxel states (cap >= n_voxels). */
@@ -371,6 +374,13 @@ int vxb_hemo_get_state(const vxb_engine* e, vxb_hemo_state* out, uint32_t cap);
 /* BOLD samples of the last advance: [steps / sample_every][n_voxels]. */
 uint64_t vxb_result_bold_size(const vxb_engine* e);
 int vxb_result_bold(const vxb_engine* e, double* out, uint64_t cap);
+/* Voxel spike counts of the last advance, [steps][n_voxels]
+ * (RateSeries::voxel_counts, stats.cpp:193-201; this rank's units only). */
+int vxb_result_voxel_counts(const vxb_engine* e, uint32_t* out, uint64_t cap);
+/* Several GPUs: run the hemodynamics of the last advance on the ranks'
+ * summed voxel counts [steps][n_voxels] (steps = the advance's); the BOLD
+ * samples are then read with vxb_result_bold. */
+int vxb_hemo_feed_counts(vxb_engine* e, const uint32_t* counts, uint32_t steps);
 /* Diagnostics: bold_from_drive (hemo.cpp:49-62) on the device for n_series
  * drive series z[series][steps]; state[n_series] in/out; out[series][steps /
  * sample_every]. */

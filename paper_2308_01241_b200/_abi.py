@@ -158,6 +158,7 @@ EXPORTS = [
     "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
     "vxb_result_exchange_wait_ms", "vxb_fnv1a", "vxb_set_hemodynamics", "vxb_hemo_get_state",
     "vxb_result_bold_size", "vxb_result_bold", "vxb_debug_bold_from_drive",
+    "vxb_result_voxel_counts", "vxb_hemo_feed_counts",
 ]
 
 _lib = None
@@ -211,6 +212,8 @@ def _declare(lib):
         "vxb_hemo_get_state": (C.c_int, [P, P, C.c_uint32]),
         "vxb_result_bold_size": (C.c_uint64, [P]),
         "vxb_result_bold": (C.c_int, [P, P, C.c_uint64]),
+        "vxb_result_voxel_counts": (C.c_int, [P, P, C.c_uint64]),
+        "vxb_hemo_feed_counts": (C.c_int, [P, P, C.c_uint32]),
         "vxb_debug_bold_from_drive": (C.c_int, [C.c_int, C.POINTER(HemoParams), P, C.c_uint32,
                                                 C.c_uint32, C.c_double, C.c_uint32, P, P]),
     }

@@ -251,8 +251,12 @@ struct Engine {
     DevBuf<HemoStateDev> d_hemo;
     DevBuf<uint32_t> d_vox_off, d_vox_units;
     DevBuf<double> d_vox_n, d_bold;
+    DevBuf<uint32_t> d_vcounts;            // [steps][voxels] of the last advance
     DevBuf<unsigned long long> d_hemo_err;
     std::vector<double> bold;
+    std::vector<uint32_t> vcounts;         // voxel counts of the last advance (this rank's units)
+    void run_hemo(uint32_t t_base, uint32_t steps);
+    bool fetch_bold();                     // false: a voxel's state diverged
     void set_hemodynamics(const vxb_hemo_params& p, double baseline_hz, uint32_t sample_every,
                           const vxb_hemo_state* init);
 
@@ -1200,8 +1204,6 @@ void validate_hemo(const vxb_hemo_params& p, double baseline_hz, uint32_t sample
 void Engine::set_hemodynamics(const vxb_hemo_params& p, double baseline_hz,
                               uint32_t sample_every, const vxb_hemo_state* init) {
     validate_hemo(p, baseline_hz, sample_every);
-    if (world > 1)
-        throw ConfigError("the device BOLD readout needs every unit on this device (one GPU)");
     CK(cudaSetDevice(device));
     // voxel -> units CSR and voxel sizes (voxel_sizes, assim.cpp:319)
     std::vector<uint32_t> off(n_voxels + 1, 0), vu(n_units);
@@ -1238,6 +1240,24 @@ void Engine::set_hemodynamics(const vxb_hemo_params& p, double baseline_hz,
     hemo_baseline = baseline_hz;
     hemo_every = sample_every;
     hemo_on = true;
+}
+
+void Engine::run_hemo(uint32_t t_base, uint32_t steps) {
+    hemo_counts_kernel<<<(n_voxels + 127) / 128, 128, 0, stream>>>(
+        d_vcounts.p, t_base, steps, d_vox_n.p, n_voxels, hemo_p, dt_ms * 1e-3, hemo_baseline,
+        hemo_every, d_hemo.p, d_bold.p, d_hemo_err.p);
+    CK(cudaGetLastError());
+    launches += 1;
+}
+
+bool Engine::fetch_bold() {
+    unsigned long long herr = 0;
+    if (!bold.empty())
+        CK(cudaMemcpyAsync(bold.data(), d_bold.p, 8 * bold.size(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&herr, d_hemo_err.p, 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    d2h += 8 * bold.size() + 8;
+    return herr == ~0ull;
 }
 
 struct Chunk {
@@ -1333,10 +1353,12 @@ void Engine::advance(uint32_t steps) {
     d_phase_wait.reserve(chunk + 2);
     exchange_wait_ms = 0;
 
-    const uint32_t n_bold = hemo_on ? steps / hemo_every : 0u;
+    const uint32_t n_bold = hemo_on && world == 1 ? steps / hemo_every : 0u;
     bold.assign((size_t)n_bold * n_voxels, 0.0);
+    vcounts.assign(hemo_on ? (size_t)steps * n_voxels : 0, 0u);
     if (hemo_on) {
         d_bold.reserve(std::max<size_t>(1, bold.size()));
+        d_vcounts.reserve(std::max<size_t>(1, vcounts.size()));
         const unsigned long long none = ~0ull;
         CK(cudaMemcpyAsync(d_hemo_err.p, &none, 8, cudaMemcpyHostToDevice, stream));
     }
@@ -1347,11 +1369,12 @@ void Engine::advance(uint32_t steps) {
         const uint32_t cs = std::min(chunk, steps - rel0);
         run_chunk(step_done + rel0, rel0, cs, steps);
         if (hemo_on) {  // window_bold (assim.cpp:51-71) over this chunk's rate rows
-            bold_kernel<<<(n_voxels + 127) / 128, 128, 0, stream>>>(
-                d_rates.p, cs, d_vox_off.p, d_vox_units.p, d_vox_n.p, n_voxels, hemo_p,
-                dt_ms * 1e-3, hemo_baseline, hemo_every, rel0, d_hemo.p, d_bold.p, d_hemo_err.p);
+            const uint32_t work = cs * n_voxels;
+            voxel_counts_kernel<<<std::min<uint32_t>(1184, (work + 255) / 256), 256, 0, stream>>>(
+                d_rates.p, cs, d_vox_off.p, d_vox_units.p, n_voxels, rel0, d_vcounts.p);
             CK(cudaGetLastError());
             launches += 1;
+            if (world == 1) run_hemo(rel0, cs);  // (several GPUs: the totals are fed back)
         }
         // phase end times of this chunk
         std::vector<unsigned long long> ph(cs + 2);
@@ -1376,14 +1399,11 @@ void Engine::advance(uint32_t steps) {
     }
     bool hemo_diverged = false;
     if (hemo_on) {
-        unsigned long long herr = 0;
-        if (!bold.empty())
-            CK(cudaMemcpyAsync(bold.data(), d_bold.p, 8 * bold.size(), cudaMemcpyDeviceToHost,
-                               stream));
-        CK(cudaMemcpyAsync(&herr, d_hemo_err.p, 8, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        d2h += 8 * bold.size() + 8;
-        hemo_diverged = herr != ~0ull;
+        if (!vcounts.empty())
+            CK(cudaMemcpyAsync(vcounts.data(), d_vcounts.p, 4 * vcounts.size(),
+                               cudaMemcpyDeviceToHost, stream));
+        d2h += 4 * vcounts.size();
+        hemo_diverged = !fetch_bold();
     }
     for (uint32_t x : rates) total_spikes += x;
     const uint64_t nn = n;
@@ -1488,10 +1508,12 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     d_work.zero(stream);
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
-    // chunks of one local spike when a row segment averages >= 512 entries
-    // (in-degree per L2 block; config 2: 1000), else up to 32 (config 3's
-    // short L2-block segments: 1.14 ms per step at 32, 1.31 ms at 13, 6.2 at 1)
-    a.ch_max = (n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
+    // chunks of one local spike on one GPU when a row segment averages >= 512
+    // entries (in-degree per L2 block; config 2: 1000), else up to 32
+    // (config 3's short L2-block segments: 1.14 ms per step at 32, 1.31 ms at
+    // 13, 6.2 at 1; config 2 on 2 GPUs: 2.44e11 events/s at 32, 2.37e11 at 1)
+    a.ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
+    if (const char* env = std::getenv("VXB_CHMAX")) a.ch_max = std::max(1, std::atoi(env));
     a.f_policy = f_policy ? 1u : 0u;
     {
         const char* ep = std::getenv("VXB_EARLY_PUBLISH");
@@ -2074,6 +2096,35 @@ int vxb_hemo_get_state(const vxb_engine* e, vxb_hemo_state* out, uint32_t cap) {
 }
 
 uint64_t vxb_result_bold_size(const vxb_engine* e) { return e->eng.bold.size(); }
+
+int vxb_result_voxel_counts(const vxb_engine* e, uint32_t* out, uint64_t cap) {
+    if (!e->eng.hemo_on || cap < e->eng.vcounts.size()) return VXB_ECONFIG;
+    std::memcpy(out, e->eng.vcounts.data(), 4 * e->eng.vcounts.size());
+    return VXB_OK;
+}
+
+int vxb_hemo_feed_counts(vxb_engine* e, const uint32_t* counts, uint32_t steps) {
+    Engine& g = e->eng;
+    try {
+        if (!g.hemo_on) throw ConfigError("hemodynamics are not enabled");
+        if (g.world == 1) throw ConfigError("one GPU: advance() already drove the hemodynamics");
+        if (steps != g.res_steps) throw ConfigError("counts must cover the last advance");
+        CK(cudaSetDevice(g.device));
+        const size_t nc = (size_t)steps * g.n_voxels;
+        g.bold.assign((size_t)(steps / g.hemo_every) * g.n_voxels, 0.0);
+        g.d_bold.reserve(std::max<size_t>(1, g.bold.size()));
+        g.d_vcounts.reserve(std::max<size_t>(1, nc));
+        const unsigned long long none = ~0ull;
+        CK(cudaMemcpyAsync(g.d_hemo_err.p, &none, 8, cudaMemcpyHostToDevice, g.stream));
+        if (nc) CK(cudaMemcpyAsync(g.d_vcounts.p, counts, 4 * nc, cudaMemcpyHostToDevice, g.stream));
+        if (steps) g.run_hemo(0, steps);
+        if (!g.fetch_bold()) throw HemoError("hemodynamic state diverged");
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
+}
 
 int vxb_result_bold(const vxb_engine* e, double* out, uint64_t cap) {
     if (cap < e->eng.bold.size()) return VXB_ECONFIG;

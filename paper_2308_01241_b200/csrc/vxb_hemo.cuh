@@ -8,9 +8,12 @@
 // of the Balloon-Windkessel model (step_hemodynamics, hemo.cpp:19-41)
 // advances the voxel's state; BOLD (bold_signal, hemo.cpp:43-47) is sampled
 // every `sample_every` steps (bold_from_drive, hemo.cpp:49-62).  Here the
-// per-unit counts never leave the device: one thread per voxel runs the
-// model over each chunk's rate rows right after the step kernel, carrying
-// the state between chunks and advance() calls.
+// per-unit counts never leave the device: after every chunk of the step
+// kernel the voxel counts are summed from its rate rows and one thread per
+// voxel runs the model over them, carrying the state between chunks and
+// advance() calls.  On several GPUs each rank sums its own units, the ranks
+// add their counts (one small all-gather per advance) and feed the totals
+// back (vxb_hemo_feed_counts).
 //
 // The arithmetic is the reference's, operation for operation in IEEE double
 // (no FMA contraction: the library is built with --fmad=false); pow() is
@@ -57,31 +60,45 @@ __device__ __forceinline__ double hemo_bold(const HemoStateDev& h, const HemoPar
                    (2.0 * p.e0 - 0.2) * (1.0 - v));
 }
 
-// One thread per voxel over the rate rows of one chunk ([unit][steps]):
-// voxel count -> drive -> Euler step; BOLD at every (t_base + t + 1) %
-// sample_every == 0 into out[sample][voxel].  A diverged voxel records the
-// first failing (advance step << 32 | voxel) in *err and stops.
-__global__ void bold_kernel(const uint32_t* __restrict__ rates, uint32_t steps,
-                            const uint32_t* __restrict__ vox_off,
-                            const uint32_t* __restrict__ vox_units,
-                            const double* __restrict__ vox_n, uint32_t n_vox, HemoParamsDev p,
-                            double dt_s, double baseline_hz, uint32_t sample_every,
-                            uint32_t t_base, HemoStateDev* __restrict__ state,
-                            double* __restrict__ out, unsigned long long* __restrict__ err) {
+// RateSeries::voxel_counts (stats.cpp:193-201) on the device for the rate
+// rows of one chunk ([unit][steps]): counts[(t_base + t) * n_vox + v].  On
+// several GPUs these are the rank's partial sums (its units only).
+__global__ void voxel_counts_kernel(const uint32_t* __restrict__ rates, uint32_t steps,
+                                    const uint32_t* __restrict__ vox_off,
+                                    const uint32_t* __restrict__ vox_units, uint32_t n_vox,
+                                    uint32_t t_base, uint32_t* __restrict__ counts) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < steps * n_vox;
+         x += gridDim.x * blockDim.x) {
+        const uint32_t t = x / n_vox, v = x - t * n_vox;
+        uint32_t c = 0;
+        for (uint32_t k = vox_off[v]; k < vox_off[v + 1]; ++k)
+            c += rates[(size_t)vox_units[k] * steps + t];
+        counts[(size_t)(t_base + t) * n_vox + v] = c;
+    }
+}
+
+// window_bold's per-voxel loop (assim.cpp:58-66), one thread per voxel, over
+// count rows [t_base, t_base + steps) of counts[step][voxel]: drive ->
+// Euler step; BOLD at every (t + 1) % sample_every == 0 into
+// out[sample][voxel].  A diverged voxel records the first failing
+// (step << 32 | voxel) in *err and stops.
+__global__ void hemo_counts_kernel(const uint32_t* __restrict__ counts, uint32_t t_base,
+                                   uint32_t steps, const double* __restrict__ vox_n,
+                                   uint32_t n_vox, HemoParamsDev p, double dt_s,
+                                   double baseline_hz, uint32_t sample_every,
+                                   HemoStateDev* __restrict__ state, double* __restrict__ out,
+                                   unsigned long long* __restrict__ err) {
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n_vox) return;
     HemoStateDev h = state[v];
-    const uint32_t k0 = vox_off[v], k1 = vox_off[v + 1];
-    for (uint32_t t = 0; t < steps; ++t) {
-        uint32_t c = 0;
-        for (uint32_t k = k0; k < k1; ++k) c += rates[(size_t)vox_units[k] * steps + t];
+    for (uint32_t t = t_base; t < t_base + steps; ++t) {
+        const uint32_t c = counts[(size_t)t * n_vox + v];
         const double hz = vox_n[v] > 0 ? c / (vox_n[v] * dt_s) : 0.0;
         if (!hemo_step(h, hz / baseline_hz, dt_s, p)) {
-            atomicMin(err, ((unsigned long long)(t_base + t) << 32) | v);
+            atomicMin(err, ((unsigned long long)t << 32) | v);
             break;
         }
-        const uint32_t ts = t_base + t + 1;
-        if (ts % sample_every == 0) out[(size_t)(ts / sample_every - 1) * n_vox + v] = hemo_bold(h, p);
+        if ((t + 1) % sample_every == 0) out[(size_t)((t + 1) / sample_every - 1) * n_vox + v] = hemo_bold(h, p);
     }
     state[v] = h;
 }

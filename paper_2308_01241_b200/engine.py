@@ -233,8 +233,10 @@ class RunResult:
     d2h_bytes: int = 0
     launches: int = 0
     exchange_wait_ms: float = 0.0
-    # BOLD-proxy readout (set_hemodynamics): [steps // sample_every][voxels]
+    # BOLD-proxy readout (set_hemodynamics): [steps // sample_every][voxels],
+    # and the voxel spike counts it was driven by, [steps][voxels]
     bold: np.ndarray | None = None
+    voxel_counts: np.ndarray | None = None
 
     @property
     def events(self) -> int:
@@ -318,16 +320,24 @@ class SimInstance:
             L.vxb_result_timings(h, ptr(timings), nt)
         rates = RateSeries(steps, self._opt.dt_ms, self._units["neurons"].astype(np.uint64),
                            counts)
-        bold = None
+        bold = vcounts = None
         if self._hemo_every:
-            bold = np.zeros((steps // self._hemo_every, self._n_voxels), np.float64)
-            if bold.size:
-                L.vxb_result_bold(h, ptr(bold), bold.size)
+            bold = self._bold(steps)
+            vcounts = np.zeros((steps, self._n_voxels), np.uint32)
+            if vcounts.size:
+                L.vxb_result_voxel_counts(h, ptr(vcounts), vcounts.size)
         return RunResult(raster, timings, probes, rates, flops,
                          int(L.vxb_result_total_spikes(h)), steps,
                          float(L.vxb_result_device_ms(h)), int(L.vxb_result_h2d_bytes(h)),
                          int(L.vxb_result_d2h_bytes(h)), int(L.vxb_result_launches(h)),
-                         float(L.vxb_result_exchange_wait_ms(h)), bold)
+                         float(L.vxb_result_exchange_wait_ms(h)), bold, vcounts)
+
+    def _bold(self, steps: int) -> np.ndarray:
+        n = int(self._lib.vxb_result_bold_size(self._h))
+        bold = np.zeros(n, np.float64)
+        if n:
+            self._lib.vxb_result_bold(self._h, ptr(bold), n)
+        return bold.reshape(-1, self._n_voxels) if self._n_voxels else bold
 
     def set_hemodynamics(self, params: HemoParams | None = None, baseline_hz: float = 1.0,
                          sample_every: int = 1, state: np.ndarray | None = None) -> None:

@@ -1127,6 +1127,7 @@ class DistributedSimInstance(SimInstance):
         self._units = net.arrays["units"].copy()
         self._n_voxels = len(net.layout.voxels)
         self._hemo_every = 0
+        self._all_gather = all_gather
         self.rank, self.world = rank, world
         spec = net.spec()
         opt, keep = options._descriptor()
@@ -1158,6 +1159,22 @@ class DistributedSimInstance(SimInstance):
             if rc:
                 self._err(rc)
             barrier()
+
+    def advance(self, steps: int, fetch: bool = True):
+        """Collective advance.  With the BOLD readout on, the ranks add their
+        voxel counts (each holds its own units' spikes) and every rank runs
+        the hemodynamics on the totals (vxb_hemo_feed_counts)."""
+        if not (self._hemo_every and self.world > 1):
+            return super().advance(steps, fetch)
+        r = super().advance(steps, fetch=True)
+        parts = self._all_gather(r.voxel_counts)
+        tot = np.ascontiguousarray(np.sum(np.stack(parts), axis=0, dtype=np.uint64)
+                                   .astype(np.uint32))
+        rc = self._lib.vxb_hemo_feed_counts(self._h, ptr(tot), steps)
+        if rc != 0:
+            self._err(rc)
+        r.voxel_counts, r.bold = tot, self._bold(steps)
+        return r if fetch else None
 
 
 # ------------------------------------------------- benchmark network shapes

@@ -21,7 +21,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from paper_2308_01241_b200 import netgen  # noqa: E402
-from paper_2308_01241_b200.engine import SimOptions  # noqa: E402
+from paper_2308_01241_b200.engine import HemoParams, SimOptions  # noqa: E402
 
 
 def main():
@@ -40,6 +40,8 @@ def main():
     probes = [17, 5000, net.total_neurons - 1]
     opt = SimOptions(steps=steps, dt_ms=cfg["dt_ms"], probe_gids=probes, device=local)
     sim = netgen.DistributedSimInstance(net, opt, rank, world)
+    # BOLD readout across ranks: voxel counts summed, hemodynamics on the totals
+    sim.set_hemodynamics(HemoParams(), baseline_hz=10.0, sample_every=50)
     r1 = sim.advance(steps // 3)
     r2 = sim.advance(steps - steps // 3)
     snap = sim.membrane_snapshot(rank)
@@ -52,6 +54,7 @@ def main():
         "pi": np.concatenate([np.stack([p.i_syn for p in r.probes]) for r in (r1, r2)], axis=1),
         "flops": {k: r1.flops[k] + r2.flops[k] for k in r1.flops},
         "snap": snap,
+        "bold": [r1.bold, r2.bold],
     }
     out = [None] * world
     dist.all_gather_object(out, mine)
@@ -73,8 +76,23 @@ def main():
         fl = {k: sum(o["flops"][k] for o in out) for k in out[0]["flops"]}
         ref_fl = {k: a.flops[k] + b.flops[k] for k in a.flops}
         snaps_ok = all(np.array_equal(out[w]["snap"], rs.membrane_snapshot(w)) for w in range(world))
+        # window_bold (assim.cpp:51-71) on the reference engine's rates
+        from refnet import ref_window_bold
+        units = net.arrays["units"]
+        vox_n = np.zeros(len(net.layout.voxels), np.uint64)
+        np.add.at(vox_n, units["voxel"].astype(np.int64), units["neurons"].astype(np.uint64))
+        st = np.tile([0.0, 1.0, 1.0, 1.0], (len(vox_n), 1))
+        ref_bold = [ref_window_bold(HemoParams(), x.rates, units["voxel"], vox_n,
+                                    cfg["dt_ms"] * 1e-3, 10.0, 50, st) for x in (a, b)]
+        bold_ok = all(np.array_equal(o["bold"][k], out[0]["bold"][k])
+                      for o in out for k in range(2))  # every rank holds the same series
+        for k in range(2):
+            g, r = out[0]["bold"][k], ref_bold[k]
+            bold_ok = bold_ok and g.shape == r.shape and \
+                float(np.max(np.abs(g - r))) <= 1e-12 * float(np.max(np.abs(r))) + 1e-15
         res = {
             "world": world, "spikes": len(raster), "ref_spikes": len(ref_raster),
+            "bold_equal": bool(bold_ok),
             "raster_equal": raster == ref_raster,
             "rates_equal": bool(np.array_equal(rates, np.concatenate([a.rates, b.rates], axis=1))),
             "probe_v_equal": bool(np.array_equal(pv, ref_pv)),

@@ -110,6 +110,11 @@ def test_engine_bold_readout_matches_reference_window_bold():
     rs = RefSim(net, opt)
     r1, r2 = rs.advance(200), rs.advance(200)
     assert np.array_equal(g1.rates.counts, r1.rates) and np.array_equal(g2.rates.counts, r2.rates)
+    for g, r in ((g1, r1), (g2, r2)):  # RateSeries::voxel_counts (stats.cpp:193-201)
+        vc = np.zeros((r.rates.shape[1], net.tables.n_voxels), np.uint32)
+        for u, unit in enumerate(units):
+            vc[:, unit["voxel"]] += r.rates[u]
+        assert np.array_equal(g.voxel_counts, vc)
     st = np.tile([0.0, 1.0, 1.0, 1.0], (net.tables.n_voxels, 1))
     b1 = ref_window_bold(HemoParams(), r1.rates, units["voxel"], vox_n, 1e-3, 10.0, 25, st)
     b2 = ref_window_bold(HemoParams(), r2.rates, units["voxel"], vox_n, 1e-3, 10.0, 25, st)

@@ -11,6 +11,8 @@ VARIANTS = {
     "t384m2dw4": {"VXB_THREADS": 384, "VXB_MINB": 2, "VXB_DWARPS": 4},
     "t512m2dw4": {"VXB_THREADS": 512, "VXB_MINB": 2, "VXB_DWARPS": 4},
     "t320m3": {"VXB_THREADS": 320, "VXB_MINB": 3},
+    "polsf": {"VXB_POL_STREAM": 0},  # synapse stream evict_first
+    "polkn": {"VXB_POL_KEEP": 1},    # pending evict_normal
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

@@ -278,7 +278,7 @@ struct Engine {
     DevBuf<uint32_t> d_blk;
     DevBuf<uint32_t> d_work;  // dynamic delivery chunk counters [2][blocks][world]
     bool dyn = false;
-    bool f_policy = false;    // neuron-state stream evict_first
+    uint32_t f_policy = 0;    // neuron-state stream: 0 evict_normal, 1 evict_first, 2 evict_last
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
@@ -659,8 +659,15 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
             CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, device));
             if (mx > 0) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx));
         }
-        const char* fp = std::getenv("VXB_FPOL");
-        f_policy = fp ? std::atoi(fp) != 0 : false;
+        // the update's state (v, j, i_ou, g: 40 B/neuron) is kept evict_last
+        // too when it fits in L2 beside both pending buffers (config 2: 72 MB,
+        // 75.3 -> 74.0 us/step; config 3's 1.4 GB would only thrash: 1.14 ->
+        // 1.20 ms); VXB_FPOL = 0/1/2 forces evict_normal / first / last
+        int l2 = 0;
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+        const uint64_t keep = (uint64_t)n * (40 + 2 * (packed ? 16 : 32));
+        f_policy = keep <= (uint64_t)l2 * 3 / 4 ? 2u : 0u;
+        if (const char* fp = std::getenv("VXB_FPOL")) f_policy = (uint32_t)std::atoi(fp);
     }
     CK(cudaStreamSynchronize(stream));
 }
@@ -1514,7 +1521,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     // 13, 6.2 at 1; config 2 on 2 GPUs: 2.44e11 events/s at 32, 2.37e11 at 1)
     a.ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
     if (const char* env = std::getenv("VXB_CHMAX")) a.ch_max = std::max(1, std::atoi(env));
-    a.f_policy = f_policy ? 1u : 0u;
+    a.f_policy = f_policy;
     {
         const char* ep = std::getenv("VXB_EARLY_PUBLISH");
         a.early_publish = ep ? (std::atoi(ep) != 0 ? 1u : 0u) : 0u;  // measured slower (config 2 at 4 GPUs 4.23e11 vs 4.72e11 events/s)

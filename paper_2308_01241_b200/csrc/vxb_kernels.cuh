@@ -179,7 +179,7 @@ struct StepArgs {
     uint32_t ch_max;    // dynamic delivery of local spikes: most spikes per chunk (1 for
                         // long rows: the phase's last chunk ends sooner, config 2 79.4 ->
                         // 77.9 us/step); peers' batches (short rows here) take up to 32
-    uint32_t f_policy;  // 1: neuron-state stream evict_first in L2
+    uint32_t f_policy;  // neuron-state stream in L2: 0 evict_normal, 1 evict_first, 2 evict_last
     // phase profile (VXB_PHASE_PROFILE): per (phase, CTA) globaltimer of the
     // end of this CTA's delivery and of its update, or null
     unsigned long long* prof;
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_syn = VXB_POL_STREAM == 0 ? pol_stream : policy_evict_normal();
     const uint64_t pol_keep = VXB_POL_KEEP == 0 ? policy_evict_last() : policy_evict_normal();
-    const uint64_t pol_f = a.f_policy ? pol_stream : policy_evict_normal();
+    const uint64_t pol_f = a.f_policy == 1 ? pol_stream : a.f_policy == 2 ? pol_keep : policy_evict_normal();
     // the update's read + zeroing of the pending buffer: kept in L2 for the
     // next phase's atomics when the buffer fits; evict-first when it is
     // L2-blocked, or the zeroed lines would displace the live block

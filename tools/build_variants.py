@@ -13,6 +13,7 @@ VARIANTS = {
     "t320m3": {"VXB_THREADS": 320, "VXB_MINB": 3},
     "polsf": {"VXB_POL_STREAM": 0},  # synapse stream evict_first
     "polkn": {"VXB_POL_KEEP": 1},    # pending evict_normal
+    "pf1": {"VXB_PREFETCH": 1},      # L2 prefetch of the update state two chunks ahead
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

@@ -14,6 +14,8 @@ VARIANTS = {
     "polsf": {"VXB_POL_STREAM": 0},  # synapse stream evict_first
     "polkn": {"VXB_POL_KEEP": 1},    # pending evict_normal
     "pf1": {"VXB_PREFETCH": 1},      # L2 prefetch of the update state two chunks ahead
+    "dw4": {"VXB_DWARPS": 4},        # 1 producer + 3 consumer warps per CTA
+    "dw2": {"VXB_DWARPS": 2},        # 1 producer + 1 consumer
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

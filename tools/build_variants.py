@@ -16,6 +16,10 @@ VARIANTS = {
     "pf1": {"VXB_PREFETCH": 1},      # L2 prefetch of the update state two chunks ahead
     "dw4": {"VXB_DWARPS": 4},        # 1 producer + 3 consumer warps per CTA
     "dw2": {"VXB_DWARPS": 2},        # 1 producer + 1 consumer
+    "s6": {"VXB_STAGES": 6},         # deeper bulk-copy ring
+    "s3": {"VXB_STAGES": 3},
+    "e1024": {"VXB_STAGE_E": 1024},  # larger stages
+    "e512": {"VXB_STAGE_E": 512},
 }
 if __name__ == "__main__":
     out = b.ROOT / "build" / "variants"

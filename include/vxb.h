@@ -388,6 +388,17 @@ int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double
                               uint32_t steps, uint32_t n_series, double dt_s,
                               uint32_t sample_every, vxb_hemo_state* state, double* out);
 
+/* ---- ensemble members (EnsembleMember, assim.hpp / assim.cpp:74-107) ------ */
+/* The assimilation caller runs `members` SimInstances of one network that
+ * differ only in the conductances set per window.  A member engine is built
+ * for the same network as `donor` (its tables as `net`, or its spec as
+ * `spec`: exactly one) on the donor's device, and views the donor's synapse
+ * tables — read-only during a run — instead of building its own (12 GB for
+ * config 2).  Neuron state, pending sums, conductances, BOLD state and results
+ * are the member's own.  The donor must outlive its members; one GPU only. */
+int vxb_create_member(const vxb_engine* donor, const vxb_network* net,
+                      const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out);
+
 /* ---- one-call convenience (run_simulation, engine.hpp:92-93) ------------- */
 /* Creates, advances `steps` and returns the engine holding the results. */
 int vxb_run_simulation(const vxb_network* net, const vxb_options* opt,

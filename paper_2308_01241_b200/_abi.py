@@ -158,7 +158,7 @@ EXPORTS = [
     "vxb_mask_out", "vxb_mask_in", "vxb_ipc_handle", "vxb_connect_peers",
     "vxb_result_exchange_wait_ms", "vxb_fnv1a", "vxb_set_hemodynamics", "vxb_hemo_get_state",
     "vxb_result_bold_size", "vxb_result_bold", "vxb_debug_bold_from_drive",
-    "vxb_result_voxel_counts", "vxb_hemo_feed_counts",
+    "vxb_result_voxel_counts", "vxb_hemo_feed_counts", "vxb_create_member",
 ]
 
 _lib = None
@@ -214,6 +214,7 @@ def _declare(lib):
         "vxb_result_bold": (C.c_int, [P, P, C.c_uint64]),
         "vxb_result_voxel_counts": (C.c_int, [P, P, C.c_uint64]),
         "vxb_hemo_feed_counts": (C.c_int, [P, P, C.c_uint32]),
+        "vxb_create_member": (C.c_int, [P, P, P, C.POINTER(Options), C.POINTER(P)]),
         "vxb_debug_bold_from_drive": (C.c_int, [C.c_int, C.POINTER(HemoParams), P, C.c_uint32,
                                                 C.c_uint32, C.c_double, C.c_uint32, P, P]),
     }

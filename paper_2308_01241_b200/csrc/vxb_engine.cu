@@ -65,14 +65,22 @@ template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    bool owned = true;  // false: a view of another engine's buffer (shared tables)
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p && owned) cudaFree(p);
         p = nullptr;
         n = 0;
+        owned = true;
+    }
+    void share(const DevBuf& o) {  // read-only view; o must outlive this
+        release();
+        p = o.p;
+        n = o.n;
+        owned = false;
     }
     void alloc(size_t count) {
         release();
@@ -282,6 +290,11 @@ struct Engine {
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
+    // ensemble members (assim.cpp's EnsembleMember on one device): the
+    // synapse tables are read-only during a run, so members view the donor's
+    // out-CSR instead of building their own (12 GB for config 2)
+    const Engine* donor = nullptr;
+    void share_tables(const Engine& d);
     std::vector<unsigned long long> gen_have_mask;  // dst masks of generated tables
     void advance(uint32_t steps);
     void run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps);
@@ -533,7 +546,9 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     d_isyn.zero(stream);
 
     // out-CSR + mask consistency
-    if (gen) {
+    if (donor) {
+        share_tables(*donor);
+    } else if (gen) {
         generate_csr(*gen);  // consistent by construction
     } else {
         build_csr(net);
@@ -619,7 +634,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
     setup_exchange();
-    build_blocks();
+    if (!donor) build_blocks();
     // dynamic chunks win on one device (+8% config 2, config 3 2.0 -> 1.5 s
     // per bio-s) and with peers when there is one block (config 2 at 4 GPUs
     // +4%); with peers and several L2 blocks the static deal measured better
@@ -1073,6 +1088,27 @@ void Engine::generate_csr(const vxb_netspec& spec) {
     if (n_src)
         CK(cudaMemcpyAsync(have_src.data(), d_keys.p, 8ull * n_src, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+}
+
+// A member engine views the donor's out-CSR, L2-block offsets and tallies;
+// its own load() built the neuron state from the same network, so only the
+// table sizes need to agree.
+void Engine::share_tables(const Engine& d) {
+    if (d.world != 1 || world != 1) throw ConfigError("ensemble members need a one-GPU donor");
+    if (d.device != device) throw ConfigError("ensemble members must run on the donor's device");
+    if (d.n != n || d.n_src != n_src || d.workers != workers || d.n_units != n_units)
+        throw ConfigError("ensemble member network does not match the donor's");
+    n_syn = d.n_syn;
+    packed = d.packed;
+    have_src = d.have_src;
+    d_off.share(d.d_off);
+    d_inner.share(d.d_inner);
+    d_tgt.share(d.d_tgt);
+    d_w.share(d.d_w);
+    d_blk.share(d.d_blk);
+    rows_sorted = d.rows_sorted;
+    n_blocks = d.n_blocks;
+    block_n = d.block_n;
 }
 
 // Exchange state: receive region (one slot per peer: ids[kSlots][n_h],
@@ -1866,6 +1902,38 @@ int vxb_create_generated(const vxb_netspec* spec, const vxb_options* opt, vxb_en
         g_gen_host = &h;
         e->eng.load(&h.net, opt, spec);
         g_gen_host = nullptr;
+    } catch (const std::exception& x) {
+        g_gen_host = nullptr;
+        g_create_error = x.what();
+        int rc = fail_code(x);
+        delete e;
+        return rc;
+    }
+    *out = e;
+    return VXB_OK;
+}
+
+int vxb_create_member(const vxb_engine* donor, const vxb_network* net,
+                      const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out) {
+    *out = nullptr;
+    auto* e = new vxb_engine();
+    try {
+        if (!donor) throw ConfigError("null donor engine");
+        if (!net == !spec) throw ConfigError("pass either the network tables or the spec");
+        e->eng.donor = &donor->eng;
+        if (spec) {
+            GenHost h;
+            build_gen_host(*spec, h);
+            g_gen_host = &h;
+            e->eng.load(&h.net, opt, nullptr);
+            g_gen_host = nullptr;
+        } else {
+            uint64_t syn = 0;
+            for (uint32_t w = 0; w < net->n_workers; ++w) syn += net->workers[w].n_synapses;
+            if (syn != donor->eng.n_syn)
+                throw ConfigError("ensemble member network does not match the donor's");
+            e->eng.load(net, opt, nullptr);
+        }
     } catch (const std::exception& x) {
         g_gen_host = nullptr;
         g_create_error = x.what();

@@ -254,6 +254,7 @@ class SimInstance:
         self._units = tables.units.copy()
         self._n_voxels = tables.n_voxels
         self._hemo_every = 0
+        self._tables = tables
         net, keep_net = tables._descriptor()
         opt, keep_opt = options._descriptor()
         h = C.c_void_p()
@@ -262,6 +263,29 @@ class SimInstance:
         if rc != 0:
             _raise(rc, self._lib.vxb_last_error(None).decode())
         self._h = h
+
+    def _member_args(self):
+        """(network descriptor, spec, keep-alive) for vxb_create_member."""
+        net, keep = self._tables._descriptor()
+        return C.byref(net), None, (net, keep)
+
+    def member(self, options: SimOptions | None = None) -> "SimInstance":
+        """An ensemble member (EnsembleMember, assim.cpp:74-80): a new
+        instance of the same network on the same GPU that views this
+        instance's synapse tables instead of building its own; its state,
+        conductances and results are its own.  It keeps this instance alive."""
+        opt = options or self._opt
+        net, spec, keep = self._member_args()
+        o, keep_opt = opt._descriptor()
+        h = C.c_void_p()
+        rc = self._lib.vxb_create_member(self._h, net, spec, C.byref(o), C.byref(h))
+        del keep, keep_opt
+        if rc != 0:
+            _raise(rc, self._lib.vxb_last_error(None).decode())
+        m = object.__new__(type(self))
+        m.__dict__.update({k: v for k, v in self.__dict__.items() if k not in ("_h", "_donor")})
+        m._opt, m._h, m._hemo_every, m._donor = opt, h, 0, self
+        return m
 
     def close(self):
         if getattr(self, "_h", None):

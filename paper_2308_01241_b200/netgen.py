@@ -1051,6 +1051,7 @@ class GeneratedSimInstance(SimInstance):
         self._units = net.arrays["units"].copy()
         self._n_voxels = len(net.layout.voxels)
         self._hemo_every = 0
+        self._net = net
         spec = net.spec()
         opt, keep = options._descriptor()
         h = C.c_void_p()
@@ -1060,6 +1061,10 @@ class GeneratedSimInstance(SimInstance):
             from .engine import _raise
             _raise(rc, self._lib.vxb_last_error(None).decode())
         self._h = h
+
+    def _member_args(self):
+        spec = self._net.spec()
+        return None, C.byref(spec), spec
 
 
 def generate_tables(net: BuiltNetwork, device: int = 0) -> NetworkTables:

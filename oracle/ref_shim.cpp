@@ -14,6 +14,7 @@
 #include "voxsim/config.hpp"
 #include "voxsim/connectome.hpp"
 #include "voxsim/engine.hpp"
+#include "voxsim/assim.hpp"
 #include "voxsim/hemo.hpp"
 #include "voxsim/layout.hpp"
 #include "voxsim/model.hpp"
@@ -459,6 +460,104 @@ int ref_window_bold(const double* p, const uint32_t* counts, uint32_t n_units, u
             }
         }
     });
+}
+
+// ---- assimilation (assim.cpp) -----------------------------------------------
+// d = {dt_ms, obs_noise_sd, inflation, min_spread, prior_sd, baseline_hz,
+//      divergence_factor, kappa, gamma, tau, alpha, e0, v0};
+// iv = {members, windows, window_steps, divergence_patience, seed};
+// tg = (unit, receptor) pairs.
+static AssimOptions assim_opts(const double* d, const int64_t* iv, const uint32_t* tg,
+                               uint32_t nt) {
+    AssimOptions o;
+    o.dt_ms = d[0];
+    o.obs_noise_sd = d[1];
+    o.inflation = d[2];
+    o.min_spread = d[3];
+    o.prior_sd = d[4];
+    o.baseline_hz = d[5];
+    o.divergence_factor = d[6];
+    o.hemo = hemo_params(d + 7);
+    o.members = static_cast<int>(iv[0]);
+    o.windows = static_cast<uint32_t>(iv[1]);
+    o.window_steps = static_cast<uint32_t>(iv[2]);
+    o.divergence_patience = static_cast<int>(iv[3]);
+    o.seed = static_cast<uint64_t>(iv[4]);
+    for (uint32_t k = 0; k < nt; ++k) o.targets.push_back({tg[2 * k], static_cast<int>(tg[2 * k + 1])});
+    return o;
+}
+// The population g_location / g_scale of a unit (layout.pop_of_unit).
+void ref_unit_pop(void* h, uint32_t unit, double* gloc, double* gscale) {
+    const PopulationSpec& ps = static_cast<RefNet*>(h)->layout.pop_of_unit(unit);
+    for (int r = 0; r < 4; ++r) {
+        gloc[r] = ps.g_location[r];
+        gscale[r] = ps.g_scale[r];
+    }
+}
+// assimilate (assim.cpp:181-299): stats[w] = {window, innovation_rms,
+// pearson_r, mean_spread, target_mean[nt]}; final = {mean[nt], spread[nt]}.
+int ref_assimilate(void* h, const double* observed, uint32_t n_win, uint32_t n_vox,
+                   const double* d, const int64_t* iv, const uint32_t* tg, uint32_t nt,
+                   double* stats, uint32_t* n_stats, double* final_ms, int* diverged,
+                   char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        RefNet* n = static_cast<RefNet*>(h);
+        std::vector<std::vector<double>> obs(n_win, std::vector<double>(n_vox));
+        for (uint32_t w = 0; w < n_win; ++w)
+            for (uint32_t v = 0; v < n_vox; ++v) obs[w][v] = observed[(size_t)w * n_vox + v];
+        AssimResult r = assimilate(n->tables, n->layout, obs, assim_opts(d, iv, tg, nt));
+        *n_stats = static_cast<uint32_t>(r.windows.size());
+        for (size_t w = 0; w < r.windows.size(); ++w) {
+            double* o = stats + w * (4 + nt);
+            o[0] = r.windows[w].window;
+            o[1] = r.windows[w].innovation_rms;
+            o[2] = r.windows[w].pearson_r;
+            o[3] = r.windows[w].mean_spread;
+            for (uint32_t k = 0; k < nt; ++k) o[4 + k] = r.windows[w].target_mean[k];
+        }
+        for (uint32_t k = 0; k < nt; ++k) {
+            final_ms[k] = r.final_mean[k];
+            final_ms[nt + k] = r.final_spread[k];
+        }
+        *diverged = r.diverged ? static_cast<int>(r.diverged_window) + 1 : 0;
+    });
+}
+// run_forward_bold (assim.cpp:301-326): out[window][voxel].
+int ref_forward_bold(void* h, const double* d, const int64_t* iv, const uint32_t* tg,
+                     uint32_t nt, uint32_t windows, const double* true_params, double* out,
+                     char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        RefNet* n = static_cast<RefNet*>(h);
+        std::vector<double> tp;
+        if (true_params) tp.assign(true_params, true_params + nt);
+        auto b = run_forward_bold(n->tables, n->layout, assim_opts(d, iv, tg, nt), windows,
+                                  true_params ? &tp : nullptr);
+        size_t k = 0;
+        for (const auto& row : b)
+            for (double x : row) out[k++] = x;
+    });
+}
+
+// EnsrfUpdate::apply (assim.cpp:108-179): ens[m][p] in/out, fc[m][q], obs[q].
+int ref_ensrf(double* ens, const double* fc, const double* obs, uint32_t m, uint32_t p,
+              uint32_t q, double obs_var, double inflation, double min_spread, char* err,
+              int errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<std::vector<double>> e(m, std::vector<double>(p)), f(m, std::vector<double>(q));
+        for (uint32_t i = 0; i < m; ++i) {
+            for (uint32_t c = 0; c < p; ++c) e[i][c] = ens[(size_t)i * p + c];
+            for (uint32_t o = 0; o < q; ++o) f[i][o] = fc[(size_t)i * q + o];
+        }
+        EnsrfUpdate::apply(e, f, std::vector<double>(obs, obs + q), obs_var, inflation, min_spread);
+        for (uint32_t i = 0; i < m; ++i)
+            for (uint32_t c = 0; c < p; ++c) ens[(size_t)i * p + c] = e[i][c];
+    });
+}
+// sample_conductances (netgen.cpp:318-329).
+void ref_sample_conductances(uint64_t seed, uint64_t salt, uint32_t unit, int receptor,
+                             double location, double scale, uint32_t count, float* out) {
+    std::vector<float> v = sample_conductances(seed, salt, unit, receptor, location, scale, count);
+    std::copy(v.begin(), v.end(), out);
 }
 
 } // extern "C"

@@ -92,6 +92,18 @@ def sample_conductances(seed: int, salt: int, unit: int, receptor: int, location
     return np.exp(location + scale * stream_normal_array(base, count)).astype(np.float32)
 
 
+def sample_conductances_exact(seed: int, salt: int, unit: int, receptor: int,
+                              location: float, scale: float, count: int) -> np.ndarray:
+    """sample_conductances (netgen.cpp:318-329) with glibc's log/cos/exp
+    (Python's math): the reference's values bit for bit.  Scalar — for the
+    per-window conductances of the assimilation loop (assim.py)."""
+    base = mix_key(mix_key(seed, RNG_CONDUCTANCE, salt), unit, receptor)
+    out = np.empty(count, np.float32)
+    for i in range(count):
+        out[i] = math.exp(location + scale * stream_normal(base, i))
+    return out
+
+
 def stream_below(base: int, k: int, n: int) -> int:
     return stream_word(base, k) % n
 

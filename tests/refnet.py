@@ -92,6 +92,14 @@ def ref_lib():
                                               C.c_int]),
             "ref_window_bold": (C.c_int, [P, P, u32, u32, P, u32, P, C.c_double, C.c_double,
                                           u32, P, P, C.c_char_p, C.c_int]),
+            "ref_unit_pop": (None, [P, u32, P, P]),
+            "ref_assimilate": (C.c_int, [P, P, u32, u32, P, P, P, u32, P, P, P, P, C.c_char_p,
+                                         C.c_int]),
+            "ref_forward_bold": (C.c_int, [P, P, P, P, u32, u32, P, P, C.c_char_p, C.c_int]),
+            "ref_ensrf": (C.c_int, [P, P, P, u32, u32, u32, C.c_double, C.c_double, C.c_double,
+                                    C.c_char_p, C.c_int]),
+            "ref_sample_conductances": (None, [u64, u64, u32, C.c_int, C.c_double, C.c_double,
+                                               u32, P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -433,4 +441,73 @@ def ref_window_bold(params, counts, unit_voxel, vox_n, dt_s, baseline_hz, sample
                            err, 1024)
     if rc:
         _raise(rc, _strip(err.value.decode()))
+    return out
+
+
+# ---------------------------------------------------------- assimilation
+def _assim_args(opts):
+    h = opts.hemo
+    d = np.array([opts.dt_ms, opts.obs_noise_sd, opts.inflation, opts.min_spread, opts.prior_sd,
+                  opts.baseline_hz, opts.divergence_factor, h.kappa, h.gamma, h.tau, h.alpha,
+                  h.e0, h.v0], np.float64)
+    iv = np.array([opts.members, opts.windows, opts.window_steps, opts.divergence_patience,
+                   opts.seed], np.int64)
+    tg = np.array([[t.unit, t.receptor] for t in opts.targets], np.uint32).reshape(-1)
+    return d, iv, tg
+
+
+def ref_unit_pop(net, unit):
+    """(g_location[4], g_scale[4]) of the unit's population (layout.pop_of_unit)."""
+    gl, gs = np.zeros(4), np.zeros(4)
+    ref_lib().ref_unit_pop(net._h, unit, ptr(gl), ptr(gs))
+    return gl, gs
+
+
+def ref_assimilate(net, observed, opts):
+    """The reference's assimilate (assim.cpp:181-299) on a RefNet."""
+    L = ref_lib()
+    obs = np.ascontiguousarray(observed, np.float64)
+    d, iv, tg = _assim_args(opts)
+    nt = len(opts.targets)
+    stats = np.zeros((obs.shape[0], 4 + nt))
+    fin = np.zeros(2 * nt)
+    ns, div = C.c_uint32(0), C.c_int(0)
+    err = C.create_string_buffer(1024)
+    rc = L.ref_assimilate(net._h, ptr(obs), obs.shape[0], obs.shape[1], ptr(d), ptr(iv), ptr(tg),
+                          nt, ptr(stats), C.byref(ns), ptr(fin), C.byref(div), err, 1024)
+    if rc:
+        _raise(rc, _strip(err.value.decode()))
+    return stats[:ns.value], fin[:nt], fin[nt:], div.value
+
+
+def ref_forward_bold(net, opts, windows, true_params=None):
+    L = ref_lib()
+    d, iv, tg = _assim_args(opts)
+    tp = None if true_params is None else np.ascontiguousarray(true_params, np.float64)
+    out = np.zeros((windows, net.tables.n_voxels))
+    err = C.create_string_buffer(1024)
+    rc = L.ref_forward_bold(net._h, ptr(d), ptr(iv), ptr(tg), len(opts.targets), windows,
+                            ptr(tp), ptr(out), err, 1024)
+    if rc:
+        _raise(rc, _strip(err.value.decode()))
+    return out
+
+
+def ref_ensrf(ensemble, forecasts, obs, obs_var, inflation, min_spread):
+    """EnsrfUpdate::apply (assim.cpp:108-179); returns the updated ensemble."""
+    e = np.ascontiguousarray(ensemble, np.float64).copy()
+    f = np.ascontiguousarray(forecasts, np.float64)
+    o = np.ascontiguousarray(obs, np.float64)
+    err = C.create_string_buffer(1024)
+    rc = ref_lib().ref_ensrf(ptr(e), ptr(f), ptr(o), e.shape[0], e.shape[1], o.size, obs_var,
+                             inflation, min_spread, err, 1024)
+    if rc:
+        _raise(rc, _strip(err.value.decode()))
+    return e
+
+
+def ref_sample_conductances(seed, salt, unit, receptor, location, scale, count):
+    out = np.zeros(count, np.float32)
+    ref_lib().ref_sample_conductances(seed, salt, unit, receptor, location, scale, count,
+                                      ptr(out))
     return out

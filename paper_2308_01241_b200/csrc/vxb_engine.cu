@@ -286,6 +286,7 @@ struct Engine {
     DevBuf<uint32_t> d_blk;
     DevBuf<uint32_t> d_work;  // dynamic delivery chunk counters [2][blocks][world]
     bool dyn = false;
+    uint32_t stage_e = 0;     // delivery ring entries per stage
     uint32_t f_policy = 0;    // neuron-state stream: 0 evict_normal, 1 evict_first, 2 evict_last
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
@@ -644,8 +645,12 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
 
     // cooperative grid
     use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg && npset <= (uint32_t)kMaxSmemPset;
+    // bigger stages for L2-blocked delivery (short block segments per row)
+    stage_e = n_blocks > 1 ? 1024u : (uint32_t)kStageE;
+    if (const char* env = std::getenv("VXB_STAGE_ENTRIES"))
+        stage_e = (uint32_t)std::max(64, std::atoi(env));
     smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u,
-                            use_smem_seg ? npset : 0u).total;
+                            use_smem_seg ? npset : 0u, stage_e).total;
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const void* kfn = packed ? (const void*)step_kernel<true> : (const void*)step_kernel<false>;
@@ -1551,6 +1556,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     d_work.zero(stream);
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
+    a.stage_e = stage_e;
     // chunks of one local spike on one GPU when a row segment averages >= 512
     // entries (in-degree per L2 block; config 2: 1000), else up to 32
     // (config 3's short L2-block segments: 1.14 ms per step at 32, 1.31 ms at

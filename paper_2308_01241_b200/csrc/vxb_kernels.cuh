@@ -176,6 +176,7 @@ struct StepArgs {
     // works on one L2 block at a time and balances itself (dyn != 0)
     uint32_t* work_ctr;
     uint32_t dyn;
+    uint32_t stage_e;   // delivery ring: synapse entries per stage (SmemLayout)
     uint32_t ch_max;    // dynamic delivery of local spikes: most spikes per chunk (1 for
                         // long rows: the phase's last chunk ends sooner, config 2 79.4 ->
                         // 77.9 us/step); peers' batches (short rows here) take up to 32
@@ -336,9 +337,7 @@ static_assert(VXB_DWARPS >= 2, "delivery needs a producer warp and >= 1 consumer
 #define VXB_STAGE_E 768
 #endif
 constexpr int kStages = VXB_STAGES;   // delivery pipeline depth (bulk copies in flight)
-constexpr int kStageE = VXB_STAGE_E;  // synapse entries per stage
-constexpr int kStageTgtBytes = (kStageE + 8) * 4;
-constexpr int kStageWBytes = (kStageE + 4) * 8;
+constexpr int kStageE = VXB_STAGE_E;  // synapse entries per stage (default; see SmemLayout)
 
 // Stage metadata: the producer packs up to kSegPerStage row segments into
 // one stage of the delivery ring.
@@ -355,12 +354,19 @@ struct TStageMeta {
 constexpr uint32_t kMetaBytes = sizeof(TStageMeta);
 
 // Dynamic shared memory carve-up of step_kernel.
+// The stage size (entries) is chosen per launch: 1024 for L2-blocked
+// networks (config 3: 1094 vs 1126 us/step), kStageE otherwise (config 2).
 struct SmemLayout {
+    uint32_t se, tb, wb;  // entries per stage, target / weight bytes per stage
     uint32_t tgt, w, bar, meta, pset, seg, start, spk, total;
-    __host__ __device__ SmemLayout(uint32_t nseg_smem, uint32_t npset_smem) {
+    __host__ __device__ SmemLayout(uint32_t nseg_smem, uint32_t npset_smem,
+                                   uint32_t stage_e = kStageE) {
+        se = stage_e;
+        tb = (se + 8) * 4;
+        wb = (se + 4) * 8;
         tgt = 0;
-        w = tgt + kStages * kStageTgtBytes;
-        bar = w + kStages * kStageWBytes;
+        w = tgt + kStages * tb;
+        bar = w + kStages * wb;
         meta = bar + 2 * kStages * 8;  // full barriers, then empty barriers
         pset = (meta + kStages * kMetaBytes + 127) & ~127u;
         seg = pset + npset_smem * (uint32_t)sizeof(ParamSet);
@@ -510,7 +516,7 @@ struct StageBuilder {
                                         uint64_t b0, uint64_t len, uint64_t pol) {
         while (len) {
             if (!open) begin(smem, L);
-            const int room_t = kStageE - (int)toff, room_w = kStageE - 4 - (int)woff + 4;
+            const int room_t = (int)L.se - (int)toff, room_w = (int)L.se - 4 - (int)woff + 4;
             int room = room_t < room_w ? room_t : room_w;
             if (ns == (uint32_t)kSegPerStage || room <= 0) {
                 commit(smem, L, 0);
@@ -528,8 +534,8 @@ struct StageBuilder {
             m->wb[ns] = woff + (uint32_t)(b0 - w0);
             uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
             mbar_expect_tx_only(full, tn * 4 + wn * 8);
-            bulk_g2s(smem + L.tgt + st * kStageTgtBytes + toff * 4, a.tgt + t0, tn * 4, full, pol);
-            bulk_g2s(smem + L.w + st * kStageWBytes + woff * 8, a.w + w0, wn * 8, full, pol);
+            bulk_g2s(smem + L.tgt + st * L.tb + toff * 4, a.tgt + t0, tn * 4, full, pol);
+            bulk_g2s(smem + L.w + st * L.wb + woff * 8, a.w + w0, wn * 8, full, pol);
             total += (uint32_t)take;
             toff += tn;
             woff += wn;
@@ -568,7 +574,7 @@ struct StageBuilder {
                         begin(smem, L);
                         ++touched;
                     }
-                    const int room_t = kStageE - (int)toff, room_w = kStageE - (int)woff;
+                    const int room_t = (int)L.se - (int)toff, room_w = (int)L.se - (int)woff;
                     const int room = room_t < room_w ? room_t : room_w;
                     const uint32_t st = ctr % kStages;
                     TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
@@ -615,9 +621,9 @@ struct StageBuilder {
                 const uint32_t st = S.pst[q];
                 uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
                 mbar_expect_tx_only(full, tn * 4 + wn * 8);
-                bulk_g2s(smem + L.tgt + st * kStageTgtBytes + S.ptoff[q] * 4, a.tgt + t0, tn * 4,
+                bulk_g2s(smem + L.tgt + st * L.tb + S.ptoff[q] * 4, a.tgt + t0, tn * 4,
                          full, pol);
-                bulk_g2s(smem + L.w + st * kStageWBytes + S.pwoff[q] * 8, a.w + w0, wn * 8, full,
+                bulk_g2s(smem + L.w + st * L.wb + S.pwoff[q] * 8, a.w + w0, wn * 8, full,
                          pol);
             }
             __syncwarp();
@@ -725,7 +731,7 @@ __device__ __forceinline__ void load_neuron(const StepArgs& a, uint32_t i, bool 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u, a.use_smem_seg ? a.npset : 0u);
+    const SmemLayout L(a.use_smem_seg ? a.nseg : 0u, a.use_smem_seg ? a.npset : 0u, a.stage_e);
     ParamSet* s_pset = reinterpret_cast<ParamSet*>(smem + L.pset);
     SegInfo* s_seg = reinterpret_cast<SegInfo*>(smem + L.seg);
     uint32_t* s_start = reinterpret_cast<uint32_t*>(smem + L.start);
@@ -971,8 +977,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                     ++g_item;
                     const TStageMeta* m = reinterpret_cast<const TStageMeta*>(s_meta_base + st * kMetaBytes);
                     const uint32_t n_e = m->n, last = m->end;
-                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * kStageTgtBytes);
-                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * kStageWBytes);
+                    const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * L.tb);
+                    const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * L.wb);
                     uint32_t sg = 0;
                     for (uint32_t e = ct; e < n_e; e += cn) {
                         while (e >= m->pre[sg + 1]) ++sg;

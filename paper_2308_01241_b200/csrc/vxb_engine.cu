@@ -1224,10 +1224,22 @@ void Engine::build_blocks() {
     n_blocks = 1;
     dyn = false;
     const uint64_t pend_per = packed ? 16 : 32;
-    uint64_t bn = (64ull << 20) / pend_per;
+    // every rank delivers in the same number of block passes (a rank with one
+    // pass more sets the pace of the whole exchange): count from the largest shard
+    uint64_t n_ref = n;
+    if (world > 1)
+        for (uint32_t w = 0; w < workers; ++w)
+            n_ref = std::max<uint64_t>(n_ref, src_base[w + 1] - src_base[w]);
+    // 64 MB blocks; 80 MB once that would take 6+ passes, where the per-pass
+    // cost of every spike's row lookup outweighs the L2 misses of the larger
+    // block (half of config 5, 25M neurons per GPU at 15 Hz: 2.56e11 ->
+    // 2.91e11 events/s; config 3's 5-10M per GPU stay faster at 64 MB)
+    uint64_t mb = ((n_ref * pend_per + (64ull << 20) - 1) / (64ull << 20)) >= 6 ? 80 : 64;
+    if (const char* env = std::getenv("VXB_BLOCK_MB")) mb = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+    uint64_t bn = (mb << 20) / pend_per;
     if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
-    if ((uint64_t)n <= bn || n_syn == 0) return;
-    n_blocks = (uint32_t)((n + bn - 1) / bn);
+    if (n_ref <= bn || n_syn == 0) return;
+    n_blocks = (uint32_t)((n_ref + bn - 1) / bn);
     block_n = (uint32_t)((n + n_blocks - 1) / n_blocks);
     sort_rows();
     d_blk.alloc((size_t)n_src * (n_blocks + 1));

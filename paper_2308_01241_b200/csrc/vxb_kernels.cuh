@@ -331,6 +331,9 @@ static_assert(VXB_DWARPS >= 2, "delivery needs a producer warp and >= 1 consumer
 // config 3 1142 -> 1133 us/step)
 #define VXB_PREFETCH 0
 #endif
+#ifndef VXB_DEPTH3
+#define VXB_DEPTH3 0  // 1: update state loaded two chunks ahead (three register sets)
+#endif
 #ifndef VXB_STAGES
 #define VXB_STAGES 4
 #endif
@@ -1040,13 +1043,30 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             prefetch(chn);
             uint32_t i = c_lo + (ch << 5) + lane;
             if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, i < keep_hi ? pol_keep : pol_f0, pol_pz);
+#if VXB_DEPTH3
+            NIn<PACKED> nx2;
+            {
+                const uint32_t i1 = c_lo + (chn << 5) + lane;
+                if (chn < nch && i1 < c_hi)
+                    load_neuron<PACKED>(a, i1, doE, pend_rd, nxt, i1 < keep_hi ? pol_keep : pol_f0, pol_pz);
+            }
+#endif
             while (ch < nch) {
                 const uint32_t chn2 = grab();
                 prefetch(chn2);
                 const uint32_t inext = c_lo + (chn << 5) + lane;
+#if VXB_DEPTH3
+                {
+                    const uint32_t i2 = c_lo + (chn2 << 5) + lane;
+                    if (chn2 < nch && i2 < c_hi)
+                        load_neuron<PACKED>(a, i2, doE, pend_rd, nx2, i2 < keep_hi ? pol_keep : pol_f0,
+                                          pol_pz);
+                }
+#else
                 if (chn < nch && inext < c_hi)
                     load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, inext < keep_hi ? pol_keep : pol_f0,
                                       pol_pz);
+#endif
                 const bool live = i < c_hi;
                 const uint64_t pol_f = i < keep_hi ? pol_keep : pol_f0;
                 bool spiked = false;
@@ -1192,6 +1212,9 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 if (a.world > 1 && __any_sync(0xffffffffu, overflow_route))
                     if (exchange_route(a, i, overflow_route, tA % kSlots)) __threadfence_system();
                 cur = nxt;
+#if VXB_DEPTH3
+                nxt = nx2;
+#endif
                 ch = chn;
                 chn = chn2;
                 i = inext;

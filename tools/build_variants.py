@@ -20,6 +20,9 @@ VARIANTS = {
     "s3": {"VXB_STAGES": 3},
     "e1024": {"VXB_STAGE_E": 1024},  # larger stages
     "e512": {"VXB_STAGE_E": 512},
+    "m2": {"VXB_MINB": 2},           # register cap lifted (2 CTAs/SM)
+    "d3": {"VXB_DEPTH3": 1},         # update state two chunks ahead in registers
+    "d3m2": {"VXB_DEPTH3": 1, "VXB_MINB": 2},  # same, register cap lifted (2 CTAs/SM)
     # diagnostic, not parity-preserving: cost of the OU noise in the update
     "xifast": {"VXB_XI_FAST_ONLY": 1},  # fp64 Box-Muller without the correct-rounding check
     "xizero": {"VXB_XI_ZERO": 1},       # no noise at all

@@ -288,7 +288,6 @@ struct Engine {
     bool dyn = false;
     uint32_t stage_e = 0;     // delivery ring entries per stage
     uint32_t f_policy = 0;    // neuron-state stream: 0 evict_normal, 1 evict_first, 2 evict_last
-    uint32_t f_keep_cta = 0;  // partial residency: neurons per CTA kept evict_last
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
     void generate_csr(const vxb_netspec& spec);
@@ -689,10 +688,6 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         const uint64_t keep = (uint64_t)n * (40 + 2 * (packed ? 16 : 32));
         f_policy = keep <= (uint64_t)l2 * 3 / 4 ? 2u : 0u;
         if (const char* fp = std::getenv("VXB_FPOL")) f_policy = (uint32_t)std::atoi(fp);
-        // VXB_FKEEP = neurons (over the whole shard) whose state stays
-        // evict_last when the rest streams: the first of each CTA's range
-        if (const char* fk = std::getenv("VXB_FKEEP"))
-            f_keep_cta = (uint32_t)((std::strtoull(fk, nullptr, 10) / (uint64_t)grid) & ~31ull);
     }
     CK(cudaStreamSynchronize(stream));
 }
@@ -1581,7 +1576,6 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
     if (const char* env = std::getenv("VXB_CHMAX")) a.ch_max = std::max(1, std::atoi(env));
     a.f_policy = f_policy;
-    a.f_keep_cta = f_keep_cta;
     {
         const char* ep = std::getenv("VXB_EARLY_PUBLISH");
         a.early_publish = ep ? (std::atoi(ep) != 0 ? 1u : 0u) : 0u;  // measured slower (config 2 at 4 GPUs 4.23e11 vs 4.72e11 events/s)

@@ -181,7 +181,6 @@ struct StepArgs {
                         // long rows: the phase's last chunk ends sooner, config 2 79.4 ->
                         // 77.9 us/step); peers' batches (short rows here) take up to 32
     uint32_t f_policy;  // neuron-state stream in L2: 0 evict_normal, 1 evict_first, 2 evict_last
-    uint32_t f_keep_cta;  // first neurons of each CTA's range kept evict_last (multiple of 32)
     // phase profile (VXB_PHASE_PROFILE): per (phase, CTA) globaltimer of the
     // end of this CTA's delivery and of its update, or null
     unsigned long long* prof;
@@ -794,10 +793,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_syn = VXB_POL_STREAM == 0 ? pol_stream : policy_evict_normal();
     const uint64_t pol_keep = VXB_POL_KEEP == 0 ? policy_evict_last() : policy_evict_normal();
-    const uint64_t pol_f0 = a.f_policy == 1 ? pol_stream : a.f_policy == 2 ? pol_keep : policy_evict_normal();
-    // partial residency: the CTA's first f_keep_cta neurons stay evict_last
-    // (chunks are 32-aligned from c_lo, so the choice is warp-uniform)
-    const uint32_t keep_hi = min(c_hi, c_lo + a.f_keep_cta);
+    const uint64_t pol_f = a.f_policy == 1 ? pol_stream : a.f_policy == 2 ? pol_keep : policy_evict_normal();
     // the update's read + zeroing of the pending buffer: kept in L2 for the
     // next phase's atomics when the buffer fits; evict-first when it is
     // L2-blocked, or the zeroed lines would displace the live block
@@ -1042,13 +1038,13 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             uint32_t chn = grab();
             prefetch(chn);
             uint32_t i = c_lo + (ch << 5) + lane;
-            if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, i < keep_hi ? pol_keep : pol_f0, pol_pz);
+            if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, pol_f, pol_pz);
 #if VXB_DEPTH3
             NIn<PACKED> nx2;
             {
                 const uint32_t i1 = c_lo + (chn << 5) + lane;
                 if (chn < nch && i1 < c_hi)
-                    load_neuron<PACKED>(a, i1, doE, pend_rd, nxt, i1 < keep_hi ? pol_keep : pol_f0, pol_pz);
+                    load_neuron<PACKED>(a, i1, doE, pend_rd, nxt, pol_f, pol_pz);
             }
 #endif
             while (ch < nch) {
@@ -1059,16 +1055,13 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 {
                     const uint32_t i2 = c_lo + (chn2 << 5) + lane;
                     if (chn2 < nch && i2 < c_hi)
-                        load_neuron<PACKED>(a, i2, doE, pend_rd, nx2, i2 < keep_hi ? pol_keep : pol_f0,
-                                          pol_pz);
+                        load_neuron<PACKED>(a, i2, doE, pend_rd, nx2, pol_f, pol_pz);
                 }
 #else
                 if (chn < nch && inext < c_hi)
-                    load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, inext < keep_hi ? pol_keep : pol_f0,
-                                      pol_pz);
+                    load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, pol_f, pol_pz);
 #endif
                 const bool live = i < c_hi;
-                const uint64_t pol_f = i < keep_hi ? pol_keep : pol_f0;
                 bool spiked = false;
                 // parameter segment: warp-uniform cached range, a galloping
                 // search when the chunk leaves it, a per-lane walk only for

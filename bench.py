@@ -217,7 +217,7 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
+    ref = CpuReference(args.cpu_voxels, args.cpu_workers or os.cpu_count() or 1)
     # size each bench step so the whole warmup + steps run takes about
     # --cpu-budget-s on this host (host core counts differ between boxes)
     e0, s0, _ = ref.step(200)
@@ -403,7 +403,7 @@ def run_b200(args):
     }
     if not args.no_cpu and args.workload == "config2":
         try:
-            ref = CpuReference(args.cpu_voxels, os.cpu_count() or 1)
+            ref = CpuReference(args.cpu_voxels, args.cpu_workers or os.cpu_count() or 1)
             _, s0, _ = ref.step(300)  # warm-up + rate probe: ~cpu_sample_seconds of sample
             n_s = int(min(args.cpu_sample_steps,
                           max(500, args.cpu_sample_seconds / max(s0 / 300, 1e-9))))
@@ -439,6 +439,8 @@ def main():
                     help="cpu_baseline of the B200 arm: target wall time of the sample")
     ap.add_argument("--cpu-budget-s", type=float, default=150.0,
                     help="--impl reference: target wall time of warmup + steps")
+    ap.add_argument("--cpu-workers", type=int, default=0,
+                    help="reference engine workers (0: one per host core, at most 2 per sample voxel)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4"])
     ap.add_argument("--rate", type=int, default=10, choices=[7, 10, 15, 30],

@@ -77,11 +77,81 @@ def dti_cfg(workers=1, rate=10, dt_ms=1.0, total=20_000_000):
                                       "ou_mean": ou}}}
 
 
+def config5_cfg(workers=1, dt_ms=1.0, per_gpu=25_000_000, rate=15):
+    """Config 5: the whole-box network, 1000-voxel DTI-like connectome with
+    lognormal voxel sizes, K = 500, ~15 Hz, 25M neurons per GPU (2e8 neurons
+    and 1e11 synapses on 8 GPUs, 150 GB of synapse table per GPU), greedy
+    partition under the B200 byte model.  Weak-scaled: --gpus N simulates
+    N x 25M neurons."""
+    from paper_2308_01241_b200 import netgen
+    total = per_gpu * workers
+    path = ROOT / "build" / f"dti1000_{total}.txt"
+    if not path.exists():
+        path.parent.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(f".{os.getpid()}.tmp")
+        netgen.write_connectome_file(
+            netgen.dti_like_connectome(voxels=1000, total_neurons=total), tmp)
+        os.replace(tmp, path)
+    ampa, ou = K500_POINTS[rate]
+    return {"seed": SEED, "dt_ms": dt_ms, "steps": 1000, "workers": workers,
+            "connectome": {"kind": "file", "path": str(path)},
+            "partition": {"method": "greedy", "byte_model": "b200"},
+            "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + G_LOC_10HZ[1:],
+                                      "ou_mean": ou}}}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def ensure_world(args) -> None:
+    """`--gpus N` means N ranks, one per GPU.  Launched by torchrun the world
+    size must match; launched bare with N > 1, re-launch this command under
+    torch.distributed.run (127.0.0.1 rendezvous) and exit with its status."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
+def host_cores() -> dict:
+    """Host CPU inventory for the CPU-baseline records: logical CPUs usable by
+    this process, and physical cores (distinct (package, core) pairs)."""
+    try:
+        logical = len(os.sched_getaffinity(0))
+    except AttributeError:
+        logical = os.cpu_count() or 1
+    phys = set()
+    try:
+        pkg = core = None
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("physical id"):
+                pkg = line.split(":")[1].strip()
+            elif line.startswith("core id"):
+                core = line.split(":")[1].strip()
+            elif not line.strip():
+                if core is not None:
+                    phys.add((pkg, core))
+                pkg = core = None
+        if core is not None:
+            phys.add((pkg, core))
+    except OSError:
+        pass
+    return {"nproc": logical, "physical_cores": len(phys) or None}
 
 
 class ClockSampler:
@@ -177,16 +247,16 @@ def measured_peak_hbm():
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """DRAM bytes per step-kernel launch from the committed ncu capture of
-    this command (profiles/), or None."""
-    p = ROOT / "profiles" / "step_kernel_traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            return None
-    return None
+def ncu_traffic(workload: str, ws: int, kernel: str):
+    """DRAM bytes per launch of `kernel` from a committed `ncu --set full`
+    capture of this same workload and GPU count (profiles/traffic.json:
+    {"<workload>/n<ws>/<kernel>": {"dram_bytes_per_launch": ...}}), else None."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        rec = json.loads(p.read_text()).get(f"{workload}/n{ws}/{kernel}")
+        return rec.get("dram_bytes_per_launch") if rec else None
+    except Exception:
+        return None
 
 
 class CpuReference:
@@ -217,7 +287,8 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    ref = CpuReference(args.cpu_voxels, args.cpu_workers or os.cpu_count() or 1)
+    hc = host_cores()
+    ref = CpuReference(args.cpu_voxels, args.cpu_workers or hc["nproc"])
     # size each bench step so the whole warmup + steps run takes about
     # --cpu-budget-s on this host (host core counts differ between boxes)
     e0, s0, _ = ref.step(200)
@@ -233,7 +304,8 @@ def run_reference(args):
     rate = spk / (ref.neurons * args.steps * args.cpu_steps * 1e-3)
     sample = (f"ring {args.cpu_voxels} voxels x 10000 neurons, K=1000, dt=1 ms, "
               f"{args.cpu_steps} steps per bench step, {ref.workers} workers "
-              f"(scheduler threads), {rate:.1f} Hz")
+              f"(scheduler threads: {ref.threads} engine threads on {hc['nproc']} CPUs), "
+              f"{rate:.1f} Hz")
     line = {"metric": "synaptic_events_per_s", "value": value, "unit": "events/s",
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
@@ -243,7 +315,9 @@ def run_reference(args):
                        "dt_ms": 1.0, "parallelism": f"cpu threads x{ref.threads}"},
             "wall_s_per_bio_s_extrapolated_1M": (sec / args.steps) / (args.cpu_steps * 1e-3)
             * (1e6 / ref.neurons),
-            "cpu_baseline": {"value": value, "unit": "events/s", "cores": ref.threads,
+            "cpu_baseline": {"value": value, "unit": "events/s", "cores": hc["nproc"],
+                             "nproc": hc["nproc"], "physical_cores": hc["physical_cores"],
+                             "engine_workers": ref.workers, "engine_threads": ref.threads,
                              "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -271,8 +345,12 @@ def run_b200(args):
         cfg = workload_cfg(voxels=100 * ws, dt_ms=args.dt, workers=ws)
         if ws > 1:
             cfg["partition"]["method"] = "sequential"
+    elif args.workload == "config5":  # weak scaling: 25M neurons per GPU, K = 500, 15 Hz
+        cfg = config5_cfg(workers=ws, dt_ms=args.dt, per_gpu=args.neurons or 25_000_000,
+                          rate=args.rate if args.rate != 10 else 15)
     else:  # config3 (10 Hz) / config4 rate sweep: strong scaling, 20M neurons
-        cfg = dti_cfg(workers=ws, rate=args.rate, dt_ms=args.dt, total=args.neurons)
+        cfg = dti_cfg(workers=ws, rate=args.rate, dt_ms=args.dt,
+                      total=args.neurons or 20_000_000)
     net = netgen.build_network(cfg)
     opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=True,
                      device=dev)
@@ -334,6 +412,7 @@ def run_b200(args):
             xwait += r.exchange_wait_ms
         barrier()
         t_all = time.perf_counter() - t_all
+    schedule = sim.schedule_info()
     sim.close()
     dev_s = sum(dev_ms) / 1e3
     wall_s = sum(wall)
@@ -360,24 +439,32 @@ def run_b200(args):
     # per advance and rank: one conductance-scatter launch (the staged
     # set_conductances) + the step kernel launch(es)
     launches_per = max(1, launches // max(1, args.steps * ws) - 1)
-    traffic = ncu_traffic()
+    if args.workload == "config2":
+        wl = "config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)"
+    elif args.workload == "config5":
+        wl = (f"config5 ({net.total_neurons} neurons, 1000-voxel DTI-like, K=500, "
+              f"{args.rate if args.rate != 10 else 15} Hz point)")
+    else:
+        wl = (f"{args.workload} (200-voxel DTI-like, {net.total_neurons} neurons, "
+              f"K=500, {args.rate} Hz point)")
+    kernel = schedule.get("kernel", "vxb::step_kernel")
+    traffic = ncu_traffic(args.workload, ws, kernel)
     line = {
         "metric": "synaptic_events_per_s", "value": value, "unit": "events/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak" if args.workload == "config2" else "strong",
+        "higher_is_better": True, "scaling": "weak" if args.workload in ("config2", "config5") else "strong",
         "vs_baseline": None,
         "dtype": "f32 state / i64 Q16 / f64 noise", "data": "synthetic",
-        "config": {"workload": (("config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)")
-                                if args.workload == "config2" else
-                                f"{args.workload} (200-voxel DTI-like, {args.neurons} neurons, "
-                                f"K=500, {args.rate} Hz point)"),
+        "config": {"workload": wl,
                    "neurons_per_gpu": net.total_neurons // ws,
                    "synapses_per_gpu": net.synapse_count // ws,
                    "k_in": 1000 if args.workload == "config2" else 500, "dt_ms": args.dt,
                    "bio_ms_per_step": args.bio_ms, "seed": SEED,
                    "parallelism": f"neuron shards x{ws}, NVLink spike exchange" if ws > 1
                    else "single",
-                   "l2": "inputs larger than L2 (12 GB synapse table)"},
+                   "l2": f"inputs larger than L2 ({12 * net.synapse_count / ws / 1e9:.0f} GB "
+                         "synapse table per GPU)",
+                   "schedule": schedule},
         "wall_s_per_bio_s": dev_s / bio_s,
         "exposed_exchange_us_per_step": 1e3 * xwait / (args.steps * bio_steps) if ws > 1 else 0.0,
         "mean_rate_hz": rate,
@@ -390,7 +477,7 @@ def run_b200(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "vxb::step_kernel",
+                     "kernel": kernel,
                      "alg_bytes_per_launch": alg_bytes / max(1, launches_per * args.steps),
                      "exchange": "4 B per (spike, destination GPU) over NVLink" if ws > 1 else None,
                      "model": "98 B/neuron-step + 12 B/event + 20 B/delivered spike"},
@@ -403,18 +490,23 @@ def run_b200(args):
     }
     if not args.no_cpu and args.workload == "config2":
         try:
-            ref = CpuReference(args.cpu_voxels, args.cpu_workers or os.cpu_count() or 1)
+            ref = CpuReference(args.cpu_voxels, args.cpu_workers or host_cores()["nproc"])
             _, s0, _ = ref.step(300)  # warm-up + rate probe: ~cpu_sample_seconds of sample
             n_s = int(min(args.cpu_sample_steps,
                           max(500, args.cpu_sample_seconds / max(s0 / 300, 1e-9))))
             args.cpu_sample_steps = n_s
             e, s, k = ref.step(n_s)
+            hc = host_cores()
             line["cpu_baseline"] = {
-                "value": e / s, "unit": "events/s", "cores": ref.threads, "kind": "reference",
+                "value": e / s, "unit": "events/s", "cores": hc["nproc"],
+                "nproc": hc["nproc"], "physical_cores": hc["physical_cores"],
+                "engine_workers": ref.workers, "engine_threads": ref.threads,
+                "kind": "reference",
                 "sample": f"ring {args.cpu_voxels}x10000 neurons, K=1000, {args.cpu_sample_steps} "
-                          f"steps, {ref.workers} workers (threads), "
+                          f"steps, {ref.workers} workers (scheduler threads: {ref.threads} "
+                          f"engine threads on {hc['nproc']} CPUs), "
                           f"{k / (ref.neurons * args.cpu_sample_steps * 1e-3):.1f} Hz, "
-                          f"{s:.1f} s wall on {ref.threads} threads"}
+                          f"{s:.1f} s wall"}
         except Exception as e:  # the checker is optional on the GPU arm
             line["cpu_baseline"] = {"value": None, "unit": "events/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
@@ -442,11 +534,14 @@ def main():
     ap.add_argument("--cpu-workers", type=int, default=0,
                     help="reference engine workers (0: one per host core, at most 2 per sample voxel)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="config2", choices=["config2", "config3", "config4"])
+    ap.add_argument("--workload", default="config2",
+                    choices=["config2", "config3", "config4", "config5"])
     ap.add_argument("--rate", type=int, default=10, choices=[7, 10, 15, 30],
                     help="config3/4 operating point (Hz)")
-    ap.add_argument("--neurons", type=int, default=20_000_000, help="config3/4 network size")
+    ap.add_argument("--neurons", type=int, default=0,
+                    help="config3/4 network size (default 20M); config5 neurons per GPU (25M)")
     args = ap.parse_args()
+    ensure_world(args)
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "reference":

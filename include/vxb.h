@@ -196,6 +196,9 @@ void vxb_destroy(vxb_engine* e);
  * vxb_create on this thread when e == NULL). */
 const char* vxb_last_error(const vxb_engine* e);
 int vxb_abi_version(void);
+/* SHA-256 prefix of the sources and flags this library was built from
+ * (paper_2308_01241_b200/build.py source_hash). */
+const char* vxb_build_hash(void);
 
 /* ---- stepping ------------------------------------------------------------ */
 /* Advances `steps` steps; results are kept inside the engine until the next
@@ -227,6 +230,11 @@ uint64_t vxb_result_h2d_bytes(const vxb_engine* e);
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e);
 /* Kernel launches issued by the last vxb_advance. */
 uint64_t vxb_result_launches(const vxb_engine* e);
+/* The delivery schedule chosen for this network as a JSON object (path, grid,
+ * L2 blocks, deal, stage size, ...) including every tuning knob applied from
+ * the environment (knobs are read only when VXB_TUNING=1).  No reference
+ * counterpart: benchmark bookkeeping. */
+int vxb_schedule_info(const vxb_engine* e, char* out, uint64_t cap);
 
 /* ---- state access -------------------------------------------------------- */
 int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor,
@@ -395,7 +403,9 @@ int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double
  * `spec`: exactly one) on the donor's device, and views the donor's synapse
  * tables — read-only during a run — instead of building its own (12 GB for
  * config 2).  Neuron state, pending sums, conductances, BOLD state and results
- * are the member's own.  The donor must outlive its members; one GPU only. */
+ * are the member's own.  The shared tables are reference-counted: they stay
+ * allocated until the donor and every member are destroyed, in any order.
+ * One GPU only. */
 int vxb_create_member(const vxb_engine* donor, const vxb_network* net,
                       const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out);
 

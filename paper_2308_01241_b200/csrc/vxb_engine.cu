@@ -61,31 +61,47 @@ struct HemoError : SimError {
 
 thread_local std::string g_create_error;
 
+// Tuning / diagnostic knobs.  They change the schedule (never the results),
+// so they are read only when VXB_TUNING=1 is set, and every knob applied is
+// recorded in the engine's schedule report (vxb_schedule_info) — a stray
+// value in the environment cannot change a run silently.
+const char* knob(const char* name, std::string* log) {
+    const char* on = std::getenv("VXB_TUNING");
+    if (!on || std::atoi(on) == 0) return nullptr;
+    const char* v = std::getenv(name);
+    if (v && log) *log += std::string(*log->c_str() ? "," : "") + "\"" + name + "\":\"" + v + "\"";
+    return v;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
-    bool owned = true;  // false: a view of another engine's buffer (shared tables)
+    // Reference-counted allocation: ensemble members view the donor's
+    // read-only tables (share), and the memory is freed only when the last
+    // engine holding it is destroyed, whatever the destruction order.
+    std::shared_ptr<void> mem;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { release(); }
     void release() {
-        if (p && owned) cudaFree(p);
+        mem.reset();
         p = nullptr;
         n = 0;
-        owned = true;
     }
-    void share(const DevBuf& o) {  // read-only view; o must outlive this
-        release();
+    void share(const DevBuf& o) {
+        mem = o.mem;
         p = o.p;
         n = o.n;
-        owned = false;
     }
     void alloc(size_t count) {
         release();
+        if (!count) return;
+        T* q = nullptr;
+        CK(cudaMalloc(&q, count * sizeof(T)));
+        mem = std::shared_ptr<void>(q, [](void* x) { cudaFree(x); });
+        p = q;
         n = count;
-        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
     }
     void reserve(size_t count) {  // grow-only: no free/sync when it already fits
         if (count > n) alloc(count);
@@ -188,6 +204,10 @@ struct Engine {
     std::vector<unsigned long long> have_src;  // per global source: workers holding targets here
     bool use_smem_seg = true;
     uint32_t smem_bytes = 0;
+    std::string knobs;  // tuning knobs applied (VXB_TUNING=1), JSON members
+    uint32_t ch_max = 1;
+    bool early_publish = false;
+    std::string schedule_info() const;
 
     // ---------------------------------------------------------- device
     cudaStream_t stream = nullptr;
@@ -214,6 +234,7 @@ struct Engine {
     DevBuf<uint32_t> d_forced_off, d_forced_local;
     DevBuf<uint32_t> d_inj_epoch;
     DevBuf<float> d_inj_table;
+    bool has_forced = false, has_inj = false;  // tables of the current advance
     DevBuf<unsigned long long> d_phase_ns;
     DevBuf<unsigned long long> d_phase_wait;
     double exchange_wait_ms = 0;  // last advance: sum over phases of the max CTA wait
@@ -436,18 +457,20 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     // shard-local layout and parameter segments
     wbase.assign(workers + 1, 0);
     src_base.assign(workers + 1, 0);
+    uint64_t wsum = 0, ssum = 0;  // 64-bit sums, checked before narrowing
     for (uint16_t wi = 0; wi < workers; ++wi) {
         const vxb_worker_table& t = net->workers[wi];
         if (t.worker != wi || t.worker_count != workers)
             throw ConfigError("worker table ids are inconsistent");
-        wbase[wi + 1] = wbase[wi] + (local(wi) ? t.n_neurons : 0u);
-        src_base[wi + 1] = src_base[wi] + t.n_neurons;
+        wsum += local(wi) ? t.n_neurons : 0u;
+        ssum += t.n_neurons;
+        if (ssum >= (1ull << 32))
+            throw ConfigError("global neuron ids exceed 32-bit source addressing");
+        if (wsum >= (1ull << 31)) throw ConfigError("more than 2^31 neurons on one device");
+        wbase[wi + 1] = (uint32_t)wsum;
+        src_base[wi + 1] = (uint32_t)ssum;
     }
-    if ((uint64_t)src_base[workers] >= (1ull << 32))
-        throw ConfigError("global neuron ids exceed 32-bit source addressing");
     n_src = src_base[workers];
-    if ((uint64_t)wbase[workers] >= (1ull << 31))
-        throw ConfigError("more than 2^31 neurons on one device");
     n = wbase[workers];
     std::vector<uint32_t> h_v(n);
     std::vector<float4> h_g(n);
@@ -641,13 +664,23 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     // +4%); with peers and several L2 blocks the static deal measured better
     // (config 3 at 4 GPUs: 0.34 vs 0.60 s per bio-s)
     dyn = world == 1 || n_blocks == 1;
-    if (const char* env = std::getenv("VXB_DYN")) dyn = std::atoi(env) != 0;
+    if (const char* env = knob("VXB_DYN", &knobs)) dyn = std::atoi(env) != 0;
+    // chunks of one local spike on one GPU when a row segment averages >= 512
+    // entries (in-degree per L2 block; config 2: 1000), else up to 32
+    // (config 3's short L2-block segments: 1.14 ms per step at 32, 1.31 ms at
+    // 13, 6.2 at 1; config 2 on 2 GPUs: 2.44e11 events/s at 32, 2.37e11 at 1)
+    ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
+    if (const char* env = knob("VXB_CHMAX", &knobs)) ch_max = (uint32_t)std::max(1, std::atoi(env));
+    // publishing S(t) as soon as every CTA has routed it (before the phase's
+    // own delivery ends) measured slower: config 2 at 4 GPUs 4.23e11 vs
+    // 4.72e11 events/s
+    if (const char* ep = knob("VXB_EARLY_PUBLISH", &knobs)) early_publish = std::atoi(ep) != 0;
 
     // cooperative grid
     use_smem_seg = segs.size() <= (size_t)kMaxSmemSeg && npset <= (uint32_t)kMaxSmemPset;
     // bigger stages for L2-blocked delivery (short block segments per row)
     stage_e = n_blocks > 1 ? 1024u : (uint32_t)kStageE;
-    if (const char* env = std::getenv("VXB_STAGE_ENTRIES"))
+    if (const char* env = knob("VXB_STAGE_ENTRIES", &knobs))
         stage_e = (uint32_t)std::max(64, std::atoi(env));
     smem_bytes = SmemLayout(use_smem_seg ? (uint32_t)segs.size() : 0u,
                             use_smem_seg ? npset : 0u, stage_e).total;
@@ -663,7 +696,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
                                                          smem_bytes));
     if (per_sm < 1) throw SimError("step kernel cannot be resident on this device");
     grid = sms * per_sm;
-    if (std::getenv("VXB_VERBOSE"))
+    if (knob("VXB_VERBOSE", nullptr))
         std::fprintf(stderr,
                      "vxb: n=%u n_src=%u syn=%llu segs=%zu psets=%u smem_seg=%d smem=%u B "
                      "grid=%d (%d/SM) blocks=%u packed=%d dyn=%d\n",
@@ -673,7 +706,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     // within the persisting carve-out, so size it to the device maximum
     // (VXB_PERSIST=0 leaves the driver default)
     {
-        const char* env = std::getenv("VXB_PERSIST");
+        const char* env = knob("VXB_PERSIST", &knobs);
         if (!env || std::atoi(env) != 0) {
             int mx = 0;
             CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, device));
@@ -687,7 +720,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
         const uint64_t keep = (uint64_t)n * (40 + 2 * (packed ? 16 : 32));
         f_policy = keep <= (uint64_t)l2 * 3 / 4 ? 2u : 0u;
-        if (const char* fp = std::getenv("VXB_FPOL")) f_policy = (uint32_t)std::atoi(fp);
+        if (const char* fp = knob("VXB_FPOL", &knobs)) f_policy = (uint32_t)std::atoi(fp);
     }
     CK(cudaStreamSynchronize(stream));
 }
@@ -1235,9 +1268,9 @@ void Engine::build_blocks() {
     // block (half of config 5, 25M neurons per GPU at 15 Hz: 2.56e11 ->
     // 2.91e11 events/s; config 3's 5-10M per GPU stay faster at 64 MB)
     uint64_t mb = ((n_ref * pend_per + (64ull << 20) - 1) / (64ull << 20)) >= 6 ? 80 : 64;
-    if (const char* env = std::getenv("VXB_BLOCK_MB")) mb = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
+    if (const char* env = knob("VXB_BLOCK_MB", &knobs)) mb = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
     uint64_t bn = (mb << 20) / pend_per;
-    if (const char* env = std::getenv("VXB_BLOCK_NEURONS")) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
+    if (const char* env = knob("VXB_BLOCK_NEURONS", &knobs)) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));
     if (n_ref <= bn || n_syn == 0) return;
     n_blocks = (uint32_t)((n_ref + bn - 1) / bn);
     block_n = (uint32_t)((n + n_blocks - 1) / n_blocks);
@@ -1372,7 +1405,18 @@ void Engine::advance(uint32_t steps) {
             inj_ep[rel] = it->second;
         }
     }
-    const bool has_forced = !f_loc.empty(), has_inj = !inj_tab.empty();
+    // tables of THIS advance only: an advance without forced spikes or active
+    // injections must not replay the previous advance's tables
+    has_forced = !f_loc.empty();
+    has_inj = !inj_tab.empty();
+    if (!has_forced) {
+        d_forced_off.release();
+        d_forced_local.release();
+    }
+    if (!has_inj) {
+        d_inj_epoch.release();
+        d_inj_table.release();
+    }
     if (has_forced) {
         d_forced_off.alloc(f_off.size());
         d_forced_local.alloc(f_loc.size());
@@ -1548,10 +1592,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.probe_slot = d_probe_slot.p;
     a.probe_v = d_probe_v.p;
     a.probe_i = d_probe_i.p;
-    a.has_forced = d_forced_off.n ? 1u : 0u;
+    a.has_forced = has_forced ? 1u : 0u;
     a.forced_off = a.has_forced ? d_forced_off.p + rel0 : nullptr;
     a.forced_local = d_forced_local.p;
-    a.has_inj = d_inj_epoch.n ? 1u : 0u;
+    a.has_inj = has_inj ? 1u : 0u;
     a.inj_epoch = a.has_inj ? d_inj_epoch.p + rel0 : nullptr;
     a.inj_table = d_inj_table.p;
     a.n_voxels = n_voxels;
@@ -1569,18 +1613,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.work_ctr = d_work.p;
     a.dyn = dyn ? 1u : 0u;
     a.stage_e = stage_e;
-    // chunks of one local spike on one GPU when a row segment averages >= 512
-    // entries (in-degree per L2 block; config 2: 1000), else up to 32
-    // (config 3's short L2-block segments: 1.14 ms per step at 32, 1.31 ms at
-    // 13, 6.2 at 1; config 2 on 2 GPUs: 2.44e11 events/s at 32, 2.37e11 at 1)
-    a.ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
-    if (const char* env = std::getenv("VXB_CHMAX")) a.ch_max = std::max(1, std::atoi(env));
+    a.ch_max = ch_max;
     a.f_policy = f_policy;
-    {
-        const char* ep = std::getenv("VXB_EARLY_PUBLISH");
-        a.early_publish = ep ? (std::atoi(ep) != 0 ? 1u : 0u) : 0u;  // measured slower (config 2 at 4 GPUs 4.23e11 vs 4.72e11 events/s)
-    }
-    const bool prof = std::getenv("VXB_PHASE_PROFILE") != nullptr;
+    a.early_publish = early_publish ? 1u : 0u;
+    const bool prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
     DevBuf<unsigned long long> d_prof;
     if (prof) {
         d_prof.alloc(2ull * (steps + 1) * grid);
@@ -1649,12 +1685,16 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     device_ms += ms;
     d2h += sizeof c + 4 * rr.size() + 4ull * (steps + 1);
     if (world > 1) {
-        uint32_t to[2] = {0, 0};
-        CK(cudaMemcpy(to, &d_ex.p->timeout, 8, cudaMemcpyDeviceToHost));
+        uint32_t to[3] = {0, 0, 0};  // timeout, timeout_step, peer_abort
+        CK(cudaMemcpy(to, &d_ex.p->timeout, 12, cudaMemcpyDeviceToHost));
         if (to[0]) {
             failed = true;
             throw SimError(fmt("step barrier timed out on worker %u at step %u (no batch from "
                                "worker %u)", rank, to[1], to[0] - 1));
+        }
+        if (to[2] && c.err == ~0ull) {  // engine.cpp:483-484
+            failed = true;
+            throw SimError("simulation aborted while waiting on the step barrier");
         }
     }
     if (c.err != ~0ull) {
@@ -1704,6 +1744,17 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     }
 }
 
+// The schedule the engine chose for this network (JSON object), with every
+// tuning knob that was applied: logged beside each benchmark result.
+std::string Engine::schedule_info() const {
+    return fmt("{\"path\":\"%s\",\"grid\":%d,\"threads\":%d,\"smem_bytes\":%u,"
+               "\"l2_blocks\":%u,\"dynamic_deal\":%d,\"stage_entries\":%u,\"ch_max\":%u,"
+               "\"state_l2_policy\":%u,\"packed_pending\":%d,\"world\":%u,\"knobs\":{",
+               "l2_atomic", grid, kThreads, smem_bytes, n_blocks, (int)dyn, stage_e, ch_max,
+               f_policy, (int)packed, world) +
+           knobs + "}}";
+}
+
 int fail_code(const std::exception& e) {
     return dynamic_cast<const ConfigError*>(&e) ? VXB_ECONFIG : VXB_ESIM;
 }
@@ -1717,6 +1768,13 @@ struct vxb_engine {
 extern "C" {
 
 int vxb_abi_version(void) { return VXB_ABI_VERSION; }
+
+#ifndef VXB_SRC_HASH
+#define VXB_SRC_HASH "unknown"
+#endif
+// "VXB_SRC_HASH=<hash>" is also the marker build.py finds in the binary
+static const char kBuildHash[] = "VXB_SRC_HASH=" VXB_SRC_HASH;
+const char* vxb_build_hash(void) { return kBuildHash + 13; }
 
 const char* vxb_last_error(const vxb_engine* e) {
     return e ? e->eng.err.c_str() : g_create_error.c_str();
@@ -1799,6 +1857,13 @@ uint64_t vxb_result_timings_size(const vxb_engine* e) { return e->eng.timings.si
 int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap) {
     if (cap < e->eng.timings.size()) return VXB_ECONFIG;
     std::memcpy(out, e->eng.timings.data(), sizeof(vxb_step_timings) * e->eng.timings.size());
+    return VXB_OK;
+}
+
+int vxb_schedule_info(const vxb_engine* e, char* out, uint64_t cap) {
+    const std::string j = e->eng.schedule_info();
+    if (!out || cap < j.size() + 1) return VXB_ECONFIG;
+    std::memcpy(out, j.c_str(), j.size() + 1);
     return VXB_OK;
 }
 

@@ -85,7 +85,10 @@ struct Control {
     unsigned long long err;    // min (step << 32 | local) of a divergence, ~0 = none
     unsigned long long flops_inner, flops_outer;
     unsigned int routed;       // CTAs that routed this phase's spikes (multi-GPU)
-    unsigned int pad[5];
+    // stop decision of the phase, taken once by the last CTA through the
+    // barrier (hook) so every CTA leaves the loop at the same phase
+    unsigned int stop;
+    unsigned int pad[4];
 };
 
 // Device-side state of the per-step spike-id exchange between ranks (one
@@ -98,7 +101,8 @@ struct Exchange {
     uint32_t cap_self;                    // ids per parity in my slots (= my neurons)
     uint32_t timeout;                     // peer + 1 whose batch never arrived, 0 = none
     uint32_t timeout_step;
-    uint32_t pad0[3];
+    uint32_t peer_abort;                  // peer + 1 that aborted the run (engine.cpp:117-142)
+    uint32_t pad0[2];
     unsigned long long timeout_ns;
     uint32_t src_base[kMaxShards + 1];    // global source index base per shard
     uint32_t cap[kMaxShards];             // neurons of shard h
@@ -108,7 +112,7 @@ struct Exchange {
     // a receiver still reading the batch of step t - 1: four slots.
     uint32_t send_cnt[4][kMaxShards];     // ids queued per (slot, destination)
     uint32_t* rx_ids[kMaxShards];         // [kSlots * cap[h]] from source shard h
-    uint32_t* rx_meta[kMaxShards];        // counts[kSlots], flag (= step + 1)
+    uint32_t* rx_meta[kMaxShards];        // counts[kSlots], flag (= step + 1), abort word
     uint32_t* tx_ids[kMaxShards];         // my slot in peer d
     uint32_t* tx_meta[kMaxShards];
 };
@@ -691,6 +695,13 @@ __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h,
     const uint32_t* meta = ex->rx_meta[h];
     const unsigned long long t0 = globaltimer();
     while (ld_acquire_sys(meta + kSlots) < tE + 1) {
+        // a peer that failed never publishes again: its abort word ends the
+        // wait at once (the reference's shared abort flag, engine.cpp:483-484)
+        for (uint32_t q = 0; q < ex->world; ++q)
+            if (q != ex->rank && ld_acquire_sys(ex->rx_meta[q] + kSlots + 1) != 0u) {
+                atomicCAS(&ex->peer_abort, 0u, q + 1);
+                return 0;
+            }
         if (ex->timeout_ns && globaltimer() - t0 > ex->timeout_ns) {
             if (atomicCAS(&ex->timeout, 0u, h + 1) == 0u) ex->timeout_step = tE;
             return 0;
@@ -698,6 +709,16 @@ __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h,
         __nanosleep(64);
     }
     return ld_acquire_sys(meta + slot);
+}
+
+// Tell every peer this rank stopped (divergence, timeout or a peer's abort):
+// their waits for this rank's next batch end with the reference's "simulation
+// aborted while waiting on the step barrier" instead of a 30 s timeout.
+__device__ __forceinline__ void exchange_abort(const StepArgs& a) {
+    Exchange* ex = a.ex;
+    __threadfence_system();
+    for (uint32_t d = 0; d < ex->world; ++d)
+        if (d != ex->rank) st_release_sys(ex->tx_meta[d] + kSlots + 1, 1u);
 }
 
 // Per-neuron state the fused update reads (prefetched one neuron ahead).
@@ -1252,12 +1273,24 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                 if (doA) a.seg_end[ph] = ctl->spk_cursor;
                 if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
                 a.phase_ns[ph + 1] = globaltimer();
+                // one stop decision for the whole grid (L2-coherent reads of
+                // the flags the phase may have raised)
+                ctl->stop = (atomicAdd(&ctl->err, 0ull) != ~0ull ||
+                             atomicAdd(&a.ex->timeout, 0u) != 0u ||
+                             atomicAdd(&a.ex->peer_abort, 0u) != 0u) ? 1u : 0u;
             },
             [&] {
-                if (a.world > 1 && doA && !a.early_publish) exchange_publish(a, tA);
+                if (a.world > 1) {
+                    // a failed step publishes no batch (the reference's worker
+                    // throws before phase B), so no peer can finish without it
+                    if (ctl->stop)
+                        exchange_abort(a);
+                    else if (doA && !a.early_publish)
+                        exchange_publish(a, tA);
+                }
             });
-        if (threadIdx.x == 0) {  // L2-coherent reads
-            s_stop = atomicAdd(&ctl->err, 0ull) != ~0ull || atomicAdd(&a.ex->timeout, 0u) != 0u;
+        if (threadIdx.x == 0) {
+            s_stop = (int)ld_acquire(&ctl->stop);
             s_nspk = 0;
             s_fwork = 0;
             s_tD = s_tF = 0;

@@ -413,6 +413,16 @@ class SimInstance:
     def workers(self) -> int:
         return int(self._lib.vxb_workers(self._h))
 
+    def schedule_info(self) -> dict:
+        """The delivery schedule the engine chose (and any tuning knob applied
+        from the environment under VXB_TUNING=1), for benchmark records."""
+        import json
+        buf = C.create_string_buffer(4096)
+        rc = self._lib.vxb_schedule_info(self._h, buf, len(buf))
+        if rc != 0:
+            self._err(rc)
+        return json.loads(buf.value.decode())
+
 
 def run_simulation(tables: NetworkTables, options: SimOptions) -> RunResult:
     """voxsim::run_simulation (engine.hpp:92-93)."""

@@ -147,8 +147,60 @@ def main_full():
     dist.destroy_process_group()
 
 
+def main_abort():
+    """Cross-rank abort (engine.cpp:117-142, 483-484): the last rank's
+    neurons diverge (an infinite injection current drives V to inf at step 30);
+    that rank reports the divergence and every other rank must leave its step
+    barrier with "simulation aborted while waiting on the step barrier" at
+    once, not after recv_timeout_ms (30 s)."""
+    import time
+    from paper_2308_01241_b200.engine import Injection, SimError
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    cfg = {"seed": 1401, "dt_ms": 1.0, "steps": 200, "workers": world,
+           "connectome": {"kind": "ring", "voxels": 12, "neurons_per_voxel": 2000},
+           "partition": {"method": "sequential"},
+           "regions": {"subcortex": {"k_in": 100, "ou_mean": 300.0}}}
+    net = netgen.build_network(cfg)
+    last_voxel = len(net.layout.voxels) - 1  # sequential partition: on rank world - 1
+    opt = SimOptions(steps=200, device=local, recv_timeout_ms=30000,
+                     injections=[Injection(30, 200, last_voxel, float("inf"))])
+    sim = netgen.DistributedSimInstance(net, opt, rank, world)
+    t0 = time.perf_counter()
+    msg = ""
+    try:
+        sim.advance(200)
+    except SimError as e:
+        msg = str(e)
+    dt = time.perf_counter() - t0
+    # a failed instance rejects further advances (engine.cpp:765-766)
+    try:
+        sim.advance(1)
+        rejected = False
+    except SimError:
+        rejected = True
+    out = [None] * world
+    dist.all_gather_object(out, {"rank": rank, "msg": msg, "seconds": dt, "rejected": rejected})
+    if rank == 0:
+        div = out[world - 1]["msg"].startswith("membrane potential diverged")
+        others = all(o["msg"] == "simulation aborted while waiting on the step barrier"
+                     for o in out[:world - 1])
+        fast = max(o["seconds"] for o in out) < 5.0
+        res = {"world": world, "mode": "abort", "ranks": out, "diverged_equal": div,
+               "aborted_equal": others, "fast_equal": fast,
+               "rejected_equal": all(o["rejected"] for o in out)}
+        res["pass"] = div and others and fast and res["rejected_equal"]
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--full":
         main_full()
+    elif len(sys.argv) > 1 and sys.argv[1] == "--abort":
+        main_abort()
     else:
         main()

@@ -395,6 +395,7 @@ def test_acceptance_1_multi_worker_equivalence():
 def test_static_and_dynamic_delivery_match_reference(monkeypatch, dyn):
     """Both producer schedules — static round-robin rows (VXB_DYN=0) and the
     default block-major dynamic chunks — are bit-exact (config 1 shape)."""
+    monkeypatch.setenv("VXB_TUNING", "1")
     monkeypatch.setenv("VXB_DYN", dyn)
     cfg = make_config(seed=1, voxels=1, npv=10000, k_in=100, dt_ms=0.1, steps=3000)
     net = RefNet(cfg)
@@ -425,6 +426,7 @@ def test_l2_blocked_delivery_matches_reference(monkeypatch):
     """L2-blocked delivery (target-sorted rows, per-source block offsets,
     blocks delivered in order), forced on a small network with 2048-neuron
     blocks: bit-exact against the reference."""
+    monkeypatch.setenv("VXB_TUNING", "1")
     monkeypatch.setenv("VXB_BLOCK_NEURONS", "2048")
     net = RefNet(make_config(seed=1401, voxels=10, npv=1000, k_in=100, rho=6 / 25))
     opt = SimOptions(steps=300, probe_gids=[5, 5000, 9999])
@@ -434,3 +436,27 @@ def test_l2_blocked_delivery_matches_reference(monkeypatch):
     assert ref.total_spikes > 0
     assert_same(gpu, ref)
     assert np.array_equal(snaps[0], rs.membrane_snapshot(0))
+
+
+def test_advance_without_forced_spikes_or_injection_after_one_with():
+    """Forced spikes and injections are keyed by absolute step
+    (engine.cpp:352-361, 389-398): an advance whose window holds none must
+    not replay the previous advance's tables, and a longer later advance
+    must not read past them."""
+    net = RefNet(make_config(seed=29, voxels=2, npv=300, k_in=12, rho=0.3), even_workers=2)
+    g = net.tables.workers[0].neurons["gid"]
+    opt = SimOptions(steps=130, probe_gids=[int(g[3]), 450],
+                     forced_spikes=[ForcedSpike(10, int(g[3])), ForcedSpike(40, int(g[7]))],
+                     injections=[Injection(0, 50, 0, 120.0), Injection(20, 45, 1, -60.0)])
+    with SimInstance(net.tables, opt) as sim:
+        a = sim.advance(50)
+        b = sim.advance(80)
+        snaps = [sim.membrane_snapshot(w) for w in range(2)]
+    rs = RefSim(net, opt)
+    ra = rs.advance(50)
+    rb = rs.advance(80)
+    assert rb.total_spikes > 0
+    assert_same(a, ra)
+    assert_same(b, rb)
+    for w in range(2):
+        assert np.array_equal(snaps[w], rs.membrane_snapshot(w))

@@ -60,6 +60,7 @@ def test_config2_piecewise_equals_whole():
 
 def test_config2_delivery_schedule_invariance(monkeypatch):
     cfg = _config2()
+    monkeypatch.setenv("VXB_TUNING", "1")
     monkeypatch.setenv("VXB_DYN", "1")
     dyn = _run(cfg, [40])
     monkeypatch.setenv("VXB_DYN", "0")
@@ -82,6 +83,7 @@ def test_config3_l2_blocked_equals_unblocked(monkeypatch):
     import bench
     cfg = bench.dti_cfg()
     blocked = _run(cfg, [12])
+    monkeypatch.setenv("VXB_TUNING", "1")
     monkeypatch.setenv("VXB_BLOCK_NEURONS", str(1 << 30))  # one block: plain L2 atomics
     plain = _run(cfg, [12])
     assert blocked[3] > 10_000_000

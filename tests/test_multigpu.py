@@ -72,8 +72,8 @@ def _gpus():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (2, {"VXB_EARLY_PUBLISH": "1"}),
-                                       (2, {"VXB_DYN": "0"})])
+@pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (2, {"VXB_TUNING": "1", "VXB_EARLY_PUBLISH": "1"}),
+                                       (2, {"VXB_TUNING": "1", "VXB_DYN": "0"})])
 def test_nvlink_exchange_matches_reference(world, env):
     """Default schedule, plus the optional early batch publication (4-slot
     ring) and the static delivery deal."""
@@ -105,3 +105,20 @@ def test_fullsize_config2_two_gpus_equal_one_gpu():
     res = json.loads(lines[-1])
     assert res["pass"], res
     assert res["events"] == res["one_gpu_events"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_divergence_on_one_rank_aborts_all_ranks():
+    """A divergence on one rank ends every rank's advance within one step:
+    the diverging rank reports it, the others the reference's "simulation
+    aborted while waiting on the step barrier" (engine.cpp:483-484), well
+    before the 30 s receive timeout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=2", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), str(ROOT / "tests" / "dist_check.py"), "--abort"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert lines, out.stdout + out.stderr
+    res = json.loads(lines[-1])
+    assert res["pass"], res

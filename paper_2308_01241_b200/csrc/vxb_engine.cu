@@ -35,6 +35,7 @@
 #include "vxb_hemo.cuh"
 #include "vxb_kernels.cuh"
 #include "vxb_netgen.cuh"
+#include "vxb_tile.cuh"
 
 namespace {
 
@@ -207,6 +208,16 @@ struct Engine {
     std::string knobs;  // tuning knobs applied (VXB_TUNING=1), JSON members
     uint32_t ch_max = 1;
     bool early_publish = false;
+    // SM-tile path (vxb_tile.cuh): pending sums in shared memory, one CTA per
+    // SM; chosen when the shard fits on chip (tile_path), else l2_atomic
+    bool tile_path = false;
+    uint32_t tile_per = 0, tile_stages = 0, tile_cons = 8, tile_smem = 0, tile_grid = 0;
+    uint64_t q_total = 0;
+    DevBuf<unsigned long long> d_tl_off;
+    DevBuf<uint4> d_tl;
+    DevBuf<uint32_t> d_qbase, d_qcnt;
+    DevBuf<uint4> d_q;
+    void setup_tiles();
     std::string schedule_info() const;
 
     // ---------------------------------------------------------- device
@@ -658,7 +669,10 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     if (tr != "queue" && tr != "nvlink") throw ConfigError("unknown transport: " + tr);
 
     setup_exchange();
-    if (!donor) build_blocks();
+    if (!donor) {
+        setup_tiles();
+        if (!tile_path) build_blocks();
+    }
     // dynamic chunks win on one device (+8% config 2, config 3 2.0 -> 1.5 s
     // per bio-s) and with peers when there is one block (config 2 at 4 GPUs
     // +4%); with peers and several L2 blocks the static deal measured better
@@ -1147,6 +1161,19 @@ void Engine::share_tables(const Engine& d) {
     rows_sorted = d.rows_sorted;
     n_blocks = d.n_blocks;
     block_n = d.block_n;
+    tile_path = d.tile_path;
+    tile_per = d.tile_per;
+    tile_stages = d.tile_stages;
+    tile_smem = d.tile_smem;
+    tile_grid = d.tile_grid;
+    q_total = d.q_total;
+    d_tl_off.share(d.d_tl_off);
+    d_tl.share(d.d_tl);
+    d_qbase.share(d.d_qbase);
+    if (tile_path) {  // the work queues are per instance
+        d_q.alloc(2 * q_total);
+        d_qcnt.alloc(2ull * tile_grid);
+    }
 }
 
 // Exchange state: receive region (one slot per peer: ids[kSlots][n_h],
@@ -1244,6 +1271,84 @@ void Engine::sort_rows() {
         s0 = s1;
     }
     rows_sorted = true;
+}
+
+// SM-tile path: every CTA (one per SM) owns a contiguous tile of neurons and
+// keeps their pending sums in shared memory (vxb_tile.cuh).  Eligible when
+// the pending tile fits beside a >= 3-stage delivery ring (shards up to
+// ~1.3M neurons on 148 SMs), on one GPU, with carry-free packed sums.  Rows
+// are sorted by target and cut into per-tile segments here, once.
+void Engine::setup_tiles() {
+    tile_path = false;
+    const char* force = knob("VXB_PATH", &knobs);
+    if (force && std::string(force) == "l2") return;
+    if (world != 1 || !packed || n == 0) return;
+    int sms = 0, optin = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    const uint32_t per = (uint32_t)((((uint64_t)n + sms - 1) / sms + 31) & ~31ull);
+    uint32_t S = kTileMaxStages;
+    while (S >= 3 && TileLayout(per, S).total > (uint32_t)optin) --S;
+    if (S < 3) return;
+    if (const char* c = knob("VXB_TILE_CONS", &knobs))
+        tile_cons = (uint32_t)std::min(20, std::max(1, std::atoi(c)));
+    if (const char* c = knob("VXB_TILE_STAGES", &knobs))
+        S = std::min(S, (uint32_t)std::max(3, std::atoi(c)));
+    const TileLayout L(per, S);
+    CK(cudaFuncSetAttribute((const void*)tile_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel, kTileThreads, L.total));
+    if (per_sm < 1) return;
+    const uint32_t tiles = (uint32_t)((n + per - 1) / per);
+    sort_rows();
+    // tile segments of every row: count, scan, write
+    DevBuf<unsigned long long> cnt;
+    cnt.alloc((size_t)n_src + 1);
+    cnt.zero(stream);
+    tile_segments_kernel<0><<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
+                                                       d_tgt.p, n_src, per, cnt.p + 1, nullptr,
+                                                       nullptr, nullptr);
+    CK(cudaGetLastError());
+    d_tl_off.alloc((size_t)n_src + 1);
+    {
+        size_t tmp = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.p + 1, d_tl_off.p + 1, n_src, stream));
+        DevBuf<unsigned char> t;
+        t.alloc(tmp ? tmp : 1);
+        CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cnt.p + 1, d_tl_off.p + 1, n_src, stream));
+        CK(cudaMemsetAsync(d_tl_off.p, 0, 8, stream));
+    }
+    unsigned long long total = 0;
+    CK(cudaMemcpyAsync(&total, d_tl_off.p + n_src, 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    cnt.release();
+    d_tl.alloc(std::max<unsigned long long>(1, total));
+    DevBuf<uint32_t> cap;
+    cap.alloc(sms);
+    cap.zero(stream);
+    tile_segments_kernel<1><<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
+                                                       d_tgt.p, n_src, per, nullptr, d_tl_off.p,
+                                                       d_tl.p, cap.p);
+    CK(cudaGetLastError());
+    std::vector<uint32_t> hcap(sms), qb(sms + 1, 0);
+    CK(cudaMemcpyAsync(hcap.data(), cap.p, 4ull * sms, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    for (int t = 0; t < sms; ++t) qb[t + 1] = qb[t] + hcap[t];
+    if (total >= (1ull << 32)) throw SimError("tile segment table exceeds 2^32 entries");
+    q_total = total;
+    d_qbase.alloc(sms + 1);
+    CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 4ull * (sms + 1), cudaMemcpyHostToDevice, stream));
+    d_q.alloc(std::max<uint64_t>(1, 2 * total));
+    d_qcnt.alloc(2ull * sms);
+    d_qcnt.zero(stream);
+    CK(cudaStreamSynchronize(stream));
+    tile_path = true;
+    tile_per = per;
+    tile_stages = S;
+    tile_smem = L.total;
+    tile_grid = (uint32_t)sms;
+    (void)tiles;
 }
 
 // L2-blocked delivery: when the pending buffer does not fit in L2, targets
@@ -1624,9 +1729,25 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         a.prof = d_prof.p;
     }
 
+    if (tile_path) {
+        a.tile_n = tile_per;
+        a.ring_stages = tile_stages;
+        a.n_cons = tile_cons;
+        a.q_total = (uint32_t)q_total;
+        a.tl_off = d_tl_off.p;
+        a.tl = d_tl.p;
+        a.q_base = d_qbase.p;
+        a.q_cnt = d_qcnt.p;
+        a.q = d_q.p;
+        a.src_self = 0;
+        d_qcnt.zero(stream);
+    }
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
-    if (packed)
+    if (tile_path)
+        CK(cudaLaunchCooperativeKernel((const void*)tile_kernel, tile_grid, kTileThreads, args,
+                                       tile_smem, stream));
+    else if (packed)
         CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args,
                                        smem_bytes, stream));
     else
@@ -1747,10 +1868,19 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
 // The schedule the engine chose for this network (JSON object), with every
 // tuning knob that was applied: logged beside each benchmark result.
 std::string Engine::schedule_info() const {
-    return fmt("{\"path\":\"%s\",\"grid\":%d,\"threads\":%d,\"smem_bytes\":%u,"
+    if (tile_path)
+        return fmt("{\"path\":\"sm_tile\",\"kernel\":\"vxb::tile_kernel\",\"grid\":%u,"
+                   "\"threads\":%d,\"smem_bytes\":%u,\"tile_neurons\":%u,\"ring_stages\":%u,"
+                   "\"stage_entries\":%u,\"consumer_warps\":%u,\"queue_items\":%llu,"
+                   "\"state_l2_policy\":%u,\"packed_pending\":%d,\"world\":%u,\"knobs\":{",
+                   tile_grid, kTileThreads, tile_smem, tile_per, tile_stages, kTileSE, tile_cons,
+                   (unsigned long long)q_total, f_policy, (int)packed, world) +
+               knobs + "}}";
+    return fmt("{\"path\":\"l2_atomic\",\"kernel\":\"vxb::step_kernel\",\"grid\":%d,"
+               "\"threads\":%d,\"smem_bytes\":%u,"
                "\"l2_blocks\":%u,\"dynamic_deal\":%d,\"stage_entries\":%u,\"ch_max\":%u,"
                "\"state_l2_policy\":%u,\"packed_pending\":%d,\"world\":%u,\"knobs\":{",
-               "l2_atomic", grid, kThreads, smem_bytes, n_blocks, (int)dyn, stage_e, ch_max,
+               grid, kThreads, smem_bytes, n_blocks, (int)dyn, stage_e, ch_max,
                f_policy, (int)packed, world) +
            knobs + "}}";
 }

@@ -190,6 +190,17 @@ struct StepArgs {
     unsigned long long* prof;
     uint32_t early_publish;  // publish S(tA) once routed (else after the phase barrier)
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
+    // ---- SM-tile path (tile_kernel, vxb_tile.cuh) ----
+    uint32_t tile_n;            // neurons per CTA tile (multiple of 32)
+    uint32_t ring_stages;       // delivery ring depth (runtime)
+    uint32_t n_cons;            // consumer warps
+    uint32_t q_total;           // queue items per parity
+    const unsigned long long* tl_off;  // per global source: first tile segment (n_src + 1)
+    const uint4* tl;            // tile segments {tile, first entry in row, length, 0}
+    const uint32_t* q_base;     // per tile: first queue slot (tiles + 1)
+    uint32_t* q_cnt;            // [2][tiles] items queued per (parity, tile)
+    uint4* q;                   // [2][q_total] {entry lo, entry hi, length, 0}
+    uint32_t src_self;          // global source index of shard-local neuron 0
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {

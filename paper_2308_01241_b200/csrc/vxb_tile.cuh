@@ -1,0 +1,598 @@
+// vxb_tile.cuh — the SM-tile path of the simulation step, for shards whose
+// pending sums fit in the GPU's shared memory (config 2: 1M neurons x 16 B
+// = 16 MB over 148 SMs).
+//
+// One CTA per SM owns a contiguous tile of neurons: it updates them AND
+// accumulates their pending synaptic input in shared memory, so delivery
+// runs on the SMs' shared-memory atomics (two ATOMS.ADD.32 per event,
+// measured 5.6e11 events/s chip-wide) instead of the L2 atomic units (the
+// l2_atomic path's ceiling, ~1.9e11 red/s).  Rows are sorted by target and
+// split at tile boundaries once at load: every (source, tile) segment is
+// contiguous in the out-CSR.  When a neuron spikes (A(tA) of phase ph) the
+// spiking lane appends one work item {first entry, length} per tile its row
+// touches to that tile's queue; in phase ph + 1 each CTA streams exactly the
+// segments of its own tile with TMA bulk copies and adds them into its
+// shared-memory pending tile.  Every synapse entry is read once, by the CTA
+// that owns its target; nothing is re-read or reduced twice.
+//
+// Phase ph of a chunk (tA = t0 + ph, tE = tA - 1), per CTA:
+//   U  (warps 1..23)  E(tE) + A(tA) of the tile's neurons: gating with the
+//                     shared-memory pending P(S(tE-1)) (zeroed after the
+//                     read), current, membrane; the OU current I_ou(tE) was
+//                     already advanced in phase ph - 1 (see N).  Spikes of
+//                     S(tA) are logged, counted and bucketed into the tile
+//                     queues of parity tA.
+//   P  (warp 0)       producer: bulk-copies the segments queued for this
+//                     tile in parity tE into an 8-stage ring while U runs.
+//   after U:
+//   C  (warps 1..C)   consumers: drain the ring into the pending tile with
+//                     shared atomics — P(S(tE)), consumed by E(tA) in ph+1.
+//   N  (other warps)  advance I_ou to tA (fp64 Box-Muller noise, ou_kernel)
+//                     for the tile, overlapping the atomics.
+//   grid barrier.
+// Moving the OU step one phase earlier is exact: I_ou(t) depends only on
+// I_ou(t-1) and xi(gid, t) (ou_kernel, model.hpp:88-90; engine.cpp:551-558).
+// Between chunks (and advance() calls) the state is the reference's
+// post-phase-E state: the last phase does not advance I_ou, and the pending
+// tile is written back to the global pending buffer of its parity.
+#pragma once
+
+#include "vxb_kernels.cuh"
+
+namespace vxb {
+
+constexpr int kTileThreads = 768;       // 24 warps: 1 producer + 23 update/consume/noise
+constexpr uint32_t kTileSE = 1024;      // synapse entries per ring stage
+constexpr uint32_t kTileMaxStages = 8;
+constexpr uint32_t kTileMaxSeg = 64;    // a tile's parameter segments kept in shared memory
+constexpr uint32_t kTileMaxPset = 32;
+
+// Dynamic shared memory of tile_kernel.
+struct TileLayout {
+    uint32_t per, S, se, tb, wb;
+    uint32_t pend, tgt, w, bar, meta, pset, seg, start, spk, total;
+    __host__ __device__ TileLayout(uint32_t per_, uint32_t stages) {
+        per = per_;
+        S = stages;
+        se = kTileSE;
+        tb = (se + 8) * 4;
+        wb = (se + 4) * 8;
+        pend = 0;                   // AMPA[per], NMDA[per], GABAA[per], GABAB[per] (u32)
+        tgt = pend + 16 * per;      // per is a multiple of 32: 16-byte aligned
+        w = tgt + S * tb;
+        bar = w + S * wb;           // full[S], then empty[S]
+        meta = bar + 2 * S * 8;
+        pset = (meta + S * kMetaBytes + 127) & ~127u;
+        seg = pset + kTileMaxPset * (uint32_t)sizeof(ParamSet);
+        start = seg + kTileMaxSeg * (uint32_t)sizeof(SegInfo);
+        spk = (start + (kTileMaxSeg + 1) * 4 + 15) & ~15u;
+        total = spk + kSpkStage * 4;
+    }
+};
+
+// Producer side of the tile ring (lane 0 of warp 0): packs queued row
+// segments into stages of kTileSE entries, one bulk copy of targets and one
+// of weights per segment piece, expect_tx per piece, one arrive per stage.
+struct TileRing {
+    uint32_t ctr;  // stages committed since launch (stage = ctr % S)
+    uint32_t open;
+    uint32_t ns, toff, woff, total;
+
+    __device__ __forceinline__ void begin(unsigned char* smem, const TileLayout& L) {
+        const uint32_t st = ctr % L.S;
+        uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.bar) + L.S;
+        mbar_wait(empty + st, ((ctr / L.S) & 1u) ^ 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        open = 1;
+        ns = toff = woff = total = 0;
+    }
+    __device__ __forceinline__ void commit(unsigned char* smem, const TileLayout& L, uint32_t end) {
+        const uint32_t st = ctr % L.S;
+        TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+        m->pre[ns] = total;
+        m->n = total;
+        m->nseg = ns;
+        m->end = end;
+        mbar_arrive(reinterpret_cast<uint64_t*>(smem + L.bar) + st);
+        ++ctr;
+        open = 0;
+    }
+    __device__ __forceinline__ void add(const StepArgs& a, unsigned char* smem, const TileLayout& L,
+                                        uint64_t b0, uint64_t len, uint64_t pol) {
+        while (len) {
+            if (!open) begin(smem, L);
+            const int room_t = (int)L.se - (int)toff, room_w = (int)L.se - (int)woff;
+            const int room = room_t < room_w ? room_t : room_w;
+            if (ns == (uint32_t)kSegPerStage || room <= 0) {
+                commit(smem, L, 0);
+                continue;
+            }
+            const uint32_t st = ctr % L.S;
+            TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
+            // the 16-byte aligned supersets copied stay within the stage's
+            // (se + 8) target and (se + 4) weight slots
+            const uint64_t take = min(len, (uint64_t)room);
+            const uint64_t b1 = b0 + take;
+            const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
+            const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0);
+            const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
+            m->pre[ns] = total;
+            m->tb[ns] = toff + (uint32_t)(b0 - t0);
+            m->wb[ns] = woff + (uint32_t)(b0 - w0);
+            uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
+            mbar_expect_tx_only(full, tn * 4 + wn * 8);
+            bulk_g2s(smem + L.tgt + st * L.tb + toff * 4, a.tgt + t0, tn * 4, full, pol);
+            bulk_g2s(smem + L.w + st * L.wb + woff * 8, a.w + w0, wn * 8, full, pol);
+            total += (uint32_t)take;
+            toff += tn;
+            woff += wn;
+            ++ns;
+            b0 = b1;
+            len -= take;
+        }
+    }
+};
+
+// Warp-uniform parameter-segment lookup over the tile's segment table:
+// starts[0..nseg) ascending, `end` = first neuron past the last segment.
+struct SegCursor {
+    uint32_t hint = 0, lo = 1u, nx = 0u;
+    __device__ __forceinline__ uint32_t find(const uint32_t* starts, uint32_t nseg, uint32_t end,
+                                             uint32_t w_lo, uint32_t w_last, uint32_t i_lane,
+                                             uint32_t lane) {
+        if (w_lo < lo || w_last >= nx) {
+            uint32_t s0 = 0;
+            if (lane == 0) s0 = find_seg_from(starts, nseg, w_lo, w_lo >= lo ? hint : 0u);
+            hint = __shfl_sync(0xffffffffu, s0, 0);
+            lo = starts[hint];
+            nx = hint + 1 < nseg ? starts[hint + 1] : end;
+        }
+        uint32_t seg = hint;
+        if (i_lane >= nx)
+            while (seg + 1 < nseg && starts[seg + 1] <= i_lane) ++seg;
+        return seg;
+    }
+};
+
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const TileLayout L(a.tile_n, a.ring_stages);
+    uint32_t* s_pA = reinterpret_cast<uint32_t*>(smem + L.pend);  // [4][per] receptor sums
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+    uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
+    __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_base;
+    __shared__ int s_stop;
+    __shared__ uint32_t s_seg_lo, s_nseg;
+
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = a.tile_n;
+    const uint32_t c_lo = min(a.n, blockIdx.x * per), c_hi = min(a.n, c_lo + per);
+    const uint32_t nt = c_hi - c_lo;
+    const uint32_t nch = (nt + 31u) >> 5;
+    Control* ctl = a.ctl;
+
+    // parameter sets and the tile's segments in shared memory
+    const ParamSet* psp = a.pset;
+    const SegInfo* segp = a.sinfo;
+    const uint32_t* startp = a.seg_start;
+    uint32_t nseg = a.nseg, seg_end = a.n;
+    if (threadIdx.x == 0) {
+        uint32_t lo = 0, cnt = 0;
+        if (nt) {
+            lo = find_seg(a.seg_start, a.nseg, c_lo);
+            const uint32_t hi = find_seg(a.seg_start, a.nseg, c_hi - 1);
+            cnt = hi - lo + 1;
+        }
+        s_seg_lo = lo;
+        s_nseg = cnt;
+        s_nspk = 0;
+        s_fwork = 0;
+        s_nwork = 0;
+        for (uint32_t k = 0; k < L.S; ++k) {
+            mbar_init(s_bar + k, 1);               // full: producer arrive + tx bytes
+            mbar_init(s_bar + L.S + k, a.n_cons);  // empty: one arrive per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (a.npset <= kTileMaxPset) {
+        ParamSet* sp = reinterpret_cast<ParamSet*>(smem + L.pset);
+        for (uint32_t k = threadIdx.x; k < a.npset; k += blockDim.x) sp[k] = a.pset[k];
+        psp = sp;
+    }
+    if (s_nseg <= kTileMaxSeg) {
+        SegInfo* ss = reinterpret_cast<SegInfo*>(smem + L.seg);
+        uint32_t* st = reinterpret_cast<uint32_t*>(smem + L.start);
+        for (uint32_t k = threadIdx.x; k < s_nseg; k += blockDim.x) {
+            ss[k] = a.sinfo[s_seg_lo + k];
+            st[k] = a.seg_start[s_seg_lo + k];
+        }
+        segp = ss;
+        startp = st;
+        nseg = s_nseg;
+        seg_end = c_hi;
+    }
+    // the pending tile: P(S(t0 - 1)), delivered before this chunk
+    {
+        const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(((a.t0 - 1u) & 1u) ? a.pend1 : a.pend0);
+        ulonglong2* gz = reinterpret_cast<ulonglong2*>(((a.t0 - 1u) & 1u) ? a.pend1 : a.pend0);
+        for (uint32_t l = threadIdx.x; l < per; l += blockDim.x) {
+            ulonglong2 p = make_ulonglong2(0ull, 0ull);
+            if (l < nt) {
+                p = __ldcg(gp + c_lo + l);
+                __stcg(gz + c_lo + l, make_ulonglong2(0ull, 0ull));
+            }
+            s_pA[l] = (uint32_t)p.x;
+            s_pA[per + l] = (uint32_t)(p.x >> 32);
+            s_pA[2 * per + l] = (uint32_t)p.y;
+            s_pA[3 * per + l] = (uint32_t)(p.y >> 32);
+        }
+    }
+    __syncthreads();
+
+    const uint64_t pol_syn = policy_evict_first();  // synapse stream: read once
+    const uint64_t pol_f = a.f_policy == 2 ? policy_evict_last() : policy_evict_normal();
+    const uint32_t G = gridDim.x;
+    unsigned long long my_inner = 0, my_outer = 0;
+    uint32_t g_item = 0;  // ring stages consumed since launch
+    SegCursor cur_u, cur_n;
+    const uint32_t n_upd = (kTileThreads / 32) - 1;  // update warps
+    const bool is_cons = warp >= 1 && warp <= a.n_cons;
+
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
+    const uint32_t nph = a.steps + 1;
+    for (uint32_t ph = 0; ph < nph; ++ph) {
+        const bool doA = ph < a.steps;
+        const bool doE = ph >= 1;
+        const uint32_t tA = a.t0 + ph;
+        const uint32_t tE = tA - 1;
+        const uint32_t inj_ep = (doA && a.has_inj) ? a.inj_epoch[ph] : 0u;
+        uint32_t f_lo = 0, f_hi = 0;
+        if (doA && a.has_forced) {
+            f_lo = a.forced_off[ph];
+            f_hi = a.forced_off[ph + 1];
+        }
+        const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
+
+        if (warp == 0) {
+            // ---------------------------------------------------- P (producer)
+            if (doE) {
+                const uint32_t par = tE & 1u;
+                uint32_t* cntp = a.q_cnt + par * G + blockIdx.x;
+                const uint32_t cnt = __ldcg(cntp);
+                const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
+                TileRing rg{g_item, 0, 0, 0, 0, 0};
+                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
+                    uint4 it = make_uint4(0, 0, 0, 0);
+                    if (i0 + lane < cnt) it = __ldcg(items + i0 + lane);
+                    for (unsigned m = __ballot_sync(0xffffffffu, it.z != 0); m; m &= m - 1) {
+                        const int l = __ffs(m) - 1;
+                        const uint64_t b0 = ((uint64_t)__shfl_sync(0xffffffffu, it.y, l) << 32) |
+                                            __shfl_sync(0xffffffffu, it.x, l);
+                        const uint32_t ln = __shfl_sync(0xffffffffu, it.z, l);
+                        if (lane == 0) rg.add(a, smem, L, b0, ln, pol_syn);
+                    }
+                }
+                if (lane == 0) {
+                    if (!rg.open) rg.begin(smem, L);
+                    rg.commit(smem, L, 1);  // end marker (possibly with data)
+                    *cntp = 0u;             // this parity serves S(tE + 2) next
+                }
+                g_item = __shfl_sync(0xffffffffu, rg.ctr, 0);
+            }
+        } else {
+            // ---------------------------------------------------- U (update)
+            {
+                uint32_t vb_n = 0, iou_n = 0;
+                float4 j_n, g_n;
+                float isyn_n = 0.0f;
+                auto grab = [&]() {
+                    uint32_t c = 0;
+                    if (lane == 0) c = atomicAdd(&s_fwork, 1u);
+                    return __shfl_sync(0xffffffffu, c, 0);
+                };
+                auto load = [&](uint32_t i) {
+                    vb_n = ldp(a.v + i, pol_f);
+                    iou_n = __float_as_uint(ldp(a.i_ou + i, pol_f));
+                    if (doE) {
+                        j_n = ldp(a.j + i, pol_f);
+                        g_n = ldp(a.g + i, pol_f);
+                    } else {
+                        isyn_n = ldp(a.i_syn + i, pol_f);
+                    }
+                };
+                uint32_t ch = grab();
+                uint32_t i = c_lo + (ch << 5) + lane;
+                if (ch < nch && i < c_hi) load(i);
+                while (ch < nch) {
+                    const uint32_t vb0 = vb_n;
+                    const float iou = __uint_as_float(iou_n);
+                    float4 j = j_n;
+                    const float4 g = g_n;
+                    const float isyn_in = isyn_n;
+                    const uint32_t chn = grab();
+                    const uint32_t inext = c_lo + (chn << 5) + lane;
+                    if (chn < nch && inext < c_hi) load(inext);
+                    const bool live = i < c_hi;
+                    bool spiked = false;
+                    const uint32_t w_lo = c_lo + (ch << 5);
+                    const uint32_t seg = cur_u.find(startp, nseg, seg_end, w_lo,
+                                                    min(w_lo + 31u, c_hi - 1u),
+                                                    live ? i : c_hi - 1u, lane);
+                    uint32_t vb = vb0;
+                    if (live) {
+                        const SegInfo& S = segp[seg];
+                        const ParamSet& P = psp[S.pset];
+                        const uint32_t l = i - c_lo;
+                        const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                        float isyn;
+                        if (doE) {
+                            // gating_kernel (model.hpp:69-71) with deq(P_prev)
+                            // (engine.cpp:543-546) from the shared pending tile
+                            const float p0 = dequantize((int64_t)s_pA[l]);
+                            const float p1 = dequantize((int64_t)s_pA[per + l]);
+                            const float p2 = dequantize((int64_t)s_pA[2 * per + l]);
+                            const float p3 = dequantize((int64_t)s_pA[3 * per + l]);
+                            s_pA[l] = 0u;
+                            s_pA[per + l] = 0u;
+                            s_pA[2 * per + l] = 0u;
+                            s_pA[3 * per + l] = 0u;
+                            j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
+                            j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
+                            j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
+                            j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
+                            // current_kernel (model.hpp:73-81), u order, from 0.0f
+                            float c = 0.0f;
+                            c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
+                            c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
+                            c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
+                            c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
+                            isyn = c;
+                            // I_ou(tE) was advanced by phase ph - 1 (N below)
+                            if (!doA) stp(a.i_syn + i, isyn, pol_f);
+                            stp(a.j + i, j, pol_f);
+                        } else {
+                            isyn = isyn_in;
+                        }
+                        if (doA) {
+                            // membrane_kernel + threshold (engine.cpp:363-385)
+                            if (is_refrac(vb)) {
+                                const uint32_t r = (vb & 0x007fffffu) - 1u;
+                                vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
+                            } else {
+                                float inoise = iou;
+                                if (inj_ep) {
+                                    const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + S.voxel);
+                                    if (x != 0.0f) inoise = fadd(iou, x);
+                                }
+                                const float nv = fadd(
+                                    v, fmul(P.dt_over_c,
+                                            fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                                if (!isfinite(nv)) {
+                                    atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
+                                    vb = __float_as_uint(nv);
+                                } else if (nv >= P.v_th) {
+                                    spiked = true;
+                                    vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                                } else {
+                                    vb = __float_as_uint(nv);
+                                }
+                            }
+                            // forced spikes (engine.cpp:389-398): join unless already fired
+                            if (f_hi > f_lo && !spiked) {
+                                const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                                if (k < f_hi && __ldg(a.forced_local + k) == i) {
+                                    spiked = true;
+                                    vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
+                                }
+                            }
+                            stp(a.v + i, vb, pol_f);
+                        }
+                        // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
+                        if (a.n_probes) {
+                            uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                            while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                                const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
+                                if (doE) a.probe_i[row + ph - 1] = isyn;
+                                if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                                ++k;
+                            }
+                        }
+                    }
+                    // spike log staging + rates (engine.cpp:400-404), warp aggregated
+                    const unsigned ball = __ballot_sync(0xffffffffu, spiked);
+                    if (ball) {
+                        unsigned base = 0;
+                        if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (spiked) {
+                            const unsigned rank = __popc(ball & ((1u << lane) - 1u));
+                            if (base + rank < kSpkStage)
+                                s_spk[base + rank] = i;
+                            else
+                                a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                            const uint32_t unit = segp[seg].unit;
+                            const unsigned peers = __match_any_sync(ball, unit);
+                            if ((unsigned)__ffs(peers) - 1u == lane)
+                                atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
+                            // deliveries of S(tA): one queue item per tile the
+                            // row touches (engine.cpp:439-442 / 444-464), and the
+                            // FLOP tally of the whole row (engine.cpp:459-463)
+                            const uint32_t s = a.src_self + i;
+                            const uint64_t row = ldg64(a.off + s);
+                            const uint64_t len = ldg64(a.off + s + 1) - row;
+                            const uint32_t in = __ldg(a.inner + s);
+                            my_inner += 2ull * in;
+                            my_outer += 2ull * (len - in);
+                            const uint32_t par = tA & 1u;
+                            const uint64_t k1 = __ldg(a.tl_off + s + 1);
+                            for (uint64_t k = __ldg(a.tl_off + s); k < k1; ++k) {
+                                const uint4 sg = __ldg(a.tl + k);
+                                const uint32_t pos = atomicAdd(a.q_cnt + par * G + sg.x, 1u);
+                                const uint64_t b = row + sg.y;
+                                a.q[(size_t)par * a.q_total + __ldg(a.q_base + sg.x) + pos] =
+                                    make_uint4((uint32_t)b, (uint32_t)(b >> 32), sg.z, 0u);
+                            }
+                        }
+                    }
+                    ch = chn;
+                    i = inext;
+                }
+            }
+            // every update warp has consumed its neurons' pending sums
+            named_sync(1, n_upd * 32);
+
+            if (is_cons) {
+                // ------------------------------------------------ C (consumers)
+                if (doE) {
+                    uint64_t* full = s_bar;
+                    uint64_t* empty = s_bar + L.S;
+                    const uint32_t ct = threadIdx.x - 32, cn = a.n_cons * 32;
+                    for (;;) {
+                        const uint32_t st = g_item % L.S;
+                        mbar_wait(full + st, (g_item / L.S) & 1u);
+                        ++g_item;
+                        const TStageMeta* m = reinterpret_cast<const TStageMeta*>(smem + L.meta + st * kMetaBytes);
+                        const uint32_t n_e = m->n, last = m->end;
+                        const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * L.tb);
+                        const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * L.wb);
+                        uint32_t sg = 0;
+                        for (uint32_t e = ct; e < n_e; e += cn) {
+                            while (e >= m->pre[sg + 1]) ++sg;
+                            const uint32_t r = e - m->pre[sg];
+                            const uint32_t t = tg[m->tb[sg] + r];
+                            const uint32_t l = (t & 0x7fffffffu) - c_lo;
+                            const uint32_t cls2 = (t >> 31) * 2u * per;
+                            const uint64_t wq = wv[m->wb[sg] + r];
+                            atomicAdd(s_pA + cls2 + l, (uint32_t)wq);
+                            atomicAdd(s_pA + cls2 + per + l, (uint32_t)(wq >> 32));
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(empty + st);
+                        if (last) break;
+                    }
+                }
+            } else if (doA) {
+                // ------------------------------------------------ N (OU step to tA)
+                // ou_kernel (model.hpp:88-90) with xi = stream word tA
+                // (engine.cpp:551-558): consumed by E(tA) in phase ph + 1
+                for (;;) {
+                    uint32_t c = 0;
+                    if (lane == 0) c = atomicAdd(&s_nwork, 1u);
+                    c = __shfl_sync(0xffffffffu, c, 0);
+                    if (c >= nch) break;
+                    const uint32_t w_lo = c_lo + (c << 5);
+                    const uint32_t i = w_lo + lane;
+                    const bool live = i < c_hi;
+                    const uint32_t seg = cur_n.find(startp, nseg, seg_end, w_lo,
+                                                    min(w_lo + 31u, c_hi - 1u),
+                                                    live ? i : c_hi - 1u, lane);
+                    if (live) {
+                        const SegInfo& S = segp[seg];
+                        const ParamSet& P = psp[S.pset];
+                        float iou = ldp(a.i_ou + i, pol_f);
+                        float xi = 0.0f;
+                        if (P.sigma_pos) {
+                            const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
+                            xi = stream_xi(mix_key(a.ou_root, gid), tA);
+                        }
+                        iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                        stp(a.i_ou + i, iou, pol_f);
+                    }
+                }
+            }
+        }
+
+        // flush the CTA's staged spikes with one log reservation
+        __syncthreads();
+        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
+        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x) a.spk[log_base + s_base + k] = s_spk[k];
+
+        grid_barrier(
+            ctl,
+            [&] {
+                if (doA) a.seg_end[ph] = ctl->spk_cursor;
+                if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
+                a.phase_ns[ph + 1] = globaltimer();
+                ctl->stop = atomicAdd(&ctl->err, 0ull) != ~0ull ? 1u : 0u;
+            },
+            [&] {});
+        if (threadIdx.x == 0) {
+            s_stop = (int)ld_acquire(&ctl->stop);
+            s_nspk = 0;
+            s_fwork = 0;
+            s_nwork = 0;
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+    // the pending tile P(S(t_last)) back to the global buffer of its parity
+    {
+        const uint32_t tl = a.t0 + a.steps - 1u;
+        ulonglong2* gp = reinterpret_cast<ulonglong2*>((tl & 1u) ? a.pend1 : a.pend0);
+        for (uint32_t l = threadIdx.x; l < nt; l += blockDim.x)
+            __stcg(gp + c_lo + l,
+                   make_ulonglong2((uint64_t)s_pA[l] | ((uint64_t)s_pA[per + l] << 32),
+                                   (uint64_t)s_pA[2 * per + l] | ((uint64_t)s_pA[3 * per + l] << 32)));
+    }
+    if (my_inner | my_outer) {
+        atomicAdd(&ctl->flops_inner, my_inner);
+        atomicAdd(&ctl->flops_outer, my_outer);
+    }
+}
+
+// ------------------------------------------------------- tile tables (load)
+// Per source row (sorted by target): the runs of entries whose targets fall
+// in one tile.  Pass 0 counts runs per source; pass 1 writes {tile, first
+// entry (row-relative), length}.  One warp per source.
+template <int PASS>
+__global__ void tile_segments_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt,
+                                     uint32_t n_src, uint32_t per,
+                                     unsigned long long* __restrict__ cnt,   // PASS 0: [n_src]
+                                     const unsigned long long* __restrict__ tl_off,  // PASS 1
+                                     uint4* __restrict__ tl, uint32_t* __restrict__ tile_cap) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t s = warp; s < n_src; s += nwarps) {
+        const uint64_t r0 = off[s], r1 = off[s + 1];
+        uint32_t runs = 0;
+        uint64_t out = PASS ? tl_off[s] : 0ull;
+        uint32_t prev_tile = 0xffffffffu;
+        for (uint64_t k0 = r0; k0 < r1; k0 += 32) {
+            const uint64_t k = k0 + lane;
+            const uint32_t t = k < r1 ? (tgt[k] & 0x7fffffffu) / per : 0xffffffffu;
+            uint32_t up = __shfl_up_sync(0xffffffffu, t, 1);
+            if (lane == 0) up = prev_tile;
+            const bool start = k < r1 && t != up;
+            const unsigned ball = __ballot_sync(0xffffffffu, start);
+            if (PASS == 1 && start) {
+                const uint64_t at = out + __popc(ball & ((1u << lane) - 1u));
+                tl[at] = make_uint4(t, (uint32_t)(k - r0), 0u, 0u);
+                atomicAdd(tile_cap + t, 1u);
+            }
+            out += __popc(ball);
+            runs += __popc(ball);
+            prev_tile = __shfl_sync(0xffffffffu, t, 31);
+        }
+        if (PASS == 0) {
+            if (lane == 0) cnt[s] = runs;
+        } else {
+            __syncwarp();
+            const uint64_t b = tl_off[s], e = tl_off[s + 1];
+            for (uint64_t q = b + lane; q < e; q += 32) {
+                const uint32_t beg = __ldcg(&tl[q].y);
+                const uint32_t nxt = q + 1 < e ? __ldcg(&tl[q + 1].y) : (uint32_t)(r1 - r0);
+                tl[q].z = nxt - beg;
+            }
+        }
+    }
+}
+
+}  // namespace vxb

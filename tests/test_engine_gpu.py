@@ -391,11 +391,13 @@ def test_acceptance_1_multi_worker_equivalence():
         assert np.array_equal(state, ref_state)
 
 
-@pytest.mark.parametrize("dyn", ["0", "1"])
-def test_static_and_dynamic_delivery_match_reference(monkeypatch, dyn):
-    """Both producer schedules — static round-robin rows (VXB_DYN=0) and the
-    default block-major dynamic chunks — are bit-exact (config 1 shape)."""
+@pytest.mark.parametrize("path,dyn", [("l2", "0"), ("l2", "1"), ("tile", "1")])
+def test_static_and_dynamic_delivery_match_reference(monkeypatch, path, dyn):
+    """Every delivery schedule is bit-exact (config 1 shape): the l2_atomic
+    path's static round-robin rows (VXB_DYN=0) and block-major dynamic
+    chunks, and the SM-tile path (shared-memory pending tiles)."""
     monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", path)
     monkeypatch.setenv("VXB_DYN", dyn)
     cfg = make_config(seed=1, voxels=1, npv=10000, k_in=100, dt_ms=0.1, steps=3000)
     net = RefNet(cfg)
@@ -427,6 +429,7 @@ def test_l2_blocked_delivery_matches_reference(monkeypatch):
     blocks delivered in order), forced on a small network with 2048-neuron
     blocks: bit-exact against the reference."""
     monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", "l2")
     monkeypatch.setenv("VXB_BLOCK_NEURONS", "2048")
     net = RefNet(make_config(seed=1401, voxels=10, npv=1000, k_in=100, rho=6 / 25))
     opt = SimOptions(steps=300, probe_gids=[5, 5000, 9999])
@@ -443,7 +446,7 @@ def test_advance_without_forced_spikes_or_injection_after_one_with():
     (engine.cpp:352-361, 389-398): an advance whose window holds none must
     not replay the previous advance's tables, and a longer later advance
     must not read past them."""
-    net = RefNet(make_config(seed=29, voxels=2, npv=300, k_in=12, rho=0.3), even_workers=2)
+    net = RefNet(make_config(seed=29, voxels=3, npv=200, k_in=12, rho=0.3), even_workers=2)
     g = net.tables.workers[0].neurons["gid"]
     opt = SimOptions(steps=130, probe_gids=[int(g[3]), 450],
                      forced_spikes=[ForcedSpike(10, int(g[3])), ForcedSpike(40, int(g[7]))],
@@ -459,4 +462,27 @@ def test_advance_without_forced_spikes_or_injection_after_one_with():
     assert_same(a, ra)
     assert_same(b, rb)
     for w in range(2):
+        assert np.array_equal(snaps[w], rs.membrane_snapshot(w))
+
+
+@pytest.mark.parametrize("path", ["tile", "l2"])
+def test_ring_multiworker_both_paths(monkeypatch, path):
+    """3 workers on one device, both delivery paths, two advances: the
+    SM-tile path (default for shards that fit on chip) and the l2_atomic
+    path give the reference's results bit for bit."""
+    monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", path)
+    net = RefNet(hot_cfg(seed=31, voxels=5, npv=900, k_in=40, rho=0.3), even_workers=3)
+    opt = SimOptions(steps=150, probe_gids=[3, 1000, 4499])
+    with SimInstance(net.tables, opt) as sim:
+        assert sim.schedule_info()["path"] == ("sm_tile" if path == "tile" else "l2_atomic")
+        a = sim.advance(70)
+        b = sim.advance(80)
+        snaps = [sim.membrane_snapshot(w) for w in range(3)]
+    rs = RefSim(net, opt)
+    ra, rb = rs.advance(70), rs.advance(80)
+    assert ra.total_spikes > 0 and rb.total_spikes > 0
+    assert_same(a, ra)
+    assert_same(b, rb)
+    for w in range(3):
         assert np.array_equal(snaps[w], rs.membrane_snapshot(w))

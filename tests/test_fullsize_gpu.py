@@ -59,13 +59,18 @@ def test_config2_piecewise_equals_whole():
 
 
 def test_config2_delivery_schedule_invariance(monkeypatch):
+    """Full config 2: SM-tile path (the default) == l2_atomic path with the
+    dynamic deal == l2_atomic path with the static deal."""
     cfg = _config2()
+    tile = _run(cfg, [40])
     monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", "l2")
     monkeypatch.setenv("VXB_DYN", "1")
     dyn = _run(cfg, [40])
     monkeypatch.setenv("VXB_DYN", "0")
     static = _run(cfg, [40])
     _same(dyn, static)
+    _same(tile, dyn)
 
 
 def test_config2_two_workers_on_one_device():

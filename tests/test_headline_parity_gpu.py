@@ -79,13 +79,17 @@ def _compare(cfg, steps, chunks, expect, tuning=None, monkeypatch=None):
     return ref, vr_ref, sched
 
 
-def test_config2_regime_ring12_k1000_one_bio_second():
+@pytest.mark.parametrize("path", ["tile", "l2"])
+def test_config2_regime_ring12_k1000_one_bio_second(monkeypatch, path):
     """Config 2's operating point on a 12-voxel ring (1.2e8 synapses), 1000
-    steps of dt = 1 ms in two advances, generated tables, one-spike chunks."""
+    steps of dt = 1 ms in two advances, generated tables: the SM-tile path
+    bench.py takes on one GPU, and the l2_atomic path (one-spike chunks)."""
     import bench
     cfg = bench.workload_cfg(voxels=12)
-    ref, vr, _ = _compare(cfg, 1000, [400, 600],
-                          {"l2_blocks": 1, "dynamic_deal": 1, "ch_max": 1})
+    expect = ({"path": "sm_tile"} if path == "tile" else
+              {"path": "l2_atomic", "l2_blocks": 1, "dynamic_deal": 1, "ch_max": 1})
+    ref, vr, _ = _compare(cfg, 1000, [400, 600], expect, tuning={"VXB_PATH": path},
+                          monkeypatch=monkeypatch)
     rate = ref.total_spikes / (120_000 * 1.0)
     assert 7.0 < rate < 13.0, rate  # the calibrated ~10 Hz point
     assert vr.min() > 0
@@ -107,6 +111,26 @@ def test_config3_regime_dti_slice_l2_blocked(monkeypatch, tmp_path):
            "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + bench.G_LOC_10HZ[1:],
                                      "ou_mean": ou}}}
     ref, vr, sched = _compare(cfg, 400, [150, 250],
-                              {"l2_blocks": 4, "stage_entries": 1024, "ch_max": 32},
-                              tuning={"VXB_BLOCK_NEURONS": "50000"}, monkeypatch=monkeypatch)
+                              {"path": "l2_atomic", "l2_blocks": 4, "stage_entries": 1024,
+                               "ch_max": 32},
+                              tuning={"VXB_PATH": "l2", "VXB_BLOCK_NEURONS": "50000"},
+                              monkeypatch=monkeypatch)
+    assert ref.total_spikes > 100_000
+
+
+def test_config3_slice_sm_tile_path(monkeypatch, tmp_path):
+    """The same DTI-like slice shape (lognormal voxel sizes, K = 500, greedy
+    2-worker partition) on the SM-tile path: short, irregular (source,
+    tile) segments."""
+    import bench
+    path = tmp_path / "dti200.txt"
+    netgen.write_connectome_file(netgen.dti_like_connectome(total_neurons=200_000), path)
+    ampa, ou = bench.K500_POINTS[10]
+    cfg = {"seed": bench.SEED, "dt_ms": 1.0, "steps": 300, "workers": 2,
+           "scheduler": "loopback",
+           "connectome": {"kind": "file", "path": str(path)},
+           "partition": {"method": "greedy"},
+           "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + bench.G_LOC_10HZ[1:],
+                                     "ou_mean": ou}}}
+    ref, _, _ = _compare(cfg, 300, [100, 200], {"path": "sm_tile"})
     assert ref.total_spikes > 100_000

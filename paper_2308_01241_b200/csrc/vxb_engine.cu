@@ -211,7 +211,7 @@ struct Engine {
     // SM-tile path (vxb_tile.cuh): pending sums in shared memory, one CTA per
     // SM; chosen when the shard fits on chip (tile_path), else l2_atomic
     bool tile_path = false;
-    uint32_t tile_per = 0, tile_stages = 0, tile_cons = 8, tile_smem = 0, tile_grid = 0;
+    uint32_t tile_per = 0, tile_cons = 12, tile_smem = 0, tile_grid = 0;
     uint64_t q_total = 0;
     DevBuf<unsigned long long> d_tl_off;
     DevBuf<uint4> d_tl;
@@ -1163,7 +1163,7 @@ void Engine::share_tables(const Engine& d) {
     block_n = d.block_n;
     tile_path = d.tile_path;
     tile_per = d.tile_per;
-    tile_stages = d.tile_stages;
+    tile_cons = d.tile_cons;
     tile_smem = d.tile_smem;
     tile_grid = d.tile_grid;
     q_total = d.q_total;
@@ -1275,9 +1275,9 @@ void Engine::sort_rows() {
 
 // SM-tile path: every CTA (one per SM) owns a contiguous tile of neurons and
 // keeps their pending sums in shared memory (vxb_tile.cuh).  Eligible when
-// the pending tile fits beside a >= 3-stage delivery ring (shards up to
-// ~1.3M neurons on 148 SMs), on one GPU, with carry-free packed sums.  Rows
-// are sorted by target and cut into per-tile segments here, once.
+// the pending tile fits in a CTA's shared memory (shards up to ~2M neurons
+// on 148 SMs), on one GPU, with carry-free packed sums.  Rows are sorted by
+// target and cut into per-tile segments here, once.
 void Engine::setup_tiles() {
     tile_path = false;
     const char* force = knob("VXB_PATH", &knobs);
@@ -1287,14 +1287,10 @@ void Engine::setup_tiles() {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     const uint32_t per = (uint32_t)((((uint64_t)n + sms - 1) / sms + 31) & ~31ull);
-    uint32_t S = kTileMaxStages;
-    while (S >= 3 && TileLayout(per, S).total > (uint32_t)optin) --S;
-    if (S < 3) return;
+    const TileLayout L(per);
+    if (L.total > (uint32_t)optin) return;
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
-        tile_cons = (uint32_t)std::min(20, std::max(1, std::atoi(c)));
-    if (const char* c = knob("VXB_TILE_STAGES", &knobs))
-        S = std::min(S, (uint32_t)std::max(3, std::atoi(c)));
-    const TileLayout L(per, S);
+        tile_cons = (uint32_t)std::min(23, std::max(1, std::atoi(c)));
     CK(cudaFuncSetAttribute((const void*)tile_kernel,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     int per_sm = 0;
@@ -1345,7 +1341,6 @@ void Engine::setup_tiles() {
     CK(cudaStreamSynchronize(stream));
     tile_path = true;
     tile_per = per;
-    tile_stages = S;
     tile_smem = L.total;
     tile_grid = (uint32_t)sms;
     (void)tiles;
@@ -1724,14 +1719,13 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     const bool prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
     DevBuf<unsigned long long> d_prof;
     if (prof) {
-        d_prof.alloc(2ull * (steps + 1) * grid);
+        d_prof.alloc((tile_path ? 4ull * tile_grid : 2ull * grid) * (steps + 1));
         d_prof.zero(stream);
         a.prof = d_prof.p;
     }
 
     if (tile_path) {
         a.tile_n = tile_per;
-        a.ring_stages = tile_stages;
         a.n_cons = tile_cons;
         a.q_total = (uint32_t)q_total;
         a.tl_off = d_tl_off.p;
@@ -1772,7 +1766,35 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         for (auto x : pw) exchange_wait_ms += x * 1e-6;
     }
     CK(cudaStreamSynchronize(stream));
-    if (prof) {  // per phase: mean / max over CTAs of delivery and update end (us)
+    if (prof && tile_path) {  // per phase: mean / max over CTAs of each part's end (us)
+        std::vector<unsigned long long> pr(d_prof.n), pn(steps + 2);
+        CK(cudaMemcpy(pr.data(), d_prof.p, 8 * pr.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(pn.data(), d_phase_ns.p, 8 * pn.size(), cudaMemcpyDeviceToHost));
+        double sum[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0}, sp = 0;
+        uint32_t cnt[4] = {0, 0, 0, 0};
+        for (uint32_t ph = 1; ph < steps; ++ph) {
+            const double t0 = (double)pn[ph];
+            sp += (double)(pn[ph + 1] - pn[ph]);
+            double pm[4] = {0, 0, 0, 0};
+            for (uint32_t b = 0; b < tile_grid; ++b)
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned long long x = pr[4 * ((size_t)ph * tile_grid + b) + k];
+                    if (!x) continue;
+                    sum[k] += x - t0;
+                    ++cnt[k];
+                    pm[k] = std::max(pm[k], x - t0);
+                }
+            for (int k = 0; k < 4; ++k) mx[k] += pm[k];
+        }
+        const double np_ = std::max(1u, steps - 1);
+        std::fprintf(stderr,
+                     "vxb tile phase profile (us): phase %.1f | update end %.1f/%.1f | producer "
+                     "%.1f/%.1f | consumers %.1f/%.1f | noise %.1f/%.1f (mean/max over CTAs)\n",
+                     sp / np_ / 1e3, sum[0] / std::max(1u, cnt[0]) / 1e3, mx[0] / np_ / 1e3,
+                     sum[1] / std::max(1u, cnt[1]) / 1e3, mx[1] / np_ / 1e3,
+                     sum[2] / std::max(1u, cnt[2]) / 1e3, mx[2] / np_ / 1e3,
+                     sum[3] / std::max(1u, cnt[3]) / 1e3, mx[3] / np_ / 1e3);
+    } else if (prof) {  // per phase: mean / max over CTAs of delivery and update end (us)
         std::vector<unsigned long long> pr(d_prof.n), pn(steps + 2);
         CK(cudaMemcpy(pr.data(), d_prof.p, 8 * pr.size(), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(pn.data(), d_phase_ns.p, 8 * pn.size(), cudaMemcpyDeviceToHost));
@@ -1870,10 +1892,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
 std::string Engine::schedule_info() const {
     if (tile_path)
         return fmt("{\"path\":\"sm_tile\",\"kernel\":\"vxb::tile_kernel\",\"grid\":%u,"
-                   "\"threads\":%d,\"smem_bytes\":%u,\"tile_neurons\":%u,\"ring_stages\":%u,"
-                   "\"stage_entries\":%u,\"consumer_warps\":%u,\"queue_items\":%llu,"
+                   "\"threads\":%d,\"smem_bytes\":%u,\"tile_neurons\":%u,"
+                   "\"unroll\":%u,\"consumer_warps\":%u,\"queue_items\":%llu,"
                    "\"state_l2_policy\":%u,\"packed_pending\":%d,\"world\":%u,\"knobs\":{",
-                   tile_grid, kTileThreads, tile_smem, tile_per, tile_stages, kTileSE, tile_cons,
+                   tile_grid, kTileThreads, tile_smem, tile_per, kTileUnroll, tile_cons,
                    (unsigned long long)q_total, f_policy, (int)packed, world) +
                knobs + "}}";
     return fmt("{\"path\":\"l2_atomic\",\"kernel\":\"vxb::step_kernel\",\"grid\":%d,"

@@ -192,7 +192,6 @@ struct StepArgs {
     const unsigned long long* dst_mask;  // per local neuron: shards holding its targets
     // ---- SM-tile path (tile_kernel, vxb_tile.cuh) ----
     uint32_t tile_n;            // neurons per CTA tile (multiple of 32)
-    uint32_t ring_stages;       // delivery ring depth (runtime)
     uint32_t n_cons;            // consumer warps
     uint32_t q_total;           // queue items per parity
     const unsigned long long* tl_off;  // per global source: first tile segment (n_src + 1)

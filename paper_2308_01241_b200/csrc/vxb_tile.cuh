@@ -16,19 +16,22 @@
 // that owns its target; nothing is re-read or reduced twice.
 //
 // Phase ph of a chunk (tA = t0 + ph, tE = tA - 1), per CTA:
-//   U  (warps 1..23)  E(tE) + A(tA) of the tile's neurons: gating with the
+//   U  (all warps)    E(tE) + A(tA) of the tile's neurons: gating with the
 //                     shared-memory pending P(S(tE-1)) (zeroed after the
 //                     read), current, membrane; the OU current I_ou(tE) was
 //                     already advanced in phase ph - 1 (see N).  Spikes of
 //                     S(tA) are logged, counted and bucketed into the tile
 //                     queues of parity tA.
-//   P  (warp 0)       producer: bulk-copies the segments queued for this
-//                     tile in parity tE into an 8-stage ring while U runs.
-//   after U:
-//   C  (warps 1..C)   consumers: drain the ring into the pending tile with
-//                     shared atomics — P(S(tE)), consumed by E(tA) in ph+1.
+//   then, concurrently:
+//   C  (warps 0..C-1) consumers: take the segments queued for this tile in
+//                     parity tE one per grab, stream their entries with
+//                     plain loads (kTileUnroll in flight per lane; a TMA bulk
+//                     copy per ~200-entry segment measured ~0.3 us of issue
+//                     each, 9x slower) and add them into the pending tile
+//                     with shared atomics — P(S(tE)), consumed by E(tA) in
+//                     phase ph + 1.
 //   N  (other warps)  advance I_ou to tA (fp64 Box-Muller noise, ou_kernel)
-//                     for the tile, overlapping the atomics.
+//                     for the tile, overlapping the delivery.
 //   grid barrier.
 // Moving the OU step one phase earlier is exact: I_ou(t) depends only on
 // I_ou(t-1) and xi(gid, t) (ou_kernel, model.hpp:88-90; engine.cpp:551-558).
@@ -41,28 +44,19 @@
 
 namespace vxb {
 
-constexpr int kTileThreads = 768;       // 24 warps: 1 producer + 23 update/consume/noise
-constexpr uint32_t kTileSE = 1024;      // synapse entries per ring stage
-constexpr uint32_t kTileMaxStages = 8;
+constexpr int kTileThreads = 768;       // 24 warps: update, then consume / advance I_ou
+constexpr uint32_t kTileUnroll = 4;     // synapse entries in flight per consumer lane
 constexpr uint32_t kTileMaxSeg = 64;    // a tile's parameter segments kept in shared memory
 constexpr uint32_t kTileMaxPset = 32;
 
 // Dynamic shared memory of tile_kernel.
 struct TileLayout {
-    uint32_t per, S, se, tb, wb;
-    uint32_t pend, tgt, w, bar, meta, pset, seg, start, spk, total;
-    __host__ __device__ TileLayout(uint32_t per_, uint32_t stages) {
+    uint32_t per;
+    uint32_t pend, pset, seg, start, spk, total;
+    __host__ __device__ explicit TileLayout(uint32_t per_) {
         per = per_;
-        S = stages;
-        se = kTileSE;
-        tb = (se + 8) * 4;
-        wb = (se + 4) * 8;
-        pend = 0;                   // AMPA[per], NMDA[per], GABAA[per], GABAB[per] (u32)
-        tgt = pend + 16 * per;      // per is a multiple of 32: 16-byte aligned
-        w = tgt + S * tb;
-        bar = w + S * wb;           // full[S], then empty[S]
-        meta = bar + 2 * S * 8;
-        pset = (meta + S * kMetaBytes + 127) & ~127u;
+        pend = 0;  // AMPA[per], NMDA[per], GABAA[per], GABAB[per] (u32)
+        pset = (pend + 16 * per + 127) & ~127u;
         seg = pset + kTileMaxPset * (uint32_t)sizeof(ParamSet);
         start = seg + kTileMaxSeg * (uint32_t)sizeof(SegInfo);
         spk = (start + (kTileMaxSeg + 1) * 4 + 15) & ~15u;
@@ -70,68 +64,19 @@ struct TileLayout {
     }
 };
 
-// Producer side of the tile ring (lane 0 of warp 0): packs queued row
-// segments into stages of kTileSE entries, one bulk copy of targets and one
-// of weights per segment piece, expect_tx per piece, one arrive per stage.
-struct TileRing {
-    uint32_t ctr;  // stages committed since launch (stage = ctr % S)
-    uint32_t open;
-    uint32_t ns, toff, woff, total;
-
-    __device__ __forceinline__ void begin(unsigned char* smem, const TileLayout& L) {
-        const uint32_t st = ctr % L.S;
-        uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.bar) + L.S;
-        mbar_wait(empty + st, ((ctr / L.S) & 1u) ^ 1u);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        open = 1;
-        ns = toff = woff = total = 0;
-    }
-    __device__ __forceinline__ void commit(unsigned char* smem, const TileLayout& L, uint32_t end) {
-        const uint32_t st = ctr % L.S;
-        TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
-        m->pre[ns] = total;
-        m->n = total;
-        m->nseg = ns;
-        m->end = end;
-        mbar_arrive(reinterpret_cast<uint64_t*>(smem + L.bar) + st);
-        ++ctr;
-        open = 0;
-    }
-    __device__ __forceinline__ void add(const StepArgs& a, unsigned char* smem, const TileLayout& L,
-                                        uint64_t b0, uint64_t len, uint64_t pol) {
-        while (len) {
-            if (!open) begin(smem, L);
-            const int room_t = (int)L.se - (int)toff, room_w = (int)L.se - (int)woff;
-            const int room = room_t < room_w ? room_t : room_w;
-            if (ns == (uint32_t)kSegPerStage || room <= 0) {
-                commit(smem, L, 0);
-                continue;
-            }
-            const uint32_t st = ctr % L.S;
-            TStageMeta* m = reinterpret_cast<TStageMeta*>(smem + L.meta + st * kMetaBytes);
-            // the 16-byte aligned supersets copied stay within the stage's
-            // (se + 8) target and (se + 4) weight slots
-            const uint64_t take = min(len, (uint64_t)room);
-            const uint64_t b1 = b0 + take;
-            const uint64_t t0 = b0 & ~3ull, w0 = b0 & ~1ull;
-            const uint32_t tn = (uint32_t)(((b1 + 3) & ~3ull) - t0);
-            const uint32_t wn = (uint32_t)(((b1 + 1) & ~1ull) - w0);
-            m->pre[ns] = total;
-            m->tb[ns] = toff + (uint32_t)(b0 - t0);
-            m->wb[ns] = woff + (uint32_t)(b0 - w0);
-            uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar) + st;
-            mbar_expect_tx_only(full, tn * 4 + wn * 8);
-            bulk_g2s(smem + L.tgt + st * L.tb + toff * 4, a.tgt + t0, tn * 4, full, pol);
-            bulk_g2s(smem + L.w + st * L.wb + woff * 8, a.w + w0, wn * 8, full, pol);
-            total += (uint32_t)take;
-            toff += tn;
-            woff += wn;
-            ++ns;
-            b0 = b1;
-            len -= take;
-        }
-    }
-};
+// Streamed synapse entries: read once, not kept in L1, evict-first in L2.
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                 : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
 
 // Warp-uniform parameter-segment lookup over the tile's segment table:
 // starts[0..nseg) ascending, `end` = first neuron past the last segment.
@@ -154,19 +99,15 @@ struct SegCursor {
     }
 };
 
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
 __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const TileLayout L(a.tile_n, a.ring_stages);
+    const TileLayout L(a.tile_n);
     uint32_t* s_pA = reinterpret_cast<uint32_t*>(smem + L.pend);  // [4][per] receptor sums
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + L.bar);
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
-    __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_base;
+    __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base;
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
+    __shared__ unsigned long long s_t[4];  // phase profile: U end, -, consumers, noise
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t per = a.tile_n;
@@ -192,11 +133,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         s_nspk = 0;
         s_fwork = 0;
         s_nwork = 0;
-        for (uint32_t k = 0; k < L.S; ++k) {
-            mbar_init(s_bar + k, 1);               // full: producer arrive + tx bytes
-            mbar_init(s_bar + L.S + k, a.n_cons);  // empty: one arrive per consumer warp
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_iwork = 0;
+        s_t[0] = s_t[1] = s_t[2] = s_t[3] = 0;
     }
     __syncthreads();
     if (a.npset <= kTileMaxPset) {
@@ -238,10 +176,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     const uint64_t pol_f = a.f_policy == 2 ? policy_evict_last() : policy_evict_normal();
     const uint32_t G = gridDim.x;
     unsigned long long my_inner = 0, my_outer = 0;
-    uint32_t g_item = 0;  // ring stages consumed since launch
     SegCursor cur_u, cur_n;
-    const uint32_t n_upd = (kTileThreads / 32) - 1;  // update warps
-    const bool is_cons = warp >= 1 && warp <= a.n_cons;
+    const bool is_cons = warp < a.n_cons;
 
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
@@ -258,33 +194,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         }
         const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
 
-        if (warp == 0) {
-            // ---------------------------------------------------- P (producer)
-            if (doE) {
-                const uint32_t par = tE & 1u;
-                uint32_t* cntp = a.q_cnt + par * G + blockIdx.x;
-                const uint32_t cnt = __ldcg(cntp);
-                const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
-                TileRing rg{g_item, 0, 0, 0, 0, 0};
-                for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-                    uint4 it = make_uint4(0, 0, 0, 0);
-                    if (i0 + lane < cnt) it = __ldcg(items + i0 + lane);
-                    for (unsigned m = __ballot_sync(0xffffffffu, it.z != 0); m; m &= m - 1) {
-                        const int l = __ffs(m) - 1;
-                        const uint64_t b0 = ((uint64_t)__shfl_sync(0xffffffffu, it.y, l) << 32) |
-                                            __shfl_sync(0xffffffffu, it.x, l);
-                        const uint32_t ln = __shfl_sync(0xffffffffu, it.z, l);
-                        if (lane == 0) rg.add(a, smem, L, b0, ln, pol_syn);
-                    }
-                }
-                if (lane == 0) {
-                    if (!rg.open) rg.begin(smem, L);
-                    rg.commit(smem, L, 1);  // end marker (possibly with data)
-                    *cntp = 0u;             // this parity serves S(tE + 2) next
-                }
-                g_item = __shfl_sync(0xffffffffu, rg.ctr, 0);
-            }
-        } else {
+        {
             // ---------------------------------------------------- U (update)
             {
                 uint32_t vb_n = 0, iou_n = 0;
@@ -443,39 +353,54 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     i = inext;
                 }
             }
-            // every update warp has consumed its neurons' pending sums
-            named_sync(1, n_upd * 32);
+            // every warp has consumed its neurons' pending sums
+            __syncthreads();
+            if (a.prof && threadIdx.x == 0) s_t[0] = globaltimer();
 
             if (is_cons) {
                 // ------------------------------------------------ C (consumers)
+                // the segments queued for this tile (parity tE), one item per
+                // warp grab; lanes stream the entries with kTileUnroll loads
+                // in flight each and add them with two shared atomics
                 if (doE) {
-                    uint64_t* full = s_bar;
-                    uint64_t* empty = s_bar + L.S;
-                    const uint32_t ct = threadIdx.x - 32, cn = a.n_cons * 32;
+                    const uint32_t par = tE & 1u;
+                    const uint32_t cnt = __ldcg(a.q_cnt + par * G + blockIdx.x);
+                    const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
                     for (;;) {
-                        const uint32_t st = g_item % L.S;
-                        mbar_wait(full + st, (g_item / L.S) & 1u);
-                        ++g_item;
-                        const TStageMeta* m = reinterpret_cast<const TStageMeta*>(smem + L.meta + st * kMetaBytes);
-                        const uint32_t n_e = m->n, last = m->end;
-                        const uint32_t* tg = reinterpret_cast<const uint32_t*>(smem + L.tgt + st * L.tb);
-                        const uint64_t* wv = reinterpret_cast<const uint64_t*>(smem + L.w + st * L.wb);
-                        uint32_t sg = 0;
-                        for (uint32_t e = ct; e < n_e; e += cn) {
-                            while (e >= m->pre[sg + 1]) ++sg;
-                            const uint32_t r = e - m->pre[sg];
-                            const uint32_t t = tg[m->tb[sg] + r];
-                            const uint32_t l = (t & 0x7fffffffu) - c_lo;
-                            const uint32_t cls2 = (t >> 31) * 2u * per;
-                            const uint64_t wq = wv[m->wb[sg] + r];
-                            atomicAdd(s_pA + cls2 + l, (uint32_t)wq);
-                            atomicAdd(s_pA + cls2 + per + l, (uint32_t)(wq >> 32));
+                        uint32_t it = 0;
+                        if (lane == 0) it = atomicAdd(&s_iwork, 1u);
+                        it = __shfl_sync(0xffffffffu, it, 0);
+                        if (it >= cnt) break;
+                        const uint4 d = __ldcg(items + it);
+                        const uint64_t beg = ((uint64_t)d.y << 32) | d.x;
+                        const uint32_t len = d.z;
+                        const uint32_t* tg = a.tgt + beg;
+                        const uint64_t* wv = a.w + beg;
+                        for (uint32_t k0 = 0; k0 < len; k0 += 32 * kTileUnroll) {
+                            uint32_t t[kTileUnroll];
+                            uint64_t wq[kTileUnroll];
+#pragma unroll
+                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
+                                const uint32_t k = k0 + u * 32 + lane;
+                                if (k < len) {
+                                    t[u] = ld_stream(tg + k, pol_syn);
+                                    wq[u] = ld_stream(wv + k, pol_syn);
+                                }
+                            }
+#pragma unroll
+                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
+                                const uint32_t k = k0 + u * 32 + lane;
+                                if (k < len) {
+                                    const uint32_t l = (t[u] & 0x7fffffffu) - c_lo;
+                                    uint32_t* q = s_pA + (t[u] >> 31) * 2u * per + l;
+                                    atomicAdd(q, (uint32_t)wq[u]);
+                                    atomicAdd(q + per, (uint32_t)(wq[u] >> 32));
+                                }
+                            }
                         }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(empty + st);
-                        if (last) break;
                     }
                 }
+                if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
             } else if (doA) {
                 // ------------------------------------------------ N (OU step to tA)
                 // ou_kernel (model.hpp:88-90) with xi = stream word tA
@@ -504,11 +429,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         stp(a.i_ou + i, iou, pol_f);
                     }
                 }
+                if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
             }
         }
 
         // flush the CTA's staged spikes with one log reservation
         __syncthreads();
+        if (threadIdx.x == 0 && doE) a.q_cnt[(tE & 1u) * G + blockIdx.x] = 0u;  // serves S(tE + 2)
+        if (a.prof && threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) {
+                a.prof[4 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
+                s_t[k] = 0;
+            }
         const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
         if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
         __syncthreads();
@@ -528,6 +460,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             s_nspk = 0;
             s_fwork = 0;
             s_nwork = 0;
+            s_iwork = 0;
         }
         __syncthreads();
         if (s_stop) break;

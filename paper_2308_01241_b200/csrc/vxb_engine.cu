@@ -217,7 +217,10 @@ struct Engine {
     DevBuf<uint4> d_tl;
     DevBuf<uint32_t> d_qbase, d_qcnt;
     DevBuf<uint4> d_q;
+    DevBuf<uint64_t> d_tent;   // 8-byte tile entries (replace tgt / w on this path)
+    DevBuf<float> d_iou_b;     // I_ou of odd steps (i_ou holds even steps)
     void setup_tiles();
+    void init_tile_state();
     std::string schedule_info() const;
 
     // ---------------------------------------------------------- device
@@ -673,6 +676,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         setup_tiles();
         if (!tile_path) build_blocks();
     }
+    if (tile_path) init_tile_state();
     // dynamic chunks win on one device (+8% config 2, config 3 2.0 -> 1.5 s
     // per bio-s) and with peers when there is one block (config 2 at 4 GPUs
     // +4%); with peers and several L2 blocks the static deal measured better
@@ -1170,10 +1174,7 @@ void Engine::share_tables(const Engine& d) {
     d_tl_off.share(d.d_tl_off);
     d_tl.share(d.d_tl);
     d_qbase.share(d.d_qbase);
-    if (tile_path) {  // the work queues are per instance
-        d_q.alloc(2 * q_total);
-        d_qcnt.alloc(2ull * tile_grid);
-    }
+    d_tent.share(d.d_tent);
 }
 
 // Exchange state: receive region (one slot per peer: ids[kSlots][n_h],
@@ -1338,12 +1339,49 @@ void Engine::setup_tiles() {
     d_q.alloc(std::max<uint64_t>(1, 2 * total));
     d_qcnt.alloc(2ull * sms);
     d_qcnt.zero(stream);
+    // 8-byte entries (tile-local target, class, both weights): 2/3 of the
+    // 12-byte stream; networks whose weights do not fit 24 bits keep the
+    // l2_atomic path
+    {
+        DevBuf<unsigned int> flag;
+        flag.alloc(1);
+        flag.zero(stream);
+        d_tent.alloc(std::max<uint64_t>(1, n_syn));
+        if (n_syn)
+            tile_entries_kernel<<<1184, 256, 0, stream>>>(d_tgt.p, d_w.p, n_syn, per, d_tent.p, flag.p);
+        CK(cudaGetLastError());
+        unsigned int bad = 0;
+        CK(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (bad) {
+            d_tent.release();
+            d_tl.release();
+            d_tl_off.release();
+            d_q.release();
+            d_qcnt.release();
+            d_qbase.release();
+            return;
+        }
+    }
+    d_tgt.release();  // the tile path reads only the 8-byte entries
+    d_w.release();
     CK(cudaStreamSynchronize(stream));
     tile_path = true;
     tile_per = per;
     tile_smem = L.total;
     tile_grid = (uint32_t)sms;
     (void)tiles;
+}
+
+// Per-instance state of the tile path: I_ou is kept by step parity (the
+// noise warps write I_ou(t+1) while the update reads I_ou(t)); the state
+// after step t-1 lives in the parity (t-1) & 1 buffer — at load, odd.
+void Engine::init_tile_state() {
+    d_iou_b.alloc(std::max<uint32_t>(1, n));
+    if (n) CK(cudaMemcpyAsync(d_iou_b.p, d_iou.p, 4ull * n, cudaMemcpyDeviceToDevice, stream));
+    d_q.reserve(std::max<uint64_t>(1, 2 * q_total));
+    d_qcnt.reserve(2ull * tile_grid);
+    CK(cudaStreamSynchronize(stream));
 }
 
 // L2-blocked delivery: when the pending buffer does not fit in L2, targets
@@ -1734,6 +1772,8 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         a.q_cnt = d_qcnt.p;
         a.q = d_q.p;
         a.src_self = 0;
+        a.tent = d_tent.p;
+        a.i_ou_b = d_iou_b.p;
         d_qcnt.zero(stream);
     }
     void* args[] = {&a};
@@ -1788,7 +1828,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         }
         const double np_ = std::max(1u, steps - 1);
         std::fprintf(stderr,
-                     "vxb tile phase profile (us): phase %.1f | update end %.1f/%.1f | producer "
+                     "vxb tile phase profile (us): phase %.1f | update end %.1f/%.1f | bucketing "
                      "%.1f/%.1f | consumers %.1f/%.1f | noise %.1f/%.1f (mean/max over CTAs)\n",
                      sp / np_ / 1e3, sum[0] / std::max(1u, cnt[0]) / 1e3, mx[0] / np_ / 1e3,
                      sum[1] / std::max(1u, cnt[1]) / 1e3, mx[1] / np_ / 1e3,

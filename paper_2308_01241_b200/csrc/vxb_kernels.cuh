@@ -200,6 +200,8 @@ struct StepArgs {
     uint32_t* q_cnt;            // [2][tiles] items queued per (parity, tile)
     uint4* q;                   // [2][q_total] {entry lo, entry hi, length, 0}
     uint32_t src_self;          // global source index of shard-local neuron 0
+    const uint64_t* tent;       // 8-byte tile entries (same indexing as tgt / w)
+    float* i_ou_b;              // I_ou of odd steps (tile path; i_ou holds even steps)
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {

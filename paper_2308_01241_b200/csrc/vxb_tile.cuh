@@ -46,6 +46,9 @@ namespace vxb {
 
 constexpr int kTileThreads = 768;       // 24 warps: update, then consume / advance I_ou
 constexpr uint32_t kTileUnroll = 4;     // synapse entries in flight per consumer lane
+constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
+constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
+constexpr uint32_t kTileBucketWarps = 2;
 constexpr uint32_t kTileMaxSeg = 64;    // a tile's parameter segments kept in shared memory
 constexpr uint32_t kTileMaxPset = 32;
 
@@ -55,8 +58,8 @@ struct TileLayout {
     uint32_t pend, pset, seg, start, spk, total;
     __host__ __device__ explicit TileLayout(uint32_t per_) {
         per = per_;
-        pend = 0;  // AMPA[per], NMDA[per], GABAA[per], GABAB[per] (u32)
-        pset = (pend + 16 * per + 127) & ~127u;
+        pend = 0;  // [parity][AMPA, NMDA, GABAA, GABAB][per] (u32)
+        pset = (pend + 32 * per + 127) & ~127u;
         seg = pset + kTileMaxPset * (uint32_t)sizeof(ParamSet);
         start = seg + kTileMaxSeg * (uint32_t)sizeof(SegInfo);
         spk = (start + (kTileMaxSeg + 1) * 4 + 15) & ~15u;
@@ -99,22 +102,40 @@ struct SegCursor {
     }
 };
 
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Decoded 8-byte tile entry: bits 0-14 tile-local target, bit 15 class
+// (0 AMPA/NMDA, 1 GABAA/GABAB), bits 16-39 wq_slow, bits 40-63 wq_fast.
+__device__ __forceinline__ void tile_add(uint32_t* Bw, uint32_t per, uint64_t e) {
+    uint32_t* q = Bw + ((uint32_t)(e >> 15) & 1u) * 2u * per + ((uint32_t)e & 0x7fffu);
+    atomicAdd(q, (uint32_t)(e >> 40));
+    atomicAdd(q + per, (uint32_t)(e >> 16) & 0xffffffu);
+}
+
 __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const TileLayout L(a.tile_n);
-    uint32_t* s_pA = reinterpret_cast<uint32_t*>(smem + L.pend);  // [4][per] receptor sums
+    const uint32_t per = a.tile_n;
+    uint32_t* s_pend = reinterpret_cast<uint32_t*>(smem + L.pend);  // [parity][receptor][per]
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base;
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
-    __shared__ unsigned long long s_t[4];  // phase profile: U end, -, consumers, noise
+    __shared__ uint32_t s_hist[kTileMaxGrid], s_qb[kTileMaxGrid];  // per-tile bucketing
+    __shared__ unsigned long long s_t[4];  // phase profile: update end, bucketing, consumers, noise
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t per = a.tile_n;
     const uint32_t c_lo = min(a.n, blockIdx.x * per), c_hi = min(a.n, c_lo + per);
     const uint32_t nt = c_hi - c_lo;
     const uint32_t nch = (nt + 31u) >> 5;
+    const uint32_t G = gridDim.x;
     Control* ctl = a.ctl;
+    const uint32_t n_cons = a.n_cons;                       // warps that start on delivery
+    const uint32_t n_upd = kTileThreads / 32 - n_cons;      // warps that start on the update
+    const bool upd_warp = warp >= n_cons;
+    const uint32_t ut = threadIdx.x - n_cons * 32;          // index among update threads
 
     // parameter sets and the tile's segments in shared memory
     const ParamSet* psp = a.pset;
@@ -130,12 +151,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         }
         s_seg_lo = lo;
         s_nseg = cnt;
-        s_nspk = 0;
-        s_fwork = 0;
-        s_nwork = 0;
-        s_iwork = 0;
+        s_nspk = s_fwork = s_nwork = s_iwork = 0;
         s_t[0] = s_t[1] = s_t[2] = s_t[3] = 0;
     }
+    for (uint32_t k = threadIdx.x; k < kTileMaxGrid; k += blockDim.x) s_hist[k] = 0;
     __syncthreads();
     if (a.npset <= kTileMaxPset) {
         ParamSet* sp = reinterpret_cast<ParamSet*>(smem + L.pset);
@@ -154,30 +173,32 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         nseg = s_nseg;
         seg_end = c_hi;
     }
-    // the pending tile: P(S(t0 - 1)), delivered before this chunk
+    // pending tiles: parity (t0 - 1) holds P(S(t0 - 1)), delivered before this
+    // chunk (moved out of the global buffer); parity t0 starts empty
     {
-        const ulonglong2* gp = reinterpret_cast<const ulonglong2*>(((a.t0 - 1u) & 1u) ? a.pend1 : a.pend0);
-        ulonglong2* gz = reinterpret_cast<ulonglong2*>(((a.t0 - 1u) & 1u) ? a.pend1 : a.pend0);
+        const uint32_t pp = (a.t0 - 1u) & 1u;
+        ulonglong2* gp = reinterpret_cast<ulonglong2*>(pp ? a.pend1 : a.pend0);
+        uint32_t* B = s_pend + pp * 4 * per;
+        uint32_t* Z = s_pend + (pp ^ 1u) * 4 * per;
         for (uint32_t l = threadIdx.x; l < per; l += blockDim.x) {
             ulonglong2 p = make_ulonglong2(0ull, 0ull);
             if (l < nt) {
                 p = __ldcg(gp + c_lo + l);
-                __stcg(gz + c_lo + l, make_ulonglong2(0ull, 0ull));
+                __stcg(gp + c_lo + l, make_ulonglong2(0ull, 0ull));
             }
-            s_pA[l] = (uint32_t)p.x;
-            s_pA[per + l] = (uint32_t)(p.x >> 32);
-            s_pA[2 * per + l] = (uint32_t)p.y;
-            s_pA[3 * per + l] = (uint32_t)(p.y >> 32);
+            B[l] = (uint32_t)p.x;
+            B[per + l] = (uint32_t)(p.x >> 32);
+            B[2 * per + l] = (uint32_t)p.y;
+            B[3 * per + l] = (uint32_t)(p.y >> 32);
+            Z[l] = Z[per + l] = Z[2 * per + l] = Z[3 * per + l] = 0u;
         }
     }
     __syncthreads();
 
     const uint64_t pol_syn = policy_evict_first();  // synapse stream: read once
     const uint64_t pol_f = a.f_policy == 2 ? policy_evict_last() : policy_evict_normal();
-    const uint32_t G = gridDim.x;
     unsigned long long my_inner = 0, my_outer = 0;
     SegCursor cur_u, cur_n;
-    const bool is_cons = warp < a.n_cons;
 
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
@@ -193,154 +214,224 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             f_hi = a.forced_off[ph + 1];
         }
         const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
+        // I_ou by parity of its step: U reads I_ou(tE), N writes I_ou(tA)
+        const float* iou_rd = (tE & 1u) ? a.i_ou_b : a.i_ou;
+        float* iou_wr = (tA & 1u) ? a.i_ou_b : a.i_ou;
 
-        {
-            // ---------------------------------------------------- U (update)
-            {
-                uint32_t vb_n = 0, iou_n = 0;
-                float4 j_n, g_n;
-                float isyn_n = 0.0f;
-                auto grab = [&]() {
-                    uint32_t c = 0;
-                    if (lane == 0) c = atomicAdd(&s_fwork, 1u);
-                    return __shfl_sync(0xffffffffu, c, 0);
-                };
-                auto load = [&](uint32_t i) {
-                    vb_n = ldp(a.v + i, pol_f);
-                    iou_n = __float_as_uint(ldp(a.i_ou + i, pol_f));
+        // C: deliver S(tE) into the pending tile of parity tE (one queued
+        // segment per warp grab, kTileUnroll entries in flight per lane)
+        auto consume = [&]() {
+            if (!doE) return;
+            const uint32_t par = tE & 1u;
+            uint32_t* Bw = s_pend + par * 4 * per;
+            const uint32_t cnt = __ldcg(a.q_cnt + par * G + blockIdx.x);
+            const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
+            for (;;) {
+                uint32_t it = 0;
+                if (lane == 0) it = atomicAdd(&s_iwork, 1u);
+                it = __shfl_sync(0xffffffffu, it, 0);
+                if (it >= cnt) break;
+                // pull the lines of a segment a few grabs ahead into L2 (no
+                // registers held): the loads below then wait on L2, not HBM
+                if (it + kTilePrefetch < cnt) {
+                    const uint4 f = __ldcg(items + it + kTilePrefetch);
+                    const uint64_t fb = ((uint64_t)f.y << 32) | f.x;
+                    const char* fp = reinterpret_cast<const char*>(a.tent + fb);
+                    const char* fe = reinterpret_cast<const char*>(a.tent + fb + f.z);
+                    const char* ln = reinterpret_cast<const char*>(
+                        reinterpret_cast<uintptr_t>(fp) & ~(uintptr_t)127) + 128 * lane;
+                    if (ln < fe) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ln));
+                }
+                const uint4 d = __ldcg(items + it);
+                const uint64_t* ev = a.tent + (((uint64_t)d.y << 32) | d.x);
+                const uint32_t len = d.z;
+                for (uint32_t k0 = 0; k0 < len; k0 += 32 * kTileUnroll) {
+                    uint64_t e[kTileUnroll];
+#pragma unroll
+                    for (uint32_t u = 0; u < kTileUnroll; ++u) {
+                        const uint32_t k = k0 + u * 32 + lane;
+                        if (k < len) e[u] = ld_stream(ev + k, pol_syn);
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < kTileUnroll; ++u)
+                        if (k0 + u * 32 + lane < len) tile_add(Bw, per, e[u]);
+                }
+            }
+        };
+        // N: advance I_ou to tA (ou_kernel, model.hpp:88-90, xi = stream word
+        // tA, engine.cpp:551-558) for the tile: consumed by E(tA) in ph + 1
+        auto noise = [&]() {
+            if (!doA) return;
+            for (;;) {
+                uint32_t c = 0;
+                if (lane == 0) c = atomicAdd(&s_nwork, 1u);
+                c = __shfl_sync(0xffffffffu, c, 0);
+                if (c >= nch) break;
+                const uint32_t w_lo = c_lo + (c << 5);
+                const uint32_t i = w_lo + lane;
+                const bool live = i < c_hi;
+                const uint32_t seg = cur_n.find(startp, nseg, seg_end, w_lo, min(w_lo + 31u, c_hi - 1u),
+                                                live ? i : c_hi - 1u, lane);
+                if (live) {
+                    const SegInfo& S = segp[seg];
+                    const ParamSet& P = psp[S.pset];
+                    float iou = ldp(iou_rd + i, pol_f);
+                    float xi = 0.0f;
+                    if (P.sigma_pos) {
+                        const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
+                        xi = stream_xi(mix_key(a.ou_root, gid), tA);
+                    }
+                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                    stp(iou_wr + i, iou, pol_f);
+                }
+            }
+        };
+        // deliveries of spike s of S(tA): the FLOP tally of its whole row
+        // (engine.cpp:459-463) and, per tile its row touches, a queue item
+        // {first entry, length} (one global reservation per (CTA, tile))
+        auto tally = [&](uint32_t s) {
+            const uint64_t row = ldg64(a.off + a.src_self + s);
+            const uint64_t len = ldg64(a.off + a.src_self + s + 1) - row;
+            const uint32_t in = __ldg(a.inner + a.src_self + s);
+            my_inner += 2ull * in;
+            my_outer += 2ull * (len - in);
+            return row;
+        };
+
+        if (upd_warp) {
+            // ------------------------------------------------ U (update)
+            uint32_t* Br = s_pend + (tA & 1u) * 4 * per;  // P(S(tE - 1)), parity tA
+            uint32_t vb_n = 0, iou_n = 0;
+            float4 j_n, g_n;
+            float isyn_n = 0.0f;
+            auto grab = [&]() {
+                uint32_t c = 0;
+                if (lane == 0) c = atomicAdd(&s_fwork, 1u);
+                return __shfl_sync(0xffffffffu, c, 0);
+            };
+            auto load = [&](uint32_t i) {
+                vb_n = ldp(a.v + i, pol_f);
+                iou_n = __float_as_uint(ldp(iou_rd + i, pol_f));
+                if (doE) {
+                    j_n = ldp(a.j + i, pol_f);
+                    g_n = ldp(a.g + i, pol_f);
+                } else {
+                    isyn_n = ldp(a.i_syn + i, pol_f);
+                }
+            };
+            uint32_t ch = grab();
+            uint32_t i = c_lo + (ch << 5) + lane;
+            if (ch < nch && i < c_hi) load(i);
+            while (ch < nch) {
+                const uint32_t vb0 = vb_n;
+                const float iou = __uint_as_float(iou_n);
+                float4 j = j_n;
+                const float4 g = g_n;
+                const float isyn_in = isyn_n;
+                const uint32_t chn = grab();
+                const uint32_t inext = c_lo + (chn << 5) + lane;
+                if (chn < nch && inext < c_hi) load(inext);
+                const bool live = i < c_hi;
+                bool spiked = false;
+                const uint32_t w_lo = c_lo + (ch << 5);
+                const uint32_t seg = cur_u.find(startp, nseg, seg_end, w_lo, min(w_lo + 31u, c_hi - 1u),
+                                                live ? i : c_hi - 1u, lane);
+                uint32_t vb = vb0;
+                if (live) {
+                    const SegInfo& S = segp[seg];
+                    const ParamSet& P = psp[S.pset];
+                    const uint32_t l = i - c_lo;
+                    const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                    float isyn;
                     if (doE) {
-                        j_n = ldp(a.j + i, pol_f);
-                        g_n = ldp(a.g + i, pol_f);
+                        // gating_kernel (model.hpp:69-71) with deq(P_prev)
+                        // (engine.cpp:543-546) from the shared pending tile
+                        const float p0 = dequantize((int64_t)Br[l]);
+                        const float p1 = dequantize((int64_t)Br[per + l]);
+                        const float p2 = dequantize((int64_t)Br[2 * per + l]);
+                        const float p3 = dequantize((int64_t)Br[3 * per + l]);
+                        Br[l] = 0u;
+                        Br[per + l] = 0u;
+                        Br[2 * per + l] = 0u;
+                        Br[3 * per + l] = 0u;
+                        j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
+                        j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
+                        j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
+                        j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
+                        // current_kernel (model.hpp:73-81), u order, from 0.0f
+                        float c = 0.0f;
+                        c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
+                        c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
+                        c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
+                        c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
+                        isyn = c;
+                        // I_ou(tE) was advanced by phase ph - 1 (N)
+                        if (!doA) stp(a.i_syn + i, isyn, pol_f);
+                        stp(a.j + i, j, pol_f);
                     } else {
-                        isyn_n = ldp(a.i_syn + i, pol_f);
+                        isyn = isyn_in;
                     }
-                };
-                uint32_t ch = grab();
-                uint32_t i = c_lo + (ch << 5) + lane;
-                if (ch < nch && i < c_hi) load(i);
-                while (ch < nch) {
-                    const uint32_t vb0 = vb_n;
-                    const float iou = __uint_as_float(iou_n);
-                    float4 j = j_n;
-                    const float4 g = g_n;
-                    const float isyn_in = isyn_n;
-                    const uint32_t chn = grab();
-                    const uint32_t inext = c_lo + (chn << 5) + lane;
-                    if (chn < nch && inext < c_hi) load(inext);
-                    const bool live = i < c_hi;
-                    bool spiked = false;
-                    const uint32_t w_lo = c_lo + (ch << 5);
-                    const uint32_t seg = cur_u.find(startp, nseg, seg_end, w_lo,
-                                                    min(w_lo + 31u, c_hi - 1u),
-                                                    live ? i : c_hi - 1u, lane);
-                    uint32_t vb = vb0;
-                    if (live) {
-                        const SegInfo& S = segp[seg];
-                        const ParamSet& P = psp[S.pset];
-                        const uint32_t l = i - c_lo;
-                        const float v = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                        float isyn;
-                        if (doE) {
-                            // gating_kernel (model.hpp:69-71) with deq(P_prev)
-                            // (engine.cpp:543-546) from the shared pending tile
-                            const float p0 = dequantize((int64_t)s_pA[l]);
-                            const float p1 = dequantize((int64_t)s_pA[per + l]);
-                            const float p2 = dequantize((int64_t)s_pA[2 * per + l]);
-                            const float p3 = dequantize((int64_t)s_pA[3 * per + l]);
-                            s_pA[l] = 0u;
-                            s_pA[per + l] = 0u;
-                            s_pA[2 * per + l] = 0u;
-                            s_pA[3 * per + l] = 0u;
-                            j.x = fadd(fmul(j.x, P.decay[0]), fmul(P.omega[0], p0));
-                            j.y = fadd(fmul(j.y, P.decay[1]), fmul(P.omega[1], p1));
-                            j.z = fadd(fmul(j.z, P.decay[2]), fmul(P.omega[2], p2));
-                            j.w = fadd(fmul(j.w, P.decay[3]), fmul(P.omega[3], p3));
-                            // current_kernel (model.hpp:73-81), u order, from 0.0f
-                            float c = 0.0f;
-                            c = fadd(c, fmul(fmul(g.x, j.x), fsub(P.e_rev[0], v)));
-                            c = fadd(c, fmul(fmul(g.y, j.y), fsub(P.e_rev[1], v)));
-                            c = fadd(c, fmul(fmul(g.z, j.z), fsub(P.e_rev[2], v)));
-                            c = fadd(c, fmul(fmul(g.w, j.w), fsub(P.e_rev[3], v)));
-                            isyn = c;
-                            // I_ou(tE) was advanced by phase ph - 1 (N below)
-                            if (!doA) stp(a.i_syn + i, isyn, pol_f);
-                            stp(a.j + i, j, pol_f);
+                    if (doA) {
+                        // membrane_kernel + threshold (engine.cpp:363-385)
+                        if (is_refrac(vb)) {
+                            const uint32_t r = (vb & 0x007fffffu) - 1u;
+                            vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
                         } else {
-                            isyn = isyn_in;
-                        }
-                        if (doA) {
-                            // membrane_kernel + threshold (engine.cpp:363-385)
-                            if (is_refrac(vb)) {
-                                const uint32_t r = (vb & 0x007fffffu) - 1u;
-                                vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
+                            float inoise = iou;
+                            if (inj_ep) {
+                                const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + S.voxel);
+                                if (x != 0.0f) inoise = fadd(iou, x);
+                            }
+                            const float nv = fadd(
+                                v, fmul(P.dt_over_c,
+                                        fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
+                            if (!isfinite(nv)) {
+                                atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
+                                vb = __float_as_uint(nv);
+                            } else if (nv >= P.v_th) {
+                                spiked = true;
+                                vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
                             } else {
-                                float inoise = iou;
-                                if (inj_ep) {
-                                    const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + S.voxel);
-                                    if (x != 0.0f) inoise = fadd(iou, x);
-                                }
-                                const float nv = fadd(
-                                    v, fmul(P.dt_over_c,
-                                            fadd(fadd(fmul(P.g_leak, fsub(P.e_leak, v)), isyn), inoise)));
-                                if (!isfinite(nv)) {
-                                    atomicMin(&ctl->err, ((unsigned long long)tA << 32) | i);
-                                    vb = __float_as_uint(nv);
-                                } else if (nv >= P.v_th) {
-                                    spiked = true;
-                                    vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                                } else {
-                                    vb = __float_as_uint(nv);
-                                }
+                                vb = __float_as_uint(nv);
                             }
-                            // forced spikes (engine.cpp:389-398): join unless already fired
-                            if (f_hi > f_lo && !spiked) {
-                                const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
-                                if (k < f_hi && __ldg(a.forced_local + k) == i) {
-                                    spiked = true;
-                                    vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
-                                }
-                            }
-                            stp(a.v + i, vb, pol_f);
                         }
-                        // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
-                        if (a.n_probes) {
-                            uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
-                            while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
-                                const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
-                                if (doE) a.probe_i[row + ph - 1] = isyn;
-                                if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
-                                ++k;
+                        // forced spikes (engine.cpp:389-398): join unless already fired
+                        if (f_hi > f_lo && !spiked) {
+                            const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
+                            if (k < f_hi && __ldg(a.forced_local + k) == i) {
+                                spiked = true;
+                                vb = P.tref ? refrac_bits(P.tref) : __float_as_uint(P.v_reset);
                             }
+                        }
+                        stp(a.v + i, vb, pol_f);
+                    }
+                    // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
+                    if (a.n_probes) {
+                        uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
+                        while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
+                            const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;
+                            if (doE) a.probe_i[row + ph - 1] = isyn;
+                            if (doA) a.probe_v[row + ph] = is_refrac(vb) ? P.v_reset : __uint_as_float(vb);
+                            ++k;
                         }
                     }
-                    // spike log staging + rates (engine.cpp:400-404), warp aggregated
-                    const unsigned ball = __ballot_sync(0xffffffffu, spiked);
-                    if (ball) {
-                        unsigned base = 0;
-                        if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (spiked) {
-                            const unsigned rank = __popc(ball & ((1u << lane) - 1u));
-                            if (base + rank < kSpkStage)
-                                s_spk[base + rank] = i;
-                            else
-                                a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
-                            const uint32_t unit = segp[seg].unit;
-                            const unsigned peers = __match_any_sync(ball, unit);
-                            if ((unsigned)__ffs(peers) - 1u == lane)
-                                atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
-                            // deliveries of S(tA): one queue item per tile the
-                            // row touches (engine.cpp:439-442 / 444-464), and the
-                            // FLOP tally of the whole row (engine.cpp:459-463)
-                            const uint32_t s = a.src_self + i;
-                            const uint64_t row = ldg64(a.off + s);
-                            const uint64_t len = ldg64(a.off + s + 1) - row;
-                            const uint32_t in = __ldg(a.inner + s);
-                            my_inner += 2ull * in;
-                            my_outer += 2ull * (len - in);
+                }
+                // spike log staging + rates (engine.cpp:400-404), warp aggregated
+                const unsigned ball = __ballot_sync(0xffffffffu, spiked);
+                if (ball) {
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(&s_nspk, (unsigned)__popc(ball));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (spiked) {
+                        const unsigned rank = __popc(ball & ((1u << lane) - 1u));
+                        if (base + rank < kSpkStage) {
+                            s_spk[base + rank] = i;  // bucketed after the update (B)
+                        } else {  // staging full: log and bucket this spike directly
+                            a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                            const uint64_t row = tally(i);
                             const uint32_t par = tA & 1u;
-                            const uint64_t k1 = __ldg(a.tl_off + s + 1);
-                            for (uint64_t k = __ldg(a.tl_off + s); k < k1; ++k) {
+                            const uint64_t k1 = __ldg(a.tl_off + a.src_self + i + 1);
+                            for (uint64_t k = __ldg(a.tl_off + a.src_self + i); k < k1; ++k) {
                                 const uint4 sg = __ldg(a.tl + k);
                                 const uint32_t pos = atomicAdd(a.q_cnt + par * G + sg.x, 1u);
                                 const uint64_t b = row + sg.y;
@@ -348,99 +439,81 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                                     make_uint4((uint32_t)b, (uint32_t)(b >> 32), sg.z, 0u);
                             }
                         }
+                        const uint32_t unit = segp[seg].unit;
+                        const unsigned peers = __match_any_sync(ball, unit);
+                        if ((unsigned)__ffs(peers) - 1u == lane)
+                            atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
                     }
-                    ch = chn;
-                    i = inext;
                 }
+                ch = chn;
+                i = inext;
             }
-            // every warp has consumed its neurons' pending sums
-            __syncthreads();
-            if (a.prof && threadIdx.x == 0) s_t[0] = globaltimer();
+            // the CTA's spikes of S(tA) are staged once every update warp is
+            // here: the bucketing warps wait for that, the others go on
+            const bool bucket_warp = warp >= kTileThreads / 32 - kTileBucketWarps;
+            if (bucket_warp)
+                named_sync(1, n_upd * 32);
+            else
+                asm volatile("bar.arrive 1, %0;" ::"r"(n_upd * 32) : "memory");
+            if (a.prof && ut == 0) s_t[0] = globaltimer();
 
-            if (is_cons) {
-                // ------------------------------------------------ C (consumers)
-                // the segments queued for this tile (parity tE), one item per
-                // warp grab; lanes stream the entries with kTileUnroll loads
-                // in flight each and add them with two shared atomics
-                if (doE) {
-                    const uint32_t par = tE & 1u;
-                    const uint32_t cnt = __ldcg(a.q_cnt + par * G + blockIdx.x);
-                    const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
-                    for (;;) {
-                        uint32_t it = 0;
-                        if (lane == 0) it = atomicAdd(&s_iwork, 1u);
-                        it = __shfl_sync(0xffffffffu, it, 0);
-                        if (it >= cnt) break;
-                        const uint4 d = __ldcg(items + it);
-                        const uint64_t beg = ((uint64_t)d.y << 32) | d.x;
-                        const uint32_t len = d.z;
-                        const uint32_t* tg = a.tgt + beg;
-                        const uint64_t* wv = a.w + beg;
-                        for (uint32_t k0 = 0; k0 < len; k0 += 32 * kTileUnroll) {
-                            uint32_t t[kTileUnroll];
-                            uint64_t wq[kTileUnroll];
-#pragma unroll
-                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
-                                const uint32_t k = k0 + u * 32 + lane;
-                                if (k < len) {
-                                    t[u] = ld_stream(tg + k, pol_syn);
-                                    wq[u] = ld_stream(wv + k, pol_syn);
-                                }
-                            }
-#pragma unroll
-                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
-                                const uint32_t k = k0 + u * 32 + lane;
-                                if (k < len) {
-                                    const uint32_t l = (t[u] & 0x7fffffffu) - c_lo;
-                                    uint32_t* q = s_pA + (t[u] >> 31) * 2u * per + l;
-                                    atomicAdd(q, (uint32_t)wq[u]);
-                                    atomicAdd(q + per, (uint32_t)(wq[u] >> 32));
-                                }
-                            }
-                        }
+            // ------------------------------------------------ B (bucketing)
+            // the staged spikes' tile segments: count per tile in shared
+            // memory, one global reservation per (CTA, tile), then the items
+            const uint32_t bt = threadIdx.x - (kTileThreads - 32 * kTileBucketWarps);
+            const uint32_t nbt = 32 * kTileBucketWarps;
+            const uint32_t nst = (doA && bucket_warp) ? min(s_nspk, (uint32_t)kSpkStage) : 0u;
+            if (nst) {
+                const uint32_t par = tA & 1u;
+                for (uint32_t k = bt; k < nst; k += nbt) {
+                    const uint32_t s = a.src_self + s_spk[k];
+                    tally(s_spk[k]);
+                    const uint64_t k1 = __ldg(a.tl_off + s + 1);
+                    for (uint64_t q = __ldg(a.tl_off + s); q < k1; ++q) atomicAdd(&s_hist[__ldg(&a.tl[q].x)], 1u);
+                }
+                named_sync(2, nbt);
+                for (uint32_t t = bt; t < G; t += nbt) {
+                    const uint32_t h = s_hist[t];
+                    if (h) {
+                        s_qb[t] = __ldg(a.q_base + t) + atomicAdd(a.q_cnt + par * G + t, h);
+                        s_hist[t] = 0u;
                     }
                 }
-                if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
-            } else if (doA) {
-                // ------------------------------------------------ N (OU step to tA)
-                // ou_kernel (model.hpp:88-90) with xi = stream word tA
-                // (engine.cpp:551-558): consumed by E(tA) in phase ph + 1
-                for (;;) {
-                    uint32_t c = 0;
-                    if (lane == 0) c = atomicAdd(&s_nwork, 1u);
-                    c = __shfl_sync(0xffffffffu, c, 0);
-                    if (c >= nch) break;
-                    const uint32_t w_lo = c_lo + (c << 5);
-                    const uint32_t i = w_lo + lane;
-                    const bool live = i < c_hi;
-                    const uint32_t seg = cur_n.find(startp, nseg, seg_end, w_lo,
-                                                    min(w_lo + 31u, c_hi - 1u),
-                                                    live ? i : c_hi - 1u, lane);
-                    if (live) {
-                        const SegInfo& S = segp[seg];
-                        const ParamSet& P = psp[S.pset];
-                        float iou = ldp(a.i_ou + i, pol_f);
-                        float xi = 0.0f;
-                        if (P.sigma_pos) {
-                            const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
-                            xi = stream_xi(mix_key(a.ou_root, gid), tA);
-                        }
-                        iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
-                        stp(a.i_ou + i, iou, pol_f);
+                named_sync(2, nbt);
+                uint4* qp = a.q + (size_t)par * a.q_total;
+                for (uint32_t k = bt; k < nst; k += nbt) {
+                    const uint32_t s = a.src_self + s_spk[k];
+                    const uint64_t row = ldg64(a.off + s);
+                    const uint64_t k1 = __ldg(a.tl_off + s + 1);
+                    for (uint64_t q = __ldg(a.tl_off + s); q < k1; ++q) {
+                        const uint4 sg = __ldg(a.tl + q);
+                        const uint32_t pos = s_qb[sg.x] + atomicAdd(&s_hist[sg.x], 1u);
+                        const uint64_t b = row + sg.y;
+                        qp[pos] = make_uint4((uint32_t)b, (uint32_t)(b >> 32), sg.z, 0u);
                     }
                 }
-                if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
+                named_sync(2, nbt);
+                for (uint32_t t = bt; t < G; t += nbt) s_hist[t] = 0u;
             }
+            if (a.prof && bt == 0) s_t[1] = globaltimer();
+            noise();
+            if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
+            consume();
+        } else {
+            consume();
+            if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
+            noise();
+            if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
         }
 
         // flush the CTA's staged spikes with one log reservation
         __syncthreads();
-        if (threadIdx.x == 0 && doE) a.q_cnt[(tE & 1u) * G + blockIdx.x] = 0u;  // serves S(tE + 2)
         if (a.prof && threadIdx.x == 0)
             for (int k = 0; k < 4; ++k) {
                 a.prof[4 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
                 s_t[k] = 0;
             }
+        if (threadIdx.x == 0 && doE) a.q_cnt[(tE & 1u) * G + blockIdx.x] = 0u;  // serves S(tE + 2)
         const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
         if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
         __syncthreads();
@@ -457,10 +530,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             [&] {});
         if (threadIdx.x == 0) {
             s_stop = (int)ld_acquire(&ctl->stop);
-            s_nspk = 0;
-            s_fwork = 0;
-            s_nwork = 0;
-            s_iwork = 0;
+            s_nspk = s_fwork = s_nwork = s_iwork = 0;
         }
         __syncthreads();
         if (s_stop) break;
@@ -469,14 +539,33 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     {
         const uint32_t tl = a.t0 + a.steps - 1u;
         ulonglong2* gp = reinterpret_cast<ulonglong2*>((tl & 1u) ? a.pend1 : a.pend0);
+        const uint32_t* B = s_pend + (tl & 1u) * 4 * per;
         for (uint32_t l = threadIdx.x; l < nt; l += blockDim.x)
             __stcg(gp + c_lo + l,
-                   make_ulonglong2((uint64_t)s_pA[l] | ((uint64_t)s_pA[per + l] << 32),
-                                   (uint64_t)s_pA[2 * per + l] | ((uint64_t)s_pA[3 * per + l] << 32)));
+                   make_ulonglong2((uint64_t)B[l] | ((uint64_t)B[per + l] << 32),
+                                   (uint64_t)B[2 * per + l] | ((uint64_t)B[3 * per + l] << 32)));
     }
     if (my_inner | my_outer) {
         atomicAdd(&ctl->flops_inner, my_inner);
         atomicAdd(&ctl->flops_outer, my_outer);
+    }
+}
+
+// 8-byte tile entries from the target-sorted out-CSR: tile-local target
+// (< 2^15), class, and both Q16 weights (< 2^24 each: checked, else the
+// engine keeps the l2_atomic path).  flag[0] is set when an entry does not fit.
+__global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ w,
+                                    uint64_t n_syn, uint32_t per, uint64_t* __restrict__ tent,
+                                    unsigned int* __restrict__ flag) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_syn;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = tgt[k], tid = t & 0x7fffffffu;
+        const uint64_t wq = w[k];
+        const uint32_t wf = (uint32_t)wq, ws = (uint32_t)(wq >> 32);
+        const uint32_t l = tid % per;
+        if (wf >= (1u << 24) || ws >= (1u << 24) || l >= (1u << 15)) atomicExch(flag, 1u);
+        tent[k] = ((uint64_t)(wf & 0xffffffu) << 40) | ((uint64_t)(ws & 0xffffffu) << 16) |
+                  ((uint64_t)(t >> 31) << 15) | (l & 0x7fffu);
     }
 }
 

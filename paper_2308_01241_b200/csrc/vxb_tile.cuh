@@ -44,7 +44,13 @@
 
 namespace vxb {
 
-constexpr int kTileThreads = 768;       // 24 warps: update, then consume / advance I_ou
+#ifndef VXB_TILE_THREADS
+// 32 warps at 64 registers: config 2 56.9 us/step vs 60.8 at 24 warps x 80
+// registers (the update, noise and delivery are all latency-bound; more
+// warps beat fewer spills), 67.9 at 20 x 96
+#define VXB_TILE_THREADS 1024
+#endif
+constexpr int kTileThreads = VXB_TILE_THREADS;      // 24 warps: update, then consume / advance I_ou
 constexpr uint32_t kTileUnroll = 4;     // synapse entries in flight per consumer lane
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
 constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers

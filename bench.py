@@ -352,7 +352,9 @@ def run_b200(args):
         cfg = dti_cfg(workers=ws, rate=args.rate, dt_ms=args.dt,
                       total=args.neurons or 20_000_000)
     net = netgen.build_network(cfg)
-    opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=True,
+    # the reference arm's options (record_raster / record_timings off): the
+    # per-step wire-byte rows would add a spike-log readback per advance
+    opt = SimOptions(steps=bio_steps, dt_ms=args.dt, record_raster=False, record_timings=False,
                      device=dev)
     if ws > 1:
         sim = netgen.DistributedSimInstance(net, opt, rank, ws)

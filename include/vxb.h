@@ -228,6 +228,14 @@ double vxb_result_exchange_wait_ms(const vxb_engine* e);
 /* Bytes copied host->device / device->host by the last vxb_advance. */
 uint64_t vxb_result_h2d_bytes(const vxb_engine* e);
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e);
+/* One worker per rank, with record_timings: the wire bytes of the batches
+ * this rank's worker sent in the last advance, [steps][dst worker] (the
+ * reference's encode_batch sizes, transport.cpp:33-55; 12 for an empty
+ * batch, 0 for itself).  The caller hands every rank the bytes its peers sent
+ * it, [steps][src worker], with vxb_set_recv_wire_bytes, which completes the
+ * StepTimings received-byte counters (engine.cpp:495-523). */
+int vxb_result_wire_bytes(const vxb_engine* e, uint64_t* out, uint64_t cap);
+int vxb_set_recv_wire_bytes(vxb_engine* e, const uint64_t* in, uint32_t steps);
 /* Kernel launches issued by the last vxb_advance. */
 uint64_t vxb_result_launches(const vxb_engine* e);
 /* The delivery schedule chosen for this network as a JSON object (path, grid,

@@ -216,7 +216,7 @@ struct Engine {
     DevBuf<unsigned long long> d_tl_off;
     DevBuf<uint4> d_tl;
     DevBuf<uint32_t> d_qbase, d_qcnt;
-    DevBuf<uint4> d_q;
+    DevBuf<uint64_t> d_q;
     DevBuf<uint64_t> d_tent;   // 8-byte tile entries (replace tgt / w on this path)
     DevBuf<float> d_iou_b;     // I_ou of odd steps (i_ou holds even steps)
     void setup_tiles();
@@ -265,6 +265,13 @@ struct Engine {
     uint32_t res_steps = 0;
     uint32_t res_start = 0;
     std::vector<uint64_t> raster_keys;  // (rel step << 32 | shard-local), sorted
+    // spikes are logged per step (linear log, sorted keys) when the raster or
+    // the timing rows' wire-byte counters need them
+    bool log_spikes() const { return record_raster || record_timings; }
+    std::vector<unsigned long long> dst_full;  // world == 1: full dst mask per shard-local neuron
+    std::vector<uint64_t> wire_sent;           // world > 1: [step][dst worker] bytes sent
+    std::vector<uint64_t> phase_wait_all;      // per phase of the last advance: max CTA wait (ns)
+    void account_wire_bytes(uint32_t steps);
     std::vector<uint32_t> rates;        // [unit][steps]
     std::vector<float> probe_v, probe_i;
     vxb_flops flops{};
@@ -590,6 +597,7 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         generate_csr(*gen);  // consistent by construction
     } else {
         build_csr(net);
+        if (world == 1) dst_full = h_mask;
         DevBuf<unsigned long long> d_mask, d_bad;
         d_mask.alloc(n);
         d_bad.alloc(1);
@@ -619,6 +627,8 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         }
     }
     d_keys.release();
+    if (world == 1 && dst_full.empty() && !have_src.empty())  // generated tables
+        dst_full.assign(have_src.begin(), have_src.begin() + n);
 
     const size_t pend_bytes = (packed ? 16ull : 32ull) * n;
     d_pend0.alloc(pend_bytes);
@@ -1276,14 +1286,16 @@ void Engine::sort_rows() {
 
 // SM-tile path: every CTA (one per SM) owns a contiguous tile of neurons and
 // keeps their pending sums in shared memory (vxb_tile.cuh).  Eligible when
-// the pending tile fits in a CTA's shared memory (shards up to ~2M neurons
-// on 148 SMs), on one GPU, with carry-free packed sums.  Rows are sorted by
-// target and cut into per-tile segments here, once.
+// both parities of the pending tile fit in a CTA's shared memory (shards up
+// to ~1M neurons on 148 SMs) with carry-free packed sums; with one process
+// per GPU the peers' spikes are delivered by every CTA from the received
+// batches.  Rows are sorted by target and cut into per-tile segments here,
+// once.
 void Engine::setup_tiles() {
     tile_path = false;
     const char* force = knob("VXB_PATH", &knobs);
     if (force && std::string(force) == "l2") return;
-    if (world != 1 || !packed || n == 0) return;
+    if (!packed || n == 0) return;
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -1292,10 +1304,11 @@ void Engine::setup_tiles() {
     if (L.total > (uint32_t)optin) return;
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
         tile_cons = (uint32_t)std::min(23, std::max(1, std::atoi(c)));
-    CK(cudaFuncSetAttribute((const void*)tile_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    const void* tk = world > 1 ? (const void*)tile_kernel<true> : (const void*)tile_kernel<false>;
+    CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel, kTileThreads, L.total));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, world > 1 ? tile_kernel<true> : tile_kernel<false>,
+                                                     kTileThreads, L.total));
     if (per_sm < 1) return;
     const uint32_t tiles = (uint32_t)((n + per - 1) / per);
     sort_rows();
@@ -1305,7 +1318,7 @@ void Engine::setup_tiles() {
     cnt.zero(stream);
     tile_segments_kernel<0><<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
                                                        d_tgt.p, n_src, per, cnt.p + 1, nullptr,
-                                                       nullptr, nullptr);
+                                                       nullptr, nullptr, nullptr);
     CK(cudaGetLastError());
     d_tl_off.alloc((size_t)n_src + 1);
     {
@@ -1322,17 +1335,23 @@ void Engine::setup_tiles() {
     cnt.release();
     d_tl.alloc(std::max<unsigned long long>(1, total));
     DevBuf<uint32_t> cap;
-    cap.alloc(sms);
+    cap.alloc(sms + 1);  // [sms]: a segment too long for a queue item
     cap.zero(stream);
     tile_segments_kernel<1><<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
                                                        d_tgt.p, n_src, per, nullptr, d_tl_off.p,
-                                                       d_tl.p, cap.p);
+                                                       d_tl.p, cap.p, cap.p + sms);
     CK(cudaGetLastError());
-    std::vector<uint32_t> hcap(sms), qb(sms + 1, 0);
-    CK(cudaMemcpyAsync(hcap.data(), cap.p, 4ull * sms, cudaMemcpyDeviceToHost, stream));
+    std::vector<uint32_t> hcap(sms + 1), qb(sms + 1, 0);
+    CK(cudaMemcpyAsync(hcap.data(), cap.p, 4ull * (sms + 1), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    if (hcap[sms]) {  // keep the l2_atomic path
+        d_tl.release();
+        d_tl_off.release();
+        return;
+    }
     for (int t = 0; t < sms; ++t) qb[t + 1] = qb[t] + hcap[t];
     if (total >= (1ull << 32)) throw SimError("tile segment table exceeds 2^32 entries");
+    if (n_syn >= (1ull << 40)) return;  // queue items address entries with 40 bits
     q_total = total;
     d_qbase.alloc(sms + 1);
     CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 4ull * (sms + 1), cudaMemcpyHostToDevice, stream));
@@ -1583,17 +1602,18 @@ void Engine::advance(uint32_t steps) {
 
     // chunking: the linear spike log holds n entries per step of a chunk
     uint32_t chunk = steps;
-    if (record_raster) {
+    if (log_spikes()) {
         const uint64_t cap = 1ull << 29;  // 2 GiB of spike ids per chunk
         chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(steps, cap / std::max(1u, n)));
     }
-    const uint32_t cap_entries = record_raster ? n * chunk : 2 * n;
+    const uint32_t cap_entries = log_spikes() ? n * chunk : 2 * n;
     if (d_spk.n < std::max<size_t>(1, cap_entries)) d_spk.alloc(std::max<size_t>(1, cap_entries));
     d_seg_end.reserve(chunk + 2);
     d_rates.reserve((size_t)n_units * chunk);
     d_phase_ns.reserve(chunk + 2);
     d_phase_wait.reserve(chunk + 2);
     exchange_wait_ms = 0;
+    phase_wait_all.assign(steps + 2, 0);
 
     const uint32_t n_bold = hemo_on && world == 1 ? steps / hemo_every : 0u;
     bold.assign((size_t)n_bold * n_voxels, 0.0);
@@ -1677,12 +1697,79 @@ void Engine::advance(uint32_t steps) {
                 r.t[2] = a + e;  // t3
                 r.t[3] = r.t[4] = r.t[0];
                 r.t[5] = r.t[6] = r.t[1];
+                // send span t8..t9: the ids are stored into the peers' slots
+                // during the phase and published at its end (no send time of
+                // their own); receive span t10..t11: the wait for the peers'
+                // batches of S(s) at the start of the phase holding E(s)
+                r.t[7] = r.t[8] = r.t[0];
+                r.t[9] = a;
+                r.t[10] = a + (world > 1 ? (int64_t)phase_wait_all[s + 1] : 0);
+                if (world > 1) {
+                    bool inter = false;
+                    for (uint32_t h = 0; h < world; ++h)
+                        inter |= h != rank && h / workers_per_node != rank / workers_per_node;
+                    (inter ? r.recv_inter_ns : r.recv_intra_ns) = r.t[10] - r.t[9];
+                }
             }
         }
+        account_wire_bytes(steps);
     }
+    if (!record_raster) raster_keys.clear();
     step_done += steps;
     // hemo.cpp:37-40, raised by the readout: the simulation state is intact
     if (hemo_diverged) throw HemoError("hemodynamic state diverged");
+}
+
+// LEB128 length of one delta (transport.cpp:10-17)
+uint32_t varint_len(uint32_t v) {
+    return v < (1u << 7) ? 1u : v < (1u << 14) ? 2u : v < (1u << 21) ? 3u : v < (1u << 28) ? 4u : 5u;
+}
+
+// Wire bytes of every (step, src, dst) spike batch as the reference encodes
+// it (encode_batch, transport.cpp:33-55: 12-byte header + the varints of the
+// ascending local ids' deltas; an empty batch is the 12-byte header) and the
+// StepTimings byte counters split by node (engine.cpp:416-437, 495-523,
+// 570-597; acceptance.cpp:651-742).  On one device every worker is here and
+// both directions are counted; with one worker per rank the sent bytes are
+// counted here and the received ones come from the peers
+// (vxb_set_recv_wire_bytes).
+void Engine::account_wire_bytes(uint32_t steps) {
+    const std::vector<unsigned long long>& mk = world > 1 ? h_mask : dst_full;
+    const uint32_t W = workers;
+    std::vector<uint64_t> b((size_t)W * W);
+    std::vector<uint32_t> prev((size_t)W * W);
+    std::vector<uint8_t> seen((size_t)W * W);
+    auto node = [&](uint32_t w) { return w / workers_per_node; };
+    if (world > 1) wire_sent.assign((size_t)steps * W, 0);
+    size_t k = 0;
+    for (uint32_t s = 0; s < steps; ++s) {
+        std::fill(b.begin(), b.end(), 12ull);
+        std::fill(seen.begin(), seen.end(), 0);
+        for (; k < raster_keys.size() && (uint32_t)(raster_keys[k] >> 32) == s; ++k) {
+            const uint32_t loc = (uint32_t)raster_keys[k];
+            const uint32_t w = (uint32_t)(std::upper_bound(wbase.begin(), wbase.end(), loc) -
+                                          wbase.begin()) - 1;
+            const uint32_t id = loc - wbase[w];
+            for (unsigned long long m = mk.empty() ? 0ull : mk[loc]; m; m &= m - 1) {
+                const uint32_t d = (uint32_t)__builtin_ctzll(m);
+                if (d == w || d >= W) continue;
+                const size_t q = (size_t)w * W + d;
+                b[q] += varint_len(seen[q] ? id - prev[q] : id);
+                seen[q] = 1;
+                prev[q] = id;
+            }
+        }
+        for (uint32_t w = local_lo; w < local_hi; ++w) {
+            vxb_step_timings& r = timings[(size_t)s * W + w];
+            for (uint32_t d = 0; d < W; ++d) {
+                if (d == w) continue;
+                (node(d) == node(w) ? r.bytes_sent_intra : r.bytes_sent_inter) += b[(size_t)w * W + d];
+                if (world > 1) wire_sent[(size_t)s * W + d] = b[(size_t)w * W + d];
+                else
+                    (node(d) == node(w) ? r.bytes_recv_intra : r.bytes_recv_inter) += b[(size_t)d * W + w];
+            }
+        }
+    }
 }
 
 void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
@@ -1704,7 +1791,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.rel0 = rel0;
     a.adv_steps = adv_steps;
     a.spk_cap = (uint32_t)d_spk.n;
-    a.ring = record_raster ? 0u : 1u;
+    a.ring = log_spikes() ? 0u : 1u;
     a.use_smem_seg = use_smem_seg ? 1u : 0u;
     a.dtf = dtf;
     a.ou_root = mix_key(seed, 1);  // rngstream::ou_noise (rng.hpp:18)
@@ -1771,7 +1858,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         a.q_base = d_qbase.p;
         a.q_cnt = d_qcnt.p;
         a.q = d_q.p;
-        a.src_self = 0;
+        a.src_self = world > 1 ? src_base[rank] : 0u;
         a.tent = d_tent.p;
         a.i_ou_b = d_iou_b.p;
         d_qcnt.zero(stream);
@@ -1779,8 +1866,9 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
     if (tile_path)
-        CK(cudaLaunchCooperativeKernel((const void*)tile_kernel, tile_grid, kTileThreads, args,
-                                       tile_smem, stream));
+        CK(cudaLaunchCooperativeKernel(world > 1 ? (const void*)tile_kernel<true>
+                                                 : (const void*)tile_kernel<false>,
+                                       tile_grid, kTileThreads, args, tile_smem, stream));
     else if (packed)
         CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args,
                                        smem_bytes, stream));
@@ -1804,6 +1892,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
                            stream));
         CK(cudaStreamSynchronize(stream));
         for (auto x : pw) exchange_wait_ms += x * 1e-6;
+        for (uint32_t p = 1; p <= steps; ++p) phase_wait_all[rel0 + p] = pw[p];
     }
     CK(cudaStreamSynchronize(stream));
     if (prof && tile_path) {  // per phase: mean / max over CTAs of each part's end (us)
@@ -1893,7 +1982,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     flops.gating_inner += c.flops_inner;
     flops.gating_outer += c.flops_outer;
 
-    if (record_raster) {
+    if (log_spikes()) {
         const uint32_t total = seg_end[steps - 1];
         if (total) {
             if (d_keys.n < total) d_keys.alloc(total);
@@ -2049,6 +2138,30 @@ uint64_t vxb_result_timings_size(const vxb_engine* e) { return e->eng.timings.si
 int vxb_result_timings(const vxb_engine* e, vxb_step_timings* out, uint64_t cap) {
     if (cap < e->eng.timings.size()) return VXB_ECONFIG;
     std::memcpy(out, e->eng.timings.data(), sizeof(vxb_step_timings) * e->eng.timings.size());
+    return VXB_OK;
+}
+
+int vxb_result_wire_bytes(const vxb_engine* e, uint64_t* out, uint64_t cap) {
+    const Engine& g = e->eng;
+    if (g.world < 2 || cap < g.wire_sent.size()) return VXB_ECONFIG;
+    std::memcpy(out, g.wire_sent.data(), 8 * g.wire_sent.size());
+    return VXB_OK;
+}
+
+int vxb_set_recv_wire_bytes(vxb_engine* e, const uint64_t* in, uint32_t steps) {
+    Engine& g = e->eng;
+    if (g.world < 2 || steps != g.res_steps || g.timings.size() != (size_t)steps * g.workers)
+        return VXB_ECONFIG;
+    const uint32_t W = g.workers, w = g.rank;
+    for (uint32_t s = 0; s < steps; ++s) {
+        vxb_step_timings& r = g.timings[(size_t)s * W + w];
+        r.bytes_recv_intra = r.bytes_recv_inter = 0;
+        for (uint32_t h = 0; h < W; ++h)
+            if (h != w)
+                (h / g.workers_per_node == w / g.workers_per_node ? r.bytes_recv_intra
+                                                                    : r.bytes_recv_inter) +=
+                    in[(size_t)s * W + h];
+    }
     return VXB_OK;
 }
 

@@ -198,7 +198,7 @@ struct StepArgs {
     const uint4* tl;            // tile segments {tile, first entry in row, length, 0}
     const uint32_t* q_base;     // per tile: first queue slot (tiles + 1)
     uint32_t* q_cnt;            // [2][tiles] items queued per (parity, tile)
-    uint4* q;                   // [2][q_total] {entry lo, entry hi, length, 0}
+    uint64_t* q;                // [2][q_total] first entry | length << 40
     uint32_t src_self;          // global source index of shard-local neuron 0
     const uint64_t* tent;       // 8-byte tile entries (same indexing as tgt / w)
     float* i_ou_b;              // I_ou of odd steps (tile path; i_ou holds even steps)

@@ -55,6 +55,8 @@ constexpr uint32_t kTileUnroll = 4;     // synapse entries in flight per consume
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
 constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
 constexpr uint32_t kTileBucketWarps = 2;
+// queue item: first entry (bits 0-39) | segment length << 40
+constexpr uint64_t kItemBeg = (1ull << 40) - 1;
 constexpr uint32_t kTileMaxSeg = 64;    // a tile's parameter segments kept in shared memory
 constexpr uint32_t kTileMaxPset = 32;
 
@@ -120,6 +122,8 @@ __device__ __forceinline__ void tile_add(uint32_t* Bw, uint32_t per, uint64_t e)
     atomicAdd(q + per, (uint32_t)(e >> 16) & 0xffffffu);
 }
 
+// MG: one process per GPU (peers' batches, P2P routing); false: one GPU
+template <bool MG>
 __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const TileLayout L(a.tile_n);
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t par = tE & 1u;
             uint32_t* Bw = s_pend + par * 4 * per;
             const uint32_t cnt = __ldcg(a.q_cnt + par * G + blockIdx.x);
-            const uint4* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
+            const uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
             for (;;) {
                 uint32_t it = 0;
                 if (lane == 0) it = atomicAdd(&s_iwork, 1u);
@@ -240,17 +244,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 // pull the lines of a segment a few grabs ahead into L2 (no
                 // registers held): the loads below then wait on L2, not HBM
                 if (it + kTilePrefetch < cnt) {
-                    const uint4 f = __ldcg(items + it + kTilePrefetch);
-                    const uint64_t fb = ((uint64_t)f.y << 32) | f.x;
+                    const uint64_t f = __ldcg(reinterpret_cast<const unsigned long long*>(items + it + kTilePrefetch));
+                    const uint64_t fb = f & kItemBeg;
                     const char* fp = reinterpret_cast<const char*>(a.tent + fb);
-                    const char* fe = reinterpret_cast<const char*>(a.tent + fb + f.z);
+                    const char* fe = reinterpret_cast<const char*>(a.tent + fb + (f >> 40));
                     const char* ln = reinterpret_cast<const char*>(
                         reinterpret_cast<uintptr_t>(fp) & ~(uintptr_t)127) + 128 * lane;
                     if (ln < fe) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ln));
                 }
-                const uint4 d = __ldcg(items + it);
-                const uint64_t* ev = a.tent + (((uint64_t)d.y << 32) | d.x);
-                const uint32_t len = d.z;
+                const uint64_t d = __ldcg(reinterpret_cast<const unsigned long long*>(items + it));
+                const uint64_t* ev = a.tent + (d & kItemBeg);
+                const uint32_t len = (uint32_t)(d >> 40);
                 for (uint32_t k0 = 0; k0 < len; k0 += 32 * kTileUnroll) {
                     uint64_t e[kTileUnroll];
 #pragma unroll
@@ -263,6 +267,68 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         if (k0 + u * 32 + lane < len) tile_add(Bw, per, e[u]);
                 }
             }
+        };
+        // R: the peers' batches of S(tE) (one process per GPU): every CTA
+        // scans each batch for the sources whose rows have a segment in its
+        // tile (the row's tile list, ascending by tile) and delivers those
+        // segments like the local ones.  Waiting for a peer's flag is the
+        // reference's step barrier (engine.cpp:468-524).
+        auto consume_remote = [&]() {
+            if (!MG || !doE) return;
+            Exchange* ex = a.ex;
+            const uint32_t par = tE & 1u, slot = tE % kSlots;
+            uint32_t* Bw = s_pend + par * 4 * per;
+            unsigned long long waited = 0;
+            for (uint32_t li = 1; li < ex->world; ++li) {
+                const uint32_t h = (ex->rank + li) % ex->world;
+                uint32_t cnt = 0;
+                if (lane == 0) {
+                    const unsigned long long w0 = globaltimer();
+                    cnt = exchange_wait(a, h, tE, slot);
+                    waited += globaltimer() - w0;
+                }
+                cnt = __shfl_sync(0xffffffffu, cnt, 0);
+                const uint32_t* ids = ex->rx_ids[h] + (size_t)slot * ex->cap[h];
+                const uint32_t sb = ex->src_base[h];
+                for (uint32_t b0 = warp * 32; b0 < cnt; b0 += a.n_cons * 32) {
+                    uint64_t beg = 0;
+                    uint32_t len = 0;
+                    if (b0 + lane < cnt) {
+                        const uint32_t s = sb + __ldcg(ids + b0 + lane);
+                        const uint64_t k1 = __ldg(a.tl_off + s + 1);
+                        for (uint64_t k = __ldg(a.tl_off + s); k < k1; ++k) {
+                            const uint4 sg = __ldg(a.tl + k);
+                            if (sg.x >= blockIdx.x) {
+                                if (sg.x == blockIdx.x) {
+                                    beg = ldg64(a.off + s) + sg.y;
+                                    len = sg.z;
+                                }
+                                break;
+                            }
+                        }
+                    }
+                    for (unsigned m = __ballot_sync(0xffffffffu, len != 0); m; m &= m - 1) {
+                        const int l = __ffs(m) - 1;
+                        const uint64_t bb = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(beg >> 32), l) << 32) |
+                                            __shfl_sync(0xffffffffu, (uint32_t)beg, l);
+                        const uint32_t ln = __shfl_sync(0xffffffffu, len, l);
+                        if (lane == 0) my_outer += 2ull * ln;  // engine.cpp:459-463 (remote: outer)
+                        const uint64_t* ev = a.tent + bb;
+                        for (uint32_t k0 = 0; k0 < ln; k0 += 32 * kTileUnroll) {
+                            uint64_t e[kTileUnroll];
+#pragma unroll
+                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
+                                const uint32_t k = k0 + u * 32 + lane;
+                                if (k < ln) e[u] = ld_stream(ev + k, pol_syn);
+                            }
+#pragma unroll
+                            for (uint32_t u = 0; u < kTileUnroll; ++u)
+                                if (k0 + u * 32 + lane < ln) tile_add(Bw, per, e[u]);
+                        }
+                    }
+                }
+            }
+            if (lane == 0 && waited && a.phase_wait) atomicMax(a.phase_wait + ph, waited);
         };
         // N: advance I_ou to tA (ou_kernel, model.hpp:88-90, xi = stream word
         // tA, engine.cpp:551-558) for the tile: consumed by E(tA) in ph + 1
@@ -423,6 +489,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     }
                 }
                 // spike log staging + rates (engine.cpp:400-404), warp aggregated
+                bool ovf_route = false;
                 const unsigned ball = __ballot_sync(0xffffffffu, spiked);
                 if (ball) {
                     unsigned base = 0;
@@ -432,8 +499,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         const unsigned rank = __popc(ball & ((1u << lane) - 1u));
                         if (base + rank < kSpkStage) {
                             s_spk[base + rank] = i;  // bucketed after the update (B)
-                        } else {  // staging full: log and bucket this spike directly
+                        } else {  // staging full: log, route and bucket this spike directly
                             a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                            ovf_route = MG;
                             const uint64_t row = tally(i);
                             const uint32_t par = tA & 1u;
                             const uint64_t k1 = __ldg(a.tl_off + a.src_self + i + 1);
@@ -442,7 +510,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                                 const uint32_t pos = atomicAdd(a.q_cnt + par * G + sg.x, 1u);
                                 const uint64_t b = row + sg.y;
                                 a.q[(size_t)par * a.q_total + __ldg(a.q_base + sg.x) + pos] =
-                                    make_uint4((uint32_t)b, (uint32_t)(b >> 32), sg.z, 0u);
+                                    b | ((uint64_t)sg.z << 40);
                             }
                         }
                         const uint32_t unit = segp[seg].unit;
@@ -451,6 +519,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             atomicAdd(&a.rates[(size_t)unit * a.steps + ph], (unsigned)__popc(peers));
                     }
                 }
+                if (MG && __any_sync(0xffffffffu, ovf_route))
+                    if (exchange_route(a, i, ovf_route, tA % kSlots)) __threadfence_system();
                 ch = chn;
                 i = inext;
             }
@@ -486,7 +556,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     }
                 }
                 named_sync(2, nbt);
-                uint4* qp = a.q + (size_t)par * a.q_total;
+                uint64_t* qp = a.q + (size_t)par * a.q_total;
                 for (uint32_t k = bt; k < nst; k += nbt) {
                     const uint32_t s = a.src_self + s_spk[k];
                     const uint64_t row = ldg64(a.off + s);
@@ -495,11 +565,20 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         const uint4 sg = __ldg(a.tl + q);
                         const uint32_t pos = s_qb[sg.x] + atomicAdd(&s_hist[sg.x], 1u);
                         const uint64_t b = row + sg.y;
-                        qp[pos] = make_uint4((uint32_t)b, (uint32_t)(b >> 32), sg.z, 0u);
+                        qp[pos] = b | ((uint64_t)sg.z << 40);
                     }
                 }
                 named_sync(2, nbt);
                 for (uint32_t t = bt; t < G; t += nbt) s_hist[t] = 0u;
+                // the peers' ids of S(tA): P2P stores into their receive slots
+                // (engine.cpp:416-437); published after the phase barrier
+                if (MG) {
+                    bool sent = false;
+                    const uint32_t nr = (nst + 31u) & ~31u;
+                    for (uint32_t k = bt; k < nr; k += nbt)
+                        sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % kSlots);
+                    if (sent) __threadfence_system();
+                }
             }
             if (a.prof && bt == 0) s_t[1] = globaltimer();
             noise();
@@ -507,6 +586,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             consume();
         } else {
             consume();
+            if (MG) consume_remote();
             if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
             noise();
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
@@ -531,9 +611,21 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 if (doA) a.seg_end[ph] = ctl->spk_cursor;
                 if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
                 a.phase_ns[ph + 1] = globaltimer();
-                ctl->stop = atomicAdd(&ctl->err, 0ull) != ~0ull ? 1u : 0u;
+                // one stop decision for the whole grid
+                ctl->stop = (atomicAdd(&ctl->err, 0ull) != ~0ull ||
+                             (MG && (atomicAdd(&a.ex->timeout, 0u) != 0u ||
+                                     atomicAdd(&a.ex->peer_abort, 0u) != 0u))) ? 1u : 0u;
             },
-            [&] {});
+            [&] {
+                if (MG) {
+                    // a failed step publishes no batch (the reference's worker
+                    // throws before phase B); the peers see the abort word
+                    if (ctl->stop)
+                        exchange_abort(a);
+                    else if (doA)
+                        exchange_publish(a, tA);
+                }
+            });
         if (threadIdx.x == 0) {
             s_stop = (int)ld_acquire(&ctl->stop);
             s_nspk = s_fwork = s_nwork = s_iwork = 0;
@@ -584,7 +676,8 @@ __global__ void tile_segments_kernel(const uint64_t* __restrict__ off, const uin
                                      uint32_t n_src, uint32_t per,
                                      unsigned long long* __restrict__ cnt,   // PASS 0: [n_src]
                                      const unsigned long long* __restrict__ tl_off,  // PASS 1
-                                     uint4* __restrict__ tl, uint32_t* __restrict__ tile_cap) {
+                                     uint4* __restrict__ tl, uint32_t* __restrict__ tile_cap,
+                                     unsigned int* __restrict__ too_long) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -618,6 +711,7 @@ __global__ void tile_segments_kernel(const uint64_t* __restrict__ off, const uin
                 const uint32_t beg = __ldcg(&tl[q].y);
                 const uint32_t nxt = q + 1 < e ? __ldcg(&tl[q + 1].y) : (uint32_t)(r1 - r0);
                 tl[q].z = nxt - beg;
+                if (nxt - beg >= (1u << 24)) atomicExch(too_long, 1u);  // queue items hold 24 bits
             }
         }
     }

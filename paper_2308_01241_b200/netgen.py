@@ -1180,10 +1180,30 @@ class DistributedSimInstance(SimInstance):
     def advance(self, steps: int, fetch: bool = True):
         """Collective advance.  With the BOLD readout on, the ranks add their
         voxel counts (each holds its own units' spikes) and every rank runs
-        the hemodynamics on the totals (vxb_hemo_feed_counts)."""
-        if not (self._hemo_every and self.world > 1):
+        the hemodynamics on the totals (vxb_hemo_feed_counts).  With timing
+        rows, the ranks exchange the wire bytes of the batches they sent so
+        every row carries its received bytes too (engine.cpp:495-523)."""
+        if self.world > 1 and self._opt.record_timings:
+            rc = self._lib.vxb_advance(self._h, steps)
+            if rc != 0:
+                self._err(rc)
+            sent = np.zeros((steps, self.world), np.uint64)
+            if sent.size:
+                self._lib.vxb_result_wire_bytes(self._h, ptr(sent), sent.size)
+            parts = self._all_gather(sent)
+            recv = np.ascontiguousarray(np.stack([p[:, self.rank] for p in parts], axis=1),
+                                        np.uint64)
+            if recv.size:
+                rc = self._lib.vxb_set_recv_wire_bytes(self._h, ptr(recv), steps)
+                if rc != 0:
+                    self._err(rc)
+            if not self._hemo_every:
+                return self.result() if fetch else None
+            r = self.result()
+        elif not (self._hemo_every and self.world > 1):
             return super().advance(steps, fetch)
-        r = super().advance(steps, fetch=True)
+        else:
+            r = super().advance(steps, fetch=True)
         parts = self._all_gather(r.voxel_counts)
         tot = np.ascontiguousarray(np.sum(np.stack(parts), axis=0, dtype=np.uint64)
                                    .astype(np.uint32))

@@ -55,6 +55,8 @@ def main():
         "flops": {k: r1.flops[k] + r2.flops[k] for k in r1.flops},
         "snap": snap,
         "bold": [r1.bold, r2.bold],
+        # this rank's StepTimings rows (its own worker's rows are filled)
+        "timings": [r.timings[r.timings["worker"] == rank] for r in (r1, r2)],
     }
     out = [None] * world
     dist.all_gather_object(out, mine)
@@ -63,7 +65,10 @@ def main():
         from refnet import RefNet, RefSim
         ref_net = RefNet(cfg)
         rs = RefSim(ref_net, SimOptions(steps=steps, dt_ms=cfg["dt_ms"], probe_gids=probes))
-        a, b = rs.advance(steps // 3), rs.advance(steps - steps // 3)
+        a = rs.advance(steps // 3)
+        ta = rs.timings()
+        b = rs.advance(steps - steps // 3)
+        tb = rs.timings()
         ref_raster = sorted(zip(a.raster["step"].tolist() + b.raster["step"].tolist(),
                                 a.raster["gid"].tolist() + b.raster["gid"].tolist()))
         raster = sorted(x for o in out for x in o["raster"])
@@ -90,8 +95,24 @@ def main():
             g, r = out[0]["bold"][k], ref_bold[k]
             bold_ok = bold_ok and g.shape == r.shape and \
                 float(np.max(np.abs(g - r))) <= 1e-12 * float(np.max(np.abs(r))) + 1e-15
+        # wire-byte counters (engine.cpp:495-523): every row equals the
+        # reference's; send / receive spans telescope
+        timings_ok = True
+        for k, tref in enumerate((ta, tb)):
+            rows = np.concatenate([o["timings"][k] for o in out])
+            rows = rows[np.lexsort((rows["worker"], rows["step"]))]
+            timings_ok = timings_ok and rows.shape == tref.shape
+            for f in ("step", "worker", "spikes", "bytes_sent_intra", "bytes_sent_inter",
+                      "bytes_recv_intra", "bytes_recv_inter"):
+                timings_ok = timings_ok and bool(np.array_equal(rows[f], tref[f]))
+            tt = rows["t"]
+            timings_ok = timings_ok and bool(np.array_equal(
+                rows["recv_intra_ns"] + rows["recv_inter_ns"], tt[:, 10] - tt[:, 9]))
+            timings_ok = timings_ok and bool(np.array_equal(
+                rows["send_intra_ns"] + rows["send_inter_ns"], tt[:, 8] - tt[:, 7]))
         res = {
             "world": world, "spikes": len(raster), "ref_spikes": len(ref_raster),
+            "timings_equal": timings_ok,
             "bold_equal": bool(bold_ok),
             "raster_equal": raster == ref_raster,
             "rates_equal": bool(np.array_equal(rates, np.concatenate([a.rates, b.rates], axis=1))),

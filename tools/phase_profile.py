@@ -32,11 +32,27 @@ from paper_2308_01241_b200.engine import SimOptions  # noqa: E402
 cfg = bench.workload_cfg(voxels=args.voxels)
 if args.silent:
     cfg["regions"]["subcortex"]["ou_mean"] = 0.0
+
+ws = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+if ws > 1:  # under torchrun: config 2 weak-scaled, one rank per GPU
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo")
+    cfg = bench.workload_cfg(voxels=args.voxels * ws, workers=ws)
+    cfg["partition"]["method"] = "sequential"
+    if args.silent:
+        cfg["regions"]["subcortex"]["ou_mean"] = 0.0
 net = netgen.build_network(cfg)
-opt = SimOptions(steps=args.steps, record_raster=False, record_timings=False)
-with netgen.GeneratedSimInstance(net, opt) as sim:
+opt = SimOptions(steps=args.steps, record_raster=False, record_timings=False, device=rank)
+sim = (netgen.DistributedSimInstance(net, opt, rank, ws) if ws > 1
+       else netgen.GeneratedSimInstance(net, opt))
+if rank == 0:
     print(sim.schedule_info(), flush=True)
-    for _ in range(args.reps):
-        r = sim.advance(args.steps)
-        print(f"advance: {r.device_ms / args.steps * 1e3:.1f} us/step, {r.events} events, "
-              f"{r.total_spikes} spikes", flush=True)
+for _ in range(args.reps):
+    r = sim.advance(args.steps)
+    print(f"rank {rank}: advance {r.device_ms / args.steps * 1e3:.1f} us/step, {r.events} events, "
+          f"{r.total_spikes} spikes, exchange wait {r.exchange_wait_ms / args.steps * 1e3:.1f} us/step",
+          flush=True)
+sim.close()

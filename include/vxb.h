@@ -236,6 +236,12 @@ uint64_t vxb_result_d2h_bytes(const vxb_engine* e);
  * StepTimings received-byte counters (engine.cpp:495-523). */
 int vxb_result_wire_bytes(const vxb_engine* e, uint64_t* out, uint64_t cap);
 int vxb_set_recv_wire_bytes(vxb_engine* e, const uint64_t* in, uint32_t steps);
+/* crossing_matrix (netgen.hpp:104-107, netgen.cpp:331-355; BuiltNetwork::
+ * crossing, pipeline.cpp:122): synapses per (source worker, target worker),
+ * [workers][workers] row-major, counted on the device from the delivery
+ * tables at load.  With one worker per rank only column `rank` is filled:
+ * the caller adds the ranks' matrices. */
+int vxb_crossing_matrix(const vxb_engine* e, uint64_t* out, uint64_t cap);
 /* Kernel launches issued by the last vxb_advance. */
 uint64_t vxb_result_launches(const vxb_engine* e);
 /* The delivery schedule chosen for this network as a JSON object (path, grid,

@@ -46,6 +46,7 @@ struct RefNet {
     NetworkTables tables;
     uint64_t synapse_count = 0;
     double build_seconds = 0;
+    std::vector<std::vector<uint64_t>> crossing;  // BuiltNetwork::crossing (pipeline.cpp:122)
 };
 
 struct RefSim {
@@ -133,6 +134,7 @@ void* ref_build(const char* cfg_json, int even_workers, char* err, int errlen) {
             net->layout = std::move(b.layout);
             net->tables = std::move(b.tables);
             net->synapse_count = b.synapse_count;
+            net->crossing = std::move(b.crossing);
         } else {
             net->graph = build_connectome(net->cfg);
             MicrocolumnSpec mc;
@@ -191,6 +193,15 @@ uint32_t ref_n_voxels(void* h) {
 }
 uint64_t ref_total_neurons(void* h) { return static_cast<RefNet*>(h)->layout.total_neurons; }
 uint64_t ref_synapse_count(void* h) { return static_cast<RefNet*>(h)->synapse_count; }
+// BuiltNetwork::crossing [src worker][dst worker] (netgen.cpp:331-355); 0 if
+// the network was not built through build_network
+int ref_crossing(void* h, uint64_t* out, uint32_t workers) {
+    const auto& c = static_cast<RefNet*>(h)->crossing;
+    if (c.size() != workers) return 0;
+    for (uint32_t a = 0; a < workers; ++a)
+        for (uint32_t b = 0; b < workers; ++b) out[a * workers + b] = c[a][b];
+    return 1;
+}
 uint32_t ref_worker_n(void* h, uint32_t w) {
     return static_cast<uint32_t>(static_cast<RefNet*>(h)->tables.workers.at(w).neurons.size());
 }

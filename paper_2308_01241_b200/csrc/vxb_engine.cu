@@ -271,6 +271,8 @@ struct Engine {
     std::vector<unsigned long long> dst_full;  // world == 1: full dst mask per shard-local neuron
     std::vector<uint64_t> wire_sent;           // world > 1: [step][dst worker] bytes sent
     std::vector<uint64_t> phase_wait_all;      // per phase of the last advance: max CTA wait (ns)
+    std::vector<uint64_t> crossing;            // [src worker][dst worker] synapses held here
+    void compute_crossing();
     void account_wire_bytes(uint32_t steps);
     std::vector<uint32_t> rates;        // [unit][steps]
     std::vector<float> probe_v, probe_i;
@@ -627,6 +629,10 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
         }
     }
     d_keys.release();
+    if (donor)
+        crossing = donor->crossing;
+    else
+        compute_crossing();
     if (world == 1 && dst_full.empty() && !have_src.empty())  // generated tables
         dst_full.assign(have_src.begin(), have_src.begin() + n);
 
@@ -1390,6 +1396,28 @@ void Engine::setup_tiles() {
     tile_smem = L.total;
     tile_grid = (uint32_t)sms;
     (void)tiles;
+}
+
+// crossing_matrix (netgen.cpp:331-355, BuiltNetwork::crossing): synapses
+// per (source worker, target worker) of the tables on this device; with one
+// worker per rank only the rank's own column is nonzero (the caller sums the
+// ranks' matrices).
+void Engine::compute_crossing() {
+    crossing.assign((size_t)workers * workers, 0);
+    if (n_syn == 0) return;
+    DevBuf<uint32_t> sb, wb;
+    DevBuf<unsigned long long> out;
+    sb.alloc(workers + 1);
+    wb.alloc(workers + 1);
+    out.alloc((size_t)workers * workers);
+    out.zero(stream);
+    CK(cudaMemcpyAsync(sb.p, src_base.data(), 4ull * (workers + 1), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(wb.p, wbase.data(), 4ull * (workers + 1), cudaMemcpyHostToDevice, stream));
+    crossing_kernel<<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p), d_tgt.p,
+                                              n_src, sb.p, wb.p, workers, out.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(crossing.data(), out.p, 8 * crossing.size(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
 }
 
 // Per-instance state of the tile path: I_ou is kept by step parity (the
@@ -2162,6 +2190,13 @@ int vxb_set_recv_wire_bytes(vxb_engine* e, const uint64_t* in, uint32_t steps) {
                                                                     : r.bytes_recv_inter) +=
                     in[(size_t)s * W + h];
     }
+    return VXB_OK;
+}
+
+int vxb_crossing_matrix(const vxb_engine* e, uint64_t* out, uint64_t cap) {
+    const Engine& g = e->eng;
+    if (cap < g.crossing.size()) return VXB_ECONFIG;
+    std::memcpy(out, g.crossing.data(), 8 * g.crossing.size());
     return VXB_OK;
 }
 

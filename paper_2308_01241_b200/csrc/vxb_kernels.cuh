@@ -1408,6 +1408,42 @@ __global__ void block_offsets_kernel(const uint64_t* __restrict__ off,
     }
 }
 
+// crossing_matrix (netgen.cpp:331-355) from the out-CSR: synapses per
+// (source worker, target worker).  Worker bases in shared memory, per-block
+// counts in shared memory, flushed once per block.  One warp per row.
+__global__ void crossing_kernel(const uint64_t* __restrict__ off, const uint32_t* __restrict__ tgt,
+                                uint32_t n_src, const uint32_t* __restrict__ src_base,
+                                const uint32_t* __restrict__ wbase, uint32_t W,
+                                unsigned long long* __restrict__ out) {
+    __shared__ uint32_t s_sb[65], s_wb[65];
+    __shared__ unsigned int s_c[64 * 64];
+    for (uint32_t k = threadIdx.x; k <= W; k += blockDim.x) {
+        s_sb[k] = src_base[k];
+        s_wb[k] = wbase[k];
+    }
+    for (uint32_t k = threadIdx.x; k < W * W; k += blockDim.x) s_c[k] = 0;
+    __syncthreads();
+    auto bin = [&](const uint32_t* b, uint32_t x) {  // last w with b[w] <= x
+        uint32_t lo = 0, hi = W;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (b[mid] <= x) lo = mid; else hi = mid;
+        }
+        return lo;
+    };
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t s = warp; s < n_src; s += nwarps) {
+        const uint32_t sw = bin(s_sb, (uint32_t)s);
+        for (uint64_t k = off[s] + lane; k < off[s + 1]; k += 32)
+            atomicAdd(&s_c[sw * W + bin(s_wb, tgt[k] & 0x7fffffffu)], 1u);
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < W * W; k += blockDim.x)
+        if (s_c[k]) atomicAdd(out + k, (unsigned long long)s_c[k]);
+}
+
 __global__ void mask_check_kernel(const unsigned long long* __restrict__ have,
                                   const unsigned long long* __restrict__ mask, uint32_t n,
                                   unsigned long long* __restrict__ first_bad) {

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     uint32_t* s_pend = reinterpret_cast<uint32_t*>(smem + L.pend);  // [parity][receptor][per]
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base;
+    __shared__ uint32_t s_ravail, s_rdone;  // MG: peers' items appended / scan done
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
     __shared__ uint32_t s_hist[kTileMaxGrid], s_qb[kTileMaxGrid];  // per-tile bucketing
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         s_seg_lo = lo;
         s_nseg = cnt;
         s_nspk = s_fwork = s_nwork = s_iwork = 0;
+        s_ravail = s_rdone = 0;
         s_t[0] = s_t[1] = s_t[2] = s_t[3] = 0;
     }
     for (uint32_t k = threadIdx.x; k < kTileMaxGrid; k += blockDim.x) s_hist[k] = 0;
@@ -230,16 +232,28 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
 
         // C: deliver S(tE) into the pending tile of parity tE (one queued
         // segment per warp grab, kTileUnroll entries in flight per lane)
+        // (MG: the peers' segments for this tile are appended after the
+        // local items by the scanning warp, see R; a consumer that runs out
+        // waits for them until the scan is done)
         auto consume = [&]() {
             if (!doE) return;
             const uint32_t par = tE & 1u;
             uint32_t* Bw = s_pend + par * 4 * per;
-            const uint32_t cnt = __ldcg(a.q_cnt + par * G + blockIdx.x);
+            const uint32_t cnt0 = __ldcg(a.q_cnt + par * G + blockIdx.x);
             const uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
             for (;;) {
                 uint32_t it = 0;
                 if (lane == 0) it = atomicAdd(&s_iwork, 1u);
                 it = __shfl_sync(0xffffffffu, it, 0);
+                uint32_t cnt = cnt0;
+                if (MG) {
+                    for (;;) {
+                        const bool done = *reinterpret_cast<volatile uint32_t*>(&s_rdone) != 0u;
+                        cnt = cnt0 + *reinterpret_cast<volatile uint32_t*>(&s_ravail);
+                        if (it < cnt || done) break;
+                        __nanosleep(200);
+                    }
+                }
                 if (it >= cnt) break;
                 // pull the lines of a segment a few grabs ahead into L2 (no
                 // registers held): the loads below then wait on L2, not HBM
@@ -268,16 +282,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 }
             }
         };
-        // R: the peers' batches of S(tE) (one process per GPU): every CTA
-        // scans each batch for the sources whose rows have a segment in its
-        // tile (the row's tile list, ascending by tile) and delivers those
-        // segments like the local ones.  Waiting for a peer's flag is the
-        // reference's step barrier (engine.cpp:468-524).
-        auto consume_remote = [&]() {
+        // R (one process per GPU): the peers' batches of S(tE).  One warp of
+        // every CTA waits for each peer's flag (the reference's step barrier,
+        // engine.cpp:468-524), scans the batch for the sources whose rows
+        // have a segment in its tile (the row's tile list, ascending by tile)
+        // and appends those segments to the tile's queue after the local
+        // items, where every consumer picks them up.
+        auto scan_remote = [&]() {
             if (!MG || !doE) return;
             Exchange* ex = a.ex;
             const uint32_t par = tE & 1u, slot = tE % kSlots;
-            uint32_t* Bw = s_pend + par * 4 * per;
+            const uint32_t cnt0 = __ldcg(a.q_cnt + par * G + blockIdx.x);
+            uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x] + cnt0;
+            uint32_t nrem = 0;
             unsigned long long waited = 0;
             for (uint32_t li = 1; li < ex->world; ++li) {
                 const uint32_t h = (ex->rank + li) % ex->world;
@@ -290,9 +307,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 cnt = __shfl_sync(0xffffffffu, cnt, 0);
                 const uint32_t* ids = ex->rx_ids[h] + (size_t)slot * ex->cap[h];
                 const uint32_t sb = ex->src_base[h];
-                for (uint32_t b0 = warp * 32; b0 < cnt; b0 += a.n_cons * 32) {
-                    uint64_t beg = 0;
-                    uint32_t len = 0;
+                for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
+                    uint64_t item = 0;
                     if (b0 + lane < cnt) {
                         const uint32_t s = sb + __ldcg(ids + b0 + lane);
                         const uint64_t k1 = __ldg(a.tl_off + s + 1);
@@ -300,35 +316,27 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             const uint4 sg = __ldg(a.tl + k);
                             if (sg.x >= blockIdx.x) {
                                 if (sg.x == blockIdx.x) {
-                                    beg = ldg64(a.off + s) + sg.y;
-                                    len = sg.z;
+                                    item = (ldg64(a.off + s) + sg.y) | ((uint64_t)sg.z << 40);
+                                    my_outer += 2ull * sg.z;  // engine.cpp:459-463 (remote: outer)
                                 }
                                 break;
                             }
                         }
                     }
-                    for (unsigned m = __ballot_sync(0xffffffffu, len != 0); m; m &= m - 1) {
-                        const int l = __ffs(m) - 1;
-                        const uint64_t bb = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(beg >> 32), l) << 32) |
-                                            __shfl_sync(0xffffffffu, (uint32_t)beg, l);
-                        const uint32_t ln = __shfl_sync(0xffffffffu, len, l);
-                        if (lane == 0) my_outer += 2ull * ln;  // engine.cpp:459-463 (remote: outer)
-                        const uint64_t* ev = a.tent + bb;
-                        for (uint32_t k0 = 0; k0 < ln; k0 += 32 * kTileUnroll) {
-                            uint64_t e[kTileUnroll];
-#pragma unroll
-                            for (uint32_t u = 0; u < kTileUnroll; ++u) {
-                                const uint32_t k = k0 + u * 32 + lane;
-                                if (k < ln) e[u] = ld_stream(ev + k, pol_syn);
-                            }
-#pragma unroll
-                            for (uint32_t u = 0; u < kTileUnroll; ++u)
-                                if (k0 + u * 32 + lane < ln) tile_add(Bw, per, e[u]);
-                        }
-                    }
+                    const unsigned ball = __ballot_sync(0xffffffffu, item != 0);
+                    if (item) items[nrem + __popc(ball & ((1u << lane) - 1u))] = item;
+                    nrem += __popc(ball);
+                    __threadfence_block();
+                    __syncwarp();
+                    if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&s_ravail) = nrem;
                 }
             }
-            if (lane == 0 && waited && a.phase_wait) atomicMax(a.phase_wait + ph, waited);
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) {
+                *reinterpret_cast<volatile uint32_t*>(&s_rdone) = 1u;
+                if (waited && a.phase_wait) atomicMax(a.phase_wait + ph, waited);
+            }
         };
         // N: advance I_ou to tA (ou_kernel, model.hpp:88-90, xi = stream word
         // tA, engine.cpp:551-558) for the tile: consumed by E(tA) in ph + 1
@@ -585,8 +593,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
             consume();
         } else {
+            if (MG && warp == 0) scan_remote();
             consume();
-            if (MG) consume_remote();
             if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
             noise();
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
@@ -629,6 +637,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         if (threadIdx.x == 0) {
             s_stop = (int)ld_acquire(&ctl->stop);
             s_nspk = s_fwork = s_nwork = s_iwork = 0;
+            s_ravail = s_rdone = 0;
         }
         __syncthreads();
         if (s_stop) break;

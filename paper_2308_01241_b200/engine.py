@@ -413,6 +413,16 @@ class SimInstance:
     def workers(self) -> int:
         return int(self._lib.vxb_workers(self._h))
 
+    def crossing_matrix(self) -> np.ndarray:
+        """BuiltNetwork::crossing (netgen.cpp:331-355): synapses per (source
+        worker, target worker) of the tables this instance holds."""
+        w = self.workers
+        out = np.zeros((w, w), np.uint64)
+        rc = self._lib.vxb_crossing_matrix(self._h, ptr(out), out.size)
+        if rc != 0:
+            self._err(rc)
+        return out
+
     def schedule_info(self) -> dict:
         """The delivery schedule the engine chose (and any tuning knob applied
         from the environment under VXB_TUNING=1), for benchmark records."""

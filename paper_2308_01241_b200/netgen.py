@@ -1177,6 +1177,12 @@ class DistributedSimInstance(SimInstance):
                 self._err(rc)
             barrier()
 
+    def crossing_matrix(self) -> np.ndarray:
+        """Collective: the full [src worker][dst worker] matrix, each rank
+        contributing the column of its own targets."""
+        return np.sum(np.stack(self._all_gather(super().crossing_matrix())), axis=0,
+                      dtype=np.uint64)
+
     def advance(self, steps: int, fetch: bool = True):
         """Collective advance.  With the BOLD readout on, the ranks add their
         voxel counts (each holds its own units' spikes) and every rank runs

@@ -58,12 +58,14 @@ def main():
         # this rank's StepTimings rows (its own worker's rows are filled)
         "timings": [r.timings[r.timings["worker"] == rank] for r in (r1, r2)],
     }
+    crossing = sim.crossing_matrix()  # collective
     out = [None] * world
     dist.all_gather_object(out, mine)
     sim.close()
     if rank == 0:
         from refnet import RefNet, RefSim
         ref_net = RefNet(cfg)
+        crossing_ok = bool(np.array_equal(crossing, ref_net.crossing()))
         rs = RefSim(ref_net, SimOptions(steps=steps, dt_ms=cfg["dt_ms"], probe_gids=probes))
         a = rs.advance(steps // 3)
         ta = rs.timings()
@@ -112,7 +114,7 @@ def main():
                 rows["send_intra_ns"] + rows["send_inter_ns"], tt[:, 8] - tt[:, 7]))
         res = {
             "world": world, "spikes": len(raster), "ref_spikes": len(ref_raster),
-            "timings_equal": timings_ok,
+            "timings_equal": timings_ok, "crossing_equal": crossing_ok,
             "bold_equal": bool(bold_ok),
             "raster_equal": raster == ref_raster,
             "rates_equal": bool(np.array_equal(rates, np.concatenate([a.rates, b.rates], axis=1))),

@@ -52,6 +52,7 @@ def ref_lib():
             "ref_n_voxels": (u32, [P]),
             "ref_total_neurons": (u64, [P]),
             "ref_synapse_count": (u64, [P]),
+            "ref_crossing": (C.c_int, [P, P, u32]),
             "ref_worker_n": (u32, [P, u32]),
             "ref_worker_nsyn": (u64, [P, u32]),
             "ref_units": (None, [P, P, P, P]),
@@ -240,6 +241,14 @@ class RefNet:
     @property
     def total_neurons(self) -> int:
         return int(ref_lib().ref_total_neurons(self._h))
+
+    def crossing(self) -> np.ndarray:
+        """BuiltNetwork::crossing, [src worker][dst worker] synapse counts."""
+        w = len(self.tables.workers)
+        out = np.zeros((w, w), np.uint64)
+        if not ref_lib().ref_crossing(self._h, ptr(out), w):
+            raise RuntimeError("network not built through build_network")
+        return out
 
     def save_tables(self, directory) -> None:
         err = C.create_string_buffer(1024)

@@ -486,3 +486,19 @@ def test_ring_multiworker_both_paths(monkeypatch, path):
     assert_same(b, rb)
     for w in range(3):
         assert np.array_equal(snaps[w], rs.membrane_snapshot(w))
+
+
+def test_crossing_matrix_matches_reference():
+    """crossing_matrix (netgen.cpp:331-355, BuiltNetwork::crossing) counted on
+    the device from the delivery tables equals the reference pipeline's, for
+    loaded tables and for tables generated on the device."""
+    from paper_2308_01241_b200 import netgen
+    cfg = make_config(seed=13, voxels=6, npv=300, k_in=25, rho=0.3, workers=3,
+                      partition="greedy")
+    net = RefNet(cfg)
+    ref = net.crossing()
+    assert ref.sum() == net.tables.synapse_count and ref[0, 1] + ref[1, 0] > 0
+    with SimInstance(net.tables, SimOptions(steps=1)) as sim:
+        assert np.array_equal(sim.crossing_matrix(), ref)
+    with netgen.GeneratedSimInstance(netgen.build_network(cfg), SimOptions(steps=1)) as sim:
+        assert np.array_equal(sim.crossing_matrix(), ref)

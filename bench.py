@@ -382,9 +382,14 @@ def run_b200(args):
             sets.append((u, buf))
         windows.append(sets)
 
+    # one boundary crossing per window: set_conductances of every local unit
+    # (vxb_set_conductances_batch, item-by-item semantics, copies on the
+    # host cores)
+    from paper_2308_01241_b200.engine import ConductanceBatch
+    batches = [ConductanceBatch([(u, 0, buf) for u, buf in w]) for w in windows]
+
     def feed(i):
-        for u, buf in windows[i % 2]:
-            sim.set_conductances(u, 0, buf)
+        sim.set_conductances_batch(batches[i % 2])
 
     for i in range(args.warmup):
         feed(i)

@@ -253,6 +253,15 @@ int vxb_schedule_info(const vxb_engine* e, char* out, uint64_t cap);
 /* ---- state access -------------------------------------------------------- */
 int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor,
                          const float* values, uint32_t n);
+/* vxb_set_conductances for `count` (unit, receptor, values[i], counts[i])
+ * items in one call: the same result and errors as calling it item by item
+ * in order (staging stops at the first failing item, whose index goes to
+ * *failed_index; `count` when all succeed), with the validation and the
+ * copies spread over the host's cores.  The assimilation caller's per-window
+ * input (assim.cpp:91-107) in one crossing of the boundary. */
+int vxb_set_conductances_batch(vxb_engine* e, uint32_t count, const uint32_t* units,
+                               const int32_t* receptors, const float* const* values,
+                               const uint32_t* counts, uint32_t* failed_index);
 int vxb_membrane_snapshot(const vxb_engine* e, uint16_t worker, float* out,
                           uint32_t cap);
 uint32_t vxb_worker_neurons(const vxb_engine* e, uint16_t worker);

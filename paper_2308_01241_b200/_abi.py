@@ -160,7 +160,7 @@ EXPORTS = [
     "vxb_result_bold_size", "vxb_result_bold", "vxb_debug_bold_from_drive",
     "vxb_result_voxel_counts", "vxb_hemo_feed_counts", "vxb_create_member",
     "vxb_schedule_info", "vxb_build_hash", "vxb_result_wire_bytes", "vxb_set_recv_wire_bytes",
-    "vxb_crossing_matrix",
+    "vxb_crossing_matrix", "vxb_set_conductances_batch",
 ]
 
 _lib = None
@@ -194,6 +194,7 @@ def _declare(lib):
         "vxb_build_hash": (C.c_char_p, []),
         "vxb_result_wire_bytes": (C.c_int, [P, P, C.c_uint64]),
         "vxb_crossing_matrix": (C.c_int, [P, P, C.c_uint64]),
+        "vxb_set_conductances_batch": (C.c_int, [P, C.c_uint32, P, P, P, P, P]),
         "vxb_set_recv_wire_bytes": (C.c_int, [P, P, C.c_uint32]),
         "vxb_set_conductances": (C.c_int, [P, C.c_uint32, C.c_int, P, C.c_uint32]),
         "vxb_membrane_snapshot": (C.c_int, [P, C.c_uint16, P, C.c_uint32]),

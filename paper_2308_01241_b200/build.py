@@ -23,8 +23,8 @@ MARKER = b"VXB_SRC_HASH="
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--fmad=false",
-    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
-    "-shared", "-lcudart",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3,-fopenmp",
+    "-shared", "-lcudart", "-lgomp",
 ]
 
 

@@ -27,6 +27,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
@@ -291,6 +293,9 @@ struct Engine {
     DevBuf<float> d_cstage;
     DevBuf<uint4> d_crec;
     uint32_t stage_conductances(uint32_t unit, int receptor, const float* values, uint32_t n);
+    int32_t& slot_of(uint32_t unit, int receptor);
+    void stage_batch(uint32_t count, const uint32_t* units_, const int32_t* receptors,
+                     const float* const* values, const uint32_t* ns, uint32_t* failed);
     void flush_conductances(bool sync);
 
     // BOLD-proxy readout on the device (vxb_hemo.cuh), enabled by
@@ -2234,8 +2239,8 @@ int vxb_set_conductances(vxb_engine* e, uint32_t unit, int receptor, const float
     }
 }
 
-uint32_t Engine::stage_conductances(uint32_t unit, int receptor, const float* values,
-                                    uint32_t n) {
+// The staging record of (unit, receptor), created with room for a full unit.
+int32_t& Engine::slot_of(uint32_t unit, int receptor) {
     const uint32_t key = unit * 4 + (uint32_t)receptor;
     if (cond_slot.size() != 4ull * n_units) cond_slot.assign(4ull * n_units, -1);
     if (cond_slot[key] < 0) {  // new record, with room for a full unit
@@ -2247,7 +2252,85 @@ uint32_t Engine::stage_conductances(uint32_t unit, int receptor, const float* va
         cond_rec.push_back(make_uint4((uint32_t)cond_total, 4 * base + (uint32_t)receptor, 0u, key));
         cond_total += full;
     }
-    uint4& r = cond_rec[cond_slot[key]];  // a later set overwrites the earlier values
+    return cond_slot[key];
+}
+
+// set_conductances of many units in one call, with the sequential
+// semantics of calling it item by item (engine.cpp:829-844: argument errors
+// stage nothing of the item, a non-finite / negative value stages the
+// item's valid prefix; either stops the sequence), but the validation and
+// the copies of the items run on the host's cores in parallel.
+void Engine::stage_batch(uint32_t count, const uint32_t* uu, const int32_t* rr,
+                         const float* const* vals, const uint32_t* ns, uint32_t* failed) {
+    *failed = count;
+    uint32_t fa = count;  // first argument error
+    std::string fa_msg;
+    for (uint32_t i = 0; i < count && fa == count; ++i) {
+        if (uu[i] >= n_units) fa_msg = "unit out of range";
+        else if (rr[i] < 0 || rr[i] >= 4) fa_msg = "receptor out of range";
+        else if (ns[i] != units[uu[i]].neurons) fa_msg = "conductance vector size does not match unit";
+        if (!fa_msg.empty()) fa = i;
+    }
+    std::vector<uint32_t> keys(fa);
+    bool dup = false;
+    {
+        std::vector<uint8_t> seen(4ull * n_units, 0);
+        for (uint32_t i = 0; i < fa; ++i) {
+            keys[i] = uu[i] * 4 + (uint32_t)rr[i];
+            dup |= seen[keys[i]] != 0;
+            seen[keys[i]] = 1;
+        }
+    }
+    if (dup) {  // the same (unit, receptor) twice: the order matters, stage one by one
+        for (uint32_t i = 0; i < count; ++i) {
+            *failed = i;
+            if (i == fa) throw ConfigError(fa_msg);
+            const uint32_t k = local(unit_worker[uu[i]]) ? stage_conductances(uu[i], rr[i], vals[i], ns[i])
+                                                         : copy_valid_prefix(nullptr, vals[i], ns[i]);
+            if (k < ns[i]) throw ConfigError("conductance values must be finite and >= 0");
+        }
+        *failed = count;
+        return;
+    }
+    // validate every item (in parallel), find the first invalid one
+    std::vector<uint32_t> kv(fa);
+    const int nt = std::max(1, std::min(8, omp_get_max_threads()));
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4)
+    for (int64_t i = 0; i < (int64_t)fa; ++i) kv[i] = copy_valid_prefix(nullptr, vals[i], ns[i]);
+    uint32_t fv = fa;
+    for (uint32_t i = 0; i < fa; ++i)
+        if (kv[i] < ns[i]) {
+            fv = i;
+            break;
+        }
+    const uint32_t last = std::min(fa, fv + (fv < fa ? 1u : 0u));  // items staged
+    // records first (creating one may grow the staging buffer), then the
+    // destinations
+    for (uint32_t i = 0; i < last; ++i)
+        if (local(unit_worker[uu[i]])) slot_of(uu[i], rr[i]);
+    std::vector<float*> dst(last, nullptr);
+    for (uint32_t i = 0; i < last; ++i)
+        if (local(unit_worker[uu[i]])) {
+            uint4& r = cond_rec[slot_of(uu[i], rr[i])];
+            r.z = std::max(r.z, kv[i]);
+            dst[i] = h_cstage.p + r.x;
+        }
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 4)
+    for (int64_t i = 0; i < (int64_t)last; ++i)
+        if (dst[i]) std::memcpy(dst[i], vals[i], 4ull * kv[i]);
+    if (fv < fa) {
+        *failed = fv;
+        throw ConfigError("conductance values must be finite and >= 0");
+    }
+    if (fa < count) {
+        *failed = fa;
+        throw ConfigError(fa_msg);
+    }
+}
+
+uint32_t Engine::stage_conductances(uint32_t unit, int receptor, const float* values,
+                                    uint32_t n) {
+    uint4& r = cond_rec[slot_of(unit, receptor)];  // a later set overwrites the earlier values
     const uint32_t k = copy_valid_prefix(h_cstage.p + r.x, values, n);
     r.z = std::max(r.z, k);
     return k;
@@ -2270,17 +2353,33 @@ void Engine::flush_conductances(bool sync) {
     CK(cudaMemcpyAsync(d_cstage.p, h_cstage.p, 4ull * total, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_crec.p, rec.data(), 16 * rec.size(), cudaMemcpyHostToDevice, stream));
     const int blocks = (int)std::min<uint32_t>(148 * 8, (total + 255) / 256);
-    cond_scatter_kernel<<<blocks, 256, 0, stream>>>(d_cstage.p, d_crec.p, (uint32_t)rec.size(),
-                                                     total, reinterpret_cast<float*>(d_g.p));
-    CK(cudaGetLastError());
+    if (blocks) {  // (records can hold no values: a set that failed at its first value)
+        cond_scatter_kernel<<<blocks, 256, 0, stream>>>(d_cstage.p, d_crec.p, (uint32_t)rec.size(),
+                                                         total, reinterpret_cast<float*>(d_g.p));
+        CK(cudaGetLastError());
+        launches += 1;
+    }
     // the pinned staging buffer is reused by the next set_conductances; `rec`
     // is pageable, so its copy has been staged by the time the call returns
     if (sync) CK(cudaStreamSynchronize(stream));
     h2d += 4ull * total + 16 * rec.size();
-    launches += 1;
     for (const uint4& r : cond_rec) cond_slot[r.w] = -1;
     cond_rec.clear();
     cond_total = 0;
+}
+
+int vxb_set_conductances_batch(vxb_engine* e, uint32_t count, const uint32_t* units,
+                               const int32_t* receptors, const float* const* values,
+                               const uint32_t* counts, uint32_t* failed_index) {
+    Engine& g = e->eng;
+    uint32_t dummy = 0;
+    try {
+        g.stage_batch(count, units, receptors, values, counts, failed_index ? failed_index : &dummy);
+        return VXB_OK;
+    } catch (const std::exception& x) {
+        g.err = x.what();
+        return fail_code(x);
+    }
 }
 
 int vxb_membrane_snapshot(const vxb_engine* e, uint16_t worker, float* out, uint32_t cap) {

@@ -245,6 +245,21 @@ class RunResult:
 
 
 # ---------------------------------------------------------------- instance
+class ConductanceBatch:
+    """Argument arrays of vxb_set_conductances_batch built once: (unit,
+    receptor, float32 buffer) items whose buffers the caller refills."""
+
+    def __init__(self, items):
+        items = list(items)
+        self.n = len(items)
+        self.units = np.array([u for u, _, _ in items], np.uint32)
+        self.recs = np.array([r for _, r, _ in items], np.int32)
+        self.arrays = [np.ascontiguousarray(v, dtype=np.float32) for _, _, v in items]
+        self.counts = np.array([a.size for a in self.arrays], np.uint32)
+        self.ptrs = (C.c_void_p * max(1, self.n))(*[a.ctypes.data for a in self.arrays])
+        self.units_p, self.recs_p, self.counts_p = ptr(self.units), ptr(self.recs), ptr(self.counts)
+
+
 class SimInstance:
     """voxsim::SimInstance (engine.hpp:68-89) backed by the CUDA engine."""
 
@@ -400,6 +415,21 @@ class SimInstance:
         rc = self._lib.vxb_set_conductances(self._h, unit, receptor, addr, v.size)
         if rc != 0:
             self._err(rc)
+
+    def set_conductances_batch(self, items) -> int:
+        """set_conductances for many (unit, receptor, values) in one call:
+        the result and errors of calling it item by item (staging stops at
+        the first failing item), validated and copied on several host cores
+        (vxb_set_conductances_batch).  `items` is a list or a prebuilt
+        ConductanceBatch (whose buffers may be refilled between calls)."""
+        b = items if isinstance(items, ConductanceBatch) else ConductanceBatch(items)
+        failed = C.c_uint32(0)
+        rc = self._lib.vxb_set_conductances_batch(self._h, b.n, b.units_p, b.recs_p, b.ptrs,
+                                                  b.counts_p, C.byref(failed))
+        if rc != 0:
+            self.failed_index = int(failed.value)
+            self._err(rc)
+        return b.n
 
     def membrane_snapshot(self, worker: int) -> np.ndarray:
         n = int(self._lib.vxb_worker_neurons(self._h, worker)) if worker < self.workers else 0

@@ -502,3 +502,37 @@ def test_crossing_matrix_matches_reference():
         assert np.array_equal(sim.crossing_matrix(), ref)
     with netgen.GeneratedSimInstance(netgen.build_network(cfg), SimOptions(steps=1)) as sim:
         assert np.array_equal(sim.crossing_matrix(), ref)
+
+
+def test_set_conductances_batch_equals_item_by_item():
+    """vxb_set_conductances_batch = set_conductances item by item, in order:
+    the later of two sets of one (unit, receptor) wins, a bad value stops the
+    sequence after staging that item's valid prefix (engine.cpp:829-844)."""
+    net = RefNet(hot_cfg(seed=41, voxels=3, npv=200, k_in=15, rho=0.3), even_workers=2)
+    units = net.tables.units
+    rng = np.random.default_rng(3)
+    items = [(u, r, rng.uniform(0.5, 2.0, int(units["neurons"][u])).astype(np.float32))
+             for u in range(units.shape[0]) for r in (0, 2)]
+    bad = items[5][2].copy()
+    bad[7] = -1.0
+    seq_items = items[:5] + [(items[5][0], items[5][1], bad)] + items[6:]
+    opt = SimOptions(steps=40, probe_gids=[3, 300, 599])
+    with SimInstance(net.tables, opt) as a, SimInstance(net.tables, opt) as b:
+        for u, r, v in items[:3] + [items[1]]:  # duplicate key: sequential path
+            a.set_conductances(u, r, v)
+        a.set_conductances_batch(items[:3] + [items[1]])  # no-op duplicate of the same values
+        b.set_conductances_batch(items[:3] + [items[1]])
+        with pytest.raises(ConfigError):
+            for u, r, v in seq_items:
+                a.set_conductances(u, r, v)
+        with pytest.raises(ConfigError):
+            b.set_conductances_batch(seq_items)
+        assert b.failed_index == 5
+        ra, rb = a.advance(40), b.advance(40)
+        assert ra.total_spikes == rb.total_spikes > 0
+        assert raster_set(ra.raster) == raster_set(rb.raster)
+        assert np.array_equal(ra.rates.counts, rb.rates.counts)
+        for pa, pb in zip(ra.probes, rb.probes):
+            assert np.array_equal(pa.v, pb.v) and np.array_equal(pa.i_syn, pb.i_syn)
+        for w in range(2):
+            assert np.array_equal(a.membrane_snapshot(w), b.membrane_snapshot(w))

@@ -114,12 +114,16 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-// Decoded 8-byte tile entry: bits 0-14 tile-local target, bit 15 class
-// (0 AMPA/NMDA, 1 GABAA/GABAB), bits 16-39 wq_slow, bits 40-63 wq_fast.
-__device__ __forceinline__ void tile_add(uint32_t* Bw, uint32_t per, uint64_t e) {
-    uint32_t* q = Bw + ((uint32_t)(e >> 15) & 1u) * 2u * per + ((uint32_t)e & 0x7fffu);
-    atomicAdd(q, (uint32_t)(e >> 40));
-    atomicAdd(q + per, (uint32_t)(e >> 16) & 0xffffffu);
+// 8-byte tile entry: bits 0-15 the word offset of its fast-receptor sum in
+// the pending tile (AMPA: l, GABAA: 2 per + l for tile-local target l; the
+// slow receptor's sum is `per` words further), bits 16-39 wq_slow, bits
+// 40-63 wq_fast.  `bw` is the shared-memory address of the tile's parity
+// buffer, per4 = 4 per: two shared reductions and four integer operations.
+__device__ __forceinline__ void tile_add(uint32_t bw, uint32_t per4, uint64_t e) {
+    const uint32_t q = bw + ((uint32_t)e & 0xffffu) * 4u;
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(q), "r"((uint32_t)(e >> 40)) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(q + per4),
+                 "r"((uint32_t)(e >> 16) & 0xffffffu) : "memory");
 }
 
 // MG: one process per GPU (peers' batches, P2P routing); false: one GPU
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         auto consume = [&]() {
             if (!doE) return;
             const uint32_t par = tE & 1u;
-            uint32_t* Bw = s_pend + par * 4 * per;
+            const uint32_t bw = smem_u32(s_pend + par * 4 * per), per4 = 4 * per;
             const uint32_t cnt0 = __ldcg(a.q_cnt + par * G + blockIdx.x);
             const uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
             for (;;) {
@@ -267,18 +271,24 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     if (ln < fe) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ln));
                 }
                 const uint64_t d = __ldcg(reinterpret_cast<const unsigned long long*>(items + it));
-                const uint64_t* ev = a.tent + (d & kItemBeg);
+                const uint64_t* ev = a.tent + (d & kItemBeg) + lane;
                 const uint32_t len = (uint32_t)(d >> 40);
-                for (uint32_t k0 = 0; k0 < len; k0 += 32 * kTileUnroll) {
+                uint32_t k0 = 0;
+                for (; k0 + 32 * kTileUnroll <= len; k0 += 32 * kTileUnroll) {  // full rounds
                     uint64_t e[kTileUnroll];
 #pragma unroll
-                    for (uint32_t u = 0; u < kTileUnroll; ++u) {
-                        const uint32_t k = k0 + u * 32 + lane;
-                        if (k < len) e[u] = ld_stream(ev + k, pol_syn);
-                    }
+                    for (uint32_t u = 0; u < kTileUnroll; ++u) e[u] = ld_stream(ev + k0 + u * 32, pol_syn);
+#pragma unroll
+                    for (uint32_t u = 0; u < kTileUnroll; ++u) tile_add(bw, per4, e[u]);
+                }
+                if (k0 < len) {  // the tail
+                    uint64_t e[kTileUnroll];
 #pragma unroll
                     for (uint32_t u = 0; u < kTileUnroll; ++u)
-                        if (k0 + u * 32 + lane < len) tile_add(Bw, per, e[u]);
+                        if (k0 + u * 32 + lane < len) e[u] = ld_stream(ev + k0 + u * 32, pol_syn);
+#pragma unroll
+                    for (uint32_t u = 0; u < kTileUnroll; ++u)
+                        if (k0 + u * 32 + lane < len) tile_add(bw, per4, e[u]);
                 }
             }
         };
@@ -658,9 +668,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     }
 }
 
-// 8-byte tile entries from the target-sorted out-CSR: tile-local target
-// (< 2^15), class, and both Q16 weights (< 2^24 each: checked, else the
-// engine keeps the l2_atomic path).  flag[0] is set when an entry does not fit.
+// 8-byte tile entries from the target-sorted out-CSR: the word offset of the
+// fast receptor's sum in the pending tile (< 2^16) and both Q16 weights
+// (< 2^24 each: checked, else the engine keeps the l2_atomic path).  flag[0]
+// is set when an entry does not fit.
 __global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ w,
                                     uint64_t n_syn, uint32_t per, uint64_t* __restrict__ tent,
                                     unsigned int* __restrict__ flag) {
@@ -669,10 +680,10 @@ __global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint
         const uint32_t t = tgt[k], tid = t & 0x7fffffffu;
         const uint64_t wq = w[k];
         const uint32_t wf = (uint32_t)wq, ws = (uint32_t)(wq >> 32);
-        const uint32_t l = tid % per;
-        if (wf >= (1u << 24) || ws >= (1u << 24) || l >= (1u << 15)) atomicExch(flag, 1u);
+        const uint32_t off = (t >> 31) * 2u * per + tid % per;  // fast receptor's word
+        if (wf >= (1u << 24) || ws >= (1u << 24) || off + per >= (1u << 16)) atomicExch(flag, 1u);
         tent[k] = ((uint64_t)(wf & 0xffffffu) << 40) | ((uint64_t)(ws & 0xffffffu) << 16) |
-                  ((uint64_t)(t >> 31) << 15) | (l & 0x7fffu);
+                  (off & 0xffffu);
     }
 }
 

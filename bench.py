@@ -400,7 +400,7 @@ def run_b200(args):
             dist.barrier()
 
     dev_ms, wall, events, spikes, h2d, d2h, launches, results = [], [], 0, 0, 0, 0, 0, []
-    xwait, stage_s = 0.0, 0.0
+    xwait, xarr, stage_s = 0.0, 0.0, 0.0
     with ClockSampler(dev) as clk:
         barrier()
         t_all = time.perf_counter()
@@ -417,6 +417,7 @@ def run_b200(args):
             d2h += r.d2h_bytes
             launches += r.launches
             xwait += r.exchange_wait_ms
+            xarr += r.exchange_arrival_ms
         barrier()
         t_all = time.perf_counter() - t_all
     schedule = sim.schedule_info()
@@ -426,9 +427,9 @@ def run_b200(args):
     # max over ranks of time, sum of work
     if dist:
         import torch
-        t = torch.tensor([dev_s, wall_s, xwait, stage_s], dtype=torch.float64)
+        t = torch.tensor([dev_s, wall_s, xwait, xarr, stage_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s, wall_s, xwait, stage_s = (float(x) for x in t)
+        dev_s, wall_s, xwait, xarr, stage_s = (float(x) for x in t)
         e = torch.tensor([events, spikes, launches], dtype=torch.float64)
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
         events, spikes, launches = (int(x) for x in e)
@@ -473,7 +474,11 @@ def run_b200(args):
                          "synapse table per GPU)",
                    "schedule": schedule},
         "wall_s_per_bio_s": dev_s / bio_s,
+        # exchange (max over ranks, per simulated step): the time CTAs spun
+        # on a peer's flag once their local work was done, and how long after
+        # the phase start the last peer's batch arrived
         "exposed_exchange_us_per_step": 1e3 * xwait / (args.steps * bio_steps) if ws > 1 else 0.0,
+        "exchange_arrival_lag_us_per_step": 1e3 * xarr / (args.steps * bio_steps) if ws > 1 else 0.0,
         "mean_rate_hz": rate,
         "events_per_s_per_gpu": value / ws,
         "e2e": {"value": events / wall_s, "unit": "events/s",

@@ -225,6 +225,13 @@ double vxb_result_device_ms(const vxb_engine* e);
 /* Exposed spike-exchange wait of the last advance: sum over steps of the
  * longest time any CTA waited for a peer's batch, milliseconds. */
 double vxb_result_exchange_wait_ms(const vxb_engine* e);
+/* Arrival lag of the last advance: sum over steps of how long after the
+ * start of the phase that delivers S(t) the last peer's batch of S(t) was
+ * first observed, milliseconds.  Unlike vxb_result_exchange_wait_ms (time
+ * CTAs spent spinning once their local work was done) it does not depend on
+ * how much local work the CTAs had; the exchange is exposed only where the
+ * lag exceeds the phase's local work. */
+double vxb_result_exchange_arrival_ms(const vxb_engine* e);
 /* Bytes copied host->device / device->host by the last vxb_advance. */
 uint64_t vxb_result_h2d_bytes(const vxb_engine* e);
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e);

@@ -253,6 +253,9 @@ struct Engine {
     bool has_forced = false, has_inj = false;  // tables of the current advance
     DevBuf<unsigned long long> d_phase_ns;
     DevBuf<unsigned long long> d_phase_wait;
+    DevBuf<unsigned long long> d_arrive;    // [phase][peer] first flag observation (globaltimer)
+    double exchange_arrival_ms = 0;         // last advance: sum over phases of the last
+                                            // peer's arrival after the phase start
     double exchange_wait_ms = 0;  // last advance: sum over phases of the max CTA wait
     DevBuf<Control> d_ctl;
     DevBuf<uint64_t> d_keys, d_keys_sorted;
@@ -1645,6 +1648,8 @@ void Engine::advance(uint32_t steps) {
     d_rates.reserve((size_t)n_units * chunk);
     d_phase_ns.reserve(chunk + 2);
     d_phase_wait.reserve(chunk + 2);
+    d_arrive.reserve((size_t)(chunk + 2) * world);
+    exchange_arrival_ms = 0;
     exchange_wait_ms = 0;
     phase_wait_all.assign(steps + 2, 0);
 
@@ -1864,6 +1869,10 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.dst_mask = d_mask.p;
     a.phase_wait = d_phase_wait.p;
     d_phase_wait.zero(stream);
+    if (world > 1) {
+        a.arrive = d_arrive.p;
+        CK(cudaMemsetAsync(d_arrive.p, 0xff, 8ull * (steps + 2) * world, stream));
+    }
     a.n_blocks = n_blocks;
     a.blk_off = d_blk.p;
     d_work.reserve(2ull * n_blocks * world);
@@ -1926,6 +1935,20 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
         CK(cudaStreamSynchronize(stream));
         for (auto x : pw) exchange_wait_ms += x * 1e-6;
         for (uint32_t p = 1; p <= steps; ++p) phase_wait_all[rel0 + p] = pw[p];
+        // arrival lag: when the last peer's batch of S(tE) was first seen,
+        // after the start of the phase that delivers it (independent of how
+        // much local work the CTAs had before they waited)
+        std::vector<unsigned long long> ar((size_t)(steps + 2) * world), pn(steps + 2);
+        CK(cudaMemcpyAsync(ar.data(), d_arrive.p, 8 * ar.size(), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(pn.data(), d_phase_ns.p, 8 * pn.size(), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        for (uint32_t p = 1; p <= steps; ++p) {
+            unsigned long long last = 0;
+            for (uint32_t h = 0; h < world; ++h)
+                if (h != rank && ar[(size_t)p * world + h] != ~0ull)
+                    last = std::max(last, ar[(size_t)p * world + h]);
+            if (last > pn[p]) exchange_arrival_ms += (last - pn[p]) * 1e-6;
+        }
     }
     CK(cudaStreamSynchronize(stream));
     if (prof && tile_path) {  // per phase: mean / max over CTAs of each part's end (us)
@@ -2214,6 +2237,7 @@ int vxb_schedule_info(const vxb_engine* e, char* out, uint64_t cap) {
 
 double vxb_result_device_ms(const vxb_engine* e) { return e->eng.device_ms; }
 double vxb_result_exchange_wait_ms(const vxb_engine* e) { return e->eng.exchange_wait_ms; }
+double vxb_result_exchange_arrival_ms(const vxb_engine* e) { return e->eng.exchange_arrival_ms; }
 uint64_t vxb_result_h2d_bytes(const vxb_engine* e) { return e->eng.h2d; }
 uint64_t vxb_result_d2h_bytes(const vxb_engine* e) { return e->eng.d2h; }
 uint64_t vxb_result_launches(const vxb_engine* e) { return e->eng.launches; }

@@ -171,6 +171,7 @@ struct StepArgs {
     Exchange* ex;
     uint32_t world;
     unsigned long long* phase_wait;  // per phase: max over CTAs of the exchange wait (ns)
+    unsigned long long* arrive;      // [phase][peer]: first globaltimer a CTA saw the peer's flag
     // L2-blocked delivery: targets split into n_blocks ranges delivered in
     // order; blk_off[s * (n_blocks + 1) + b] = row offset of block b
     uint32_t n_blocks;
@@ -702,7 +703,7 @@ __device__ __forceinline__ void exchange_publish(const StepArgs& a, uint32_t t) 
 // Wait for peer h's batch of step tE (receiver side of the step barrier);
 // returns its id count.  recv_timeout_ms maps to a device-side timeout.
 __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h, uint32_t tE,
-                                                 uint32_t slot) {
+                                                 uint32_t slot, uint32_t ph) {
     Exchange* ex = a.ex;
     const uint32_t* meta = ex->rx_meta[h];
     const unsigned long long t0 = globaltimer();
@@ -720,6 +721,7 @@ __device__ __forceinline__ uint32_t exchange_wait(const StepArgs& a, uint32_t h,
         }
         __nanosleep(64);
     }
+    if (a.arrive) atomicMin(a.arrive + (size_t)ph * ex->world + h, (unsigned long long)globaltimer());
     return ld_acquire_sys(meta + slot);
 }
 
@@ -896,7 +898,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                             if (li) {
                                 if (blk == 0 && lane == 0) {
                                     const unsigned long long w0 = globaltimer();
-                                    s_hcnt[li] = exchange_wait(a, h, tE, tslot);
+                                    s_hcnt[li] = exchange_wait(a, h, tE, tslot, ph);
                                     wait_ns += globaltimer() - w0;
                                 }
                                 __syncwarp();
@@ -955,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                             uint32_t c = 0;
                             if (lane == 0) {
                                 const unsigned long long w0 = globaltimer();
-                                c = exchange_wait(a, h, tE, tslot);
+                                c = exchange_wait(a, h, tE, tslot, ph);
                                 wait_ns += globaltimer() - w0;
                             }
                             cnt = __shfl_sync(0xffffffffu, c, 0);

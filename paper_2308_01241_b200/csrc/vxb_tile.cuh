@@ -51,7 +51,10 @@ namespace vxb {
 #define VXB_TILE_THREADS 1024
 #endif
 constexpr int kTileThreads = VXB_TILE_THREADS;      // 24 warps: update, then consume / advance I_ou
-constexpr uint32_t kTileUnroll = 4;     // synapse entries in flight per consumer lane
+#ifndef VXB_TILE_UNROLL
+#define VXB_TILE_UNROLL 4
+#endif
+constexpr uint32_t kTileUnroll = VXB_TILE_UNROLL;  // synapse entries in flight per consumer lane
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
 constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
 constexpr uint32_t kTileBucketWarps = 2;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 uint32_t cnt = 0;
                 if (lane == 0) {
                     const unsigned long long w0 = globaltimer();
-                    cnt = exchange_wait(a, h, tE, slot);
+                    cnt = exchange_wait(a, h, tE, slot, ph);
                     waited += globaltimer() - w0;
                 }
                 cnt = __shfl_sync(0xffffffffu, cnt, 0);

@@ -237,6 +237,7 @@ class RunResult:
     # and the voxel spike counts it was driven by, [steps][voxels]
     bold: np.ndarray | None = None
     voxel_counts: np.ndarray | None = None
+    exchange_arrival_ms: float = 0.0
 
     @property
     def events(self) -> int:
@@ -369,7 +370,8 @@ class SimInstance:
                          int(L.vxb_result_total_spikes(h)), steps,
                          float(L.vxb_result_device_ms(h)), int(L.vxb_result_h2d_bytes(h)),
                          int(L.vxb_result_d2h_bytes(h)), int(L.vxb_result_launches(h)),
-                         float(L.vxb_result_exchange_wait_ms(h)), bold, vcounts)
+                         float(L.vxb_result_exchange_wait_ms(h)), bold, vcounts,
+                         float(L.vxb_result_exchange_arrival_ms(h)))
 
     def _bold(self, steps: int) -> np.ndarray:
         n = int(self._lib.vxb_result_bold_size(self._h))

@@ -1035,6 +1035,55 @@ def build_network(cfg, workers: Optional[int] = None, method: Optional[str] = No
     return BuiltNetwork(cfg, g, layout, intra, ug, list(uw), W, syn, arrays)
 
 
+B200_HBM_BYTES = 183e9   # one B200 (nvidia-smi: 183359 MiB... 179 GiB usable)
+SORT_SLICE = 1 << 28      # entries per row-sort slice (Engine::sort_rows)
+
+
+def memory_plan(net: "BuiltNetwork", record_raster: bool = False) -> list:
+    """Per-rank device memory of the engine for `net` with one worker per
+    rank (the allocations of csrc/vxb_engine.cu, l2_atomic path unless the
+    shard fits the SM-tile path): resident bytes by buffer, the load-time
+    scratch peak (generation counts, row-sort slices) and the total, against
+    the 180 GB of a B200 (config 5 dry run)."""
+    W = net.workers
+    units = net.layout.units
+    n_w = [0] * W
+    syn_w = [0] * W
+    for u, x in enumerate(units):
+        n_w[net.unit_worker[u]] += x.neurons
+        syn_w[net.unit_worker[u]] += x.neurons * net.layout.voxels[x.voxel].k_in
+    N = sum(n_w)  # global sources: every rank indexes its out-CSR by global source
+    out = []
+    for r in range(W):
+        n, S = n_w[r], syn_w[r]
+        tile = W == 1 and n <= 148 * 6784 or W > 1 and n <= 148 * 6784
+        res = {"neuron_state": 44 * n + (4 * n if tile else 0),  # V, j, I_ou(x2 tile), I_syn, g
+               "pending": 32 * n, "dst_mask": 8 * n,
+               "out_csr_offsets": 8 * (N + 1) + 4 * N,              # off + inner per global source
+               "synapse_table": (8 if tile else 12) * S + 24,
+               "spike_log": 4 * (min(n * 100, 1 << 29) if record_raster else 2 * n),
+               "exchange_slots": 16 * (N - n) + 32 * W if W > 1 else 0}
+        blocks = 1
+        if not tile:
+            n_ref = max(n_w)
+            mb = 80 if (n_ref * 16 + (64 << 20) - 1) // (64 << 20) >= 6 else 64
+            bn = (mb << 20) // 16
+            blocks = 1 if n_ref <= bn else -(-n_ref // bn)
+            if blocks > 1:
+                res["l2_block_offsets"] = 4 * N * (blocks + 1)
+        else:
+            res["tile_segments"] = 16 * (S // 150 + N) + 2 * 8 * (S // 150)  # ~1 per 150 entries
+        resident = sum(res.values())
+        slice_ = min(S, SORT_SLICE)
+        scratch = max(16 * (N + 1),                      # generation: counts + have-mask
+                      12 * slice_ * 2 + 8 * (N + 1) if (blocks > 1 or tile) else 0)
+        out.append({"rank": r, "neurons": n, "synapses": S, "path": "sm_tile" if tile else "l2_atomic",
+                    "l2_blocks": blocks, "resident_bytes": resident, "load_scratch_bytes": scratch,
+                    "peak_bytes": resident + scratch, "budget_bytes": B200_HBM_BYTES,
+                    "fits": resident + scratch <= B200_HBM_BYTES, "buffers": res})
+    return out
+
+
 def hbm_bytes_per_worker(net: "BuiltNetwork") -> list:
     """Device bytes per worker under the B200 byte model."""
     s1, s2, s3 = BYTE_MODELS["b200"]

@@ -119,3 +119,21 @@ def test_sample_conductances_matches_reference_tables():
             assert np.allclose(got, want, rtol=2e-7, atol=0)
             flips += int((got != want).sum())
     assert flips <= 2  # numpy log/cos/exp vs glibc: rare last-ulp float flips
+
+
+def test_config5_memory_plan_fits_eight_b200():
+    """the whole-box network — 2e8 neurons x K = 500 =
+    1e11 synapses over 8 ranks — fits each rank's 180 GB with the tables,
+    offsets, L2-block offsets, exchange slots and the load-time row-sort
+    scratch (netgen.memory_plan mirrors the engine's allocations)."""
+    import bench
+    net = netgen.build_network(bench.config5_cfg(workers=8))
+    assert net.total_neurons == 200_000_000 and net.synapse_count == 100_000_000_000
+    plan = netgen.memory_plan(net)
+    assert len(plan) == 8
+    for r in plan:
+        assert r["fits"], r
+        assert r["path"] == "l2_atomic" and r["l2_blocks"] >= 5
+        assert 145e9 < r["buffers"]["synapse_table"] < 155e9
+    # one rank per GPU at 25M neurons is near the limit: 16 ranks would halve it
+    assert max(r["peak_bytes"] for r in plan) > 0.85 * plan[0]["budget_bytes"]

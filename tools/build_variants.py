@@ -9,6 +9,9 @@ VARIANTS = {
     # tile path (vxb_tile.cuh)
     "tt768": {"VXB_TILE_THREADS": 768},    # 24 warps at 80 registers
     "tt640": {"VXB_TILE_THREADS": 640},    # 20 warps at 96 registers
+    "tt768u8": {"VXB_TILE_THREADS": 768, "VXB_TILE_UNROLL": 8},
+    "u8": {"VXB_TILE_UNROLL": 8},
+    "u2": {"VXB_TILE_UNROLL": 2},
     # l2_atomic path (vxb_kernels.cuh)
     "m2": {"VXB_MINB": 2},           # register cap lifted (2 CTAs/SM)
     "d3": {"VXB_DEPTH3": 1},         # update state two chunks ahead in registers

@@ -360,6 +360,9 @@ def run_b200(args):
         sim = netgen.DistributedSimInstance(net, opt, rank, ws)
     else:
         sim = netgen.GeneratedSimInstance(net, opt)
+    import torch
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    mem_used = float(total_b - free_b)
     # e2e input per step, as the assimilation caller feeds the boundary
     # (assim.cpp:91-107, EnsembleMember::run_window): fresh AMPA conductance
     # scales for every local unit from pinned host buffers, staged by
@@ -427,9 +430,9 @@ def run_b200(args):
     # max over ranks of time, sum of work
     if dist:
         import torch
-        t = torch.tensor([dev_s, wall_s, xwait, xarr, stage_s], dtype=torch.float64)
+        t = torch.tensor([dev_s, wall_s, xwait, xarr, stage_s, mem_used], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s, wall_s, xwait, xarr, stage_s = (float(x) for x in t)
+        dev_s, wall_s, xwait, xarr, stage_s, mem_used = (float(x) for x in t)
         e = torch.tensor([events, spikes, launches], dtype=torch.float64)
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
         events, spikes, launches = (int(x) for x in e)
@@ -480,6 +483,7 @@ def run_b200(args):
         "exposed_exchange_us_per_step": 1e3 * xwait / (args.steps * bio_steps) if ws > 1 else 0.0,
         "exchange_arrival_lag_us_per_step": 1e3 * xarr / (args.steps * bio_steps) if ws > 1 else 0.0,
         "mean_rate_hz": rate,
+        "device_memory_used_gb": mem_used / 1e9,  # max over ranks, after load
         "events_per_s_per_gpu": value / ws,
         "e2e": {"value": events / wall_s, "unit": "events/s",
                 "h2d_bytes_per_step": h2d // max(1, args.steps * ws),

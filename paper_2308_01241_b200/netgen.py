@@ -502,7 +502,7 @@ def parse_config(cfg) -> dict:
         raise ConfigError("unknown partition method: " + str(part["method"]))
     if part["method"] == "file" and not part["path"]:
         raise ConfigError("partition method 'file' needs a path")
-    if part["byte_model"] not in BYTE_MODELS:
+    if part["byte_model"] not in BYTE_MODELS_ALL:
         raise ConfigError("unknown byte_model: " + str(part["byte_model"]))
     regions = {}
     for name, rc in cfg.get("regions", {}).items():
@@ -620,6 +620,14 @@ STATE_BYTES, ENTRY_BYTES, BUFFER_BYTES = 48, 16, 12  # partition.cpp:16-18
 #                gamma = the per-GPU HBM budget, greedy/sequential place units
 #                under the 180 GB of a B200.
 BYTE_MODELS = {"reference": (48, 16, 12), "b200": (92, 12, 12)}
+#  "b200_time" — a time model instead of bytes: femtoseconds of one step on a
+#                B200 per neuron (update + noise, 38 ps: config 3 silent,
+#                760 us for 20M neurons) and per synapse (3.6 ps per delivered
+#                event x rate_hz x dt: config 3 at 10 Hz, 360 us for 1e8
+#                events), so greedy balances the ranks' step time; the HBM
+#                fit is still checked with the "b200" bytes.
+TIME_MODEL_FS = (38_000, 3_600)  # per neuron-step, per delivered event
+BYTE_MODELS_ALL = set(BYTE_MODELS) | {"b200_time"}
 B200_HBM_BUDGET = 170e9  # bytes per GPU left for tables + state (of 183 GB)
 
 
@@ -692,7 +700,10 @@ def build_unit_graph(layout: Layout, g: Connectome, intra, rate_hz: float,
                 picks = n_t * ppn * q
                 bytes_ = rate_hz * dt_s * distinct(n_s, picks) * 4.0
                 traffic[b0 + sp][b0 + tp] += llround(bytes_ * 1e6)
-    s1, s2, s3 = BYTE_MODELS[byte_model]
+    if byte_model == "b200_time":
+        s1, s2, s3 = TIME_MODEL_FS[0], max(1, round(TIME_MODEL_FS[1] * rate_hz * dt_s)), 0
+    else:
+        s1, s2, s3 = BYTE_MODELS[byte_model]
     return UnitGraph(n, n * s1, n * kin * s2, n * s3, np.array(traffic, np.int64).reshape(U, U))
 
 
@@ -984,14 +995,14 @@ def build_network(cfg, workers: Optional[int] = None, method: Optional[str] = No
         else:
             fn = {"greedy": partition_greedy, "sequential": partition_sequential,
                   "exact": partition_exact}[p["method"]]
-            if p["byte_model"] == "b200" and p["gamma"] <= 0:
+            if p["byte_model"] in ("b200", "b200_time") and p["gamma"] <= 0:
                 # per-GPU budget: the HBM budget, tightened to a near-even share
                 # so the traffic objective cannot pile units onto one GPU
                 total = sum(_load(ug, p, u) for u in range(len(layout.units)))
+                cap = B200_HBM_BUDGET if p["byte_model"] == "b200" else float("inf")
                 for slack in (1.1, 1.25, 1.5, 2.0, None):
                     q = dict(p)
-                    q["gamma"] = B200_HBM_BUDGET if slack is None else \
-                        min(B200_HBM_BUDGET, slack * total / W)
+                    q["gamma"] = cap if slack is None else min(cap, slack * total / W)
                     try:
                         uw = fn(ug, W, q)
                         break
@@ -1020,12 +1031,12 @@ def build_network(cfg, workers: Optional[int] = None, method: Optional[str] = No
         edges[i] = e
     intra_arr = {r: np.ascontiguousarray(np.array(m, np.float64)) for r, m in intra.items()}
     syn = sum(u.neurons * layout.voxels[u.voxel].k_in for u in layout.units)
-    if p["byte_model"] == "b200":  # every GPU must fit its share of the network
+    if p["byte_model"] in ("b200", "b200_time"):  # every GPU must fit its share of the network
         s1, s2, s3 = BYTE_MODELS["b200"]
         load = [0.0] * W
         for u, x in enumerate(layout.units):
             load[uw[u]] += x.neurons * (s1 + s3 + layout.voxels[x.voxel].k_in * s2)
-        budget = p["gamma"] if p["gamma"] > 0 else B200_HBM_BUDGET
+        budget = p["gamma"] if p["gamma"] > 0 and p["byte_model"] == "b200" else B200_HBM_BUDGET
         for w in range(W):
             if load[w] > budget:
                 raise ConfigError(f"worker {w} needs {load[w] / 1e9:.1f} GB of HBM "

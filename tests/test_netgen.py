@@ -137,3 +137,32 @@ def test_config5_memory_plan_fits_eight_b200():
         assert 145e9 < r["buffers"]["synapse_table"] < 155e9
     # one rank per GPU at 25M neurons is near the limit: 16 ranks would halve it
     assert max(r["peak_bytes"] for r in plan) > 0.85 * plan[0]["budget_bytes"]
+
+
+def test_time_model_partition_balances_step_time(tmp_path):
+    """byte_model "b200_time" (per-neuron + per-event step time) balances
+    the ranks' estimated step time where in-degrees differ across regions;
+    the byte model balances bytes instead (multi-GPU at scale)."""
+    g = netgen.make_ring(12, 2000)
+    g.region = ["subcortex" if v % 3 else "brainstem" for v in range(12)]
+    g.neuron_count = [2000 if v % 3 else 6000 for v in range(12)]
+    path = tmp_path / "mixed.txt"
+    netgen.write_connectome_file(g, path)
+
+    def est_time(net, W):
+        t = [0.0] * W
+        n_fs, e_fs = netgen.TIME_MODEL_FS
+        for u, x in enumerate(net.layout.units):
+            k = net.layout.voxels[x.voxel].k_in
+            t[net.unit_worker[u]] += x.neurons * (n_fs + e_fs * k * 10.0 * 1e-3)
+        return t
+
+    out = {}
+    for bm in ("b200", "b200_time"):
+        cfg = {"seed": 3, "workers": 3, "connectome": {"kind": "file", "path": str(path)},
+               "partition": {"method": "greedy", "byte_model": bm, "rate_hz": 10.0},
+               "regions": {"subcortex": {"k_in": 400}, "brainstem": {"k_in": 20}}}
+        net = netgen.build_network(cfg)
+        t = est_time(net, 3)
+        out[bm] = max(t) / (sum(t) / 3)
+    assert out["b200_time"] <= out["b200"] + 1e-9

@@ -439,6 +439,15 @@ int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double
 int vxb_create_member(const vxb_engine* donor, const vxb_network* net,
                       const vxb_netspec* spec, const vxb_options* opt, vxb_engine** out);
 
+/* Advance `count` ensemble members of one donor by `steps` together: each
+ * member's step kernel is launched on its own stream with an equal share of
+ * the SMs, so the members run concurrently over the shared tables (the
+ * reference advances EnsembleMembers one after another, assim.cpp:231-233).
+ * Results per member as after vxb_advance; the first error is returned and
+ * the failing member's error text is in vxb_last_error(member).  Members on
+ * the SM-tile path advance one after another. */
+int vxb_advance_members(vxb_engine** members, uint32_t count, uint32_t steps);
+
 /* ---- one-call convenience (run_simulation, engine.hpp:92-93) ------------- */
 /* Creates, advances `steps` and returns the engine holding the results. */
 int vxb_run_simulation(const vxb_network* net, const vxb_options* opt,

@@ -161,6 +161,7 @@ EXPORTS = [
     "vxb_result_voxel_counts", "vxb_hemo_feed_counts", "vxb_create_member",
     "vxb_schedule_info", "vxb_build_hash", "vxb_result_wire_bytes", "vxb_set_recv_wire_bytes",
     "vxb_crossing_matrix", "vxb_set_conductances_batch", "vxb_result_exchange_arrival_ms",
+    "vxb_advance_members",
 ]
 
 _lib = None
@@ -188,6 +189,7 @@ def _declare(lib):
         "vxb_result_h2d_bytes": (C.c_uint64, [P]),
         "vxb_result_exchange_wait_ms": (C.c_double, [P]),
         "vxb_result_exchange_arrival_ms": (C.c_double, [P]),
+        "vxb_advance_members": (C.c_int, [P, C.c_uint32, C.c_uint32]),
         "vxb_fnv1a": (C.c_uint64, [P, C.c_uint64, C.c_uint64]),
         "vxb_result_d2h_bytes": (C.c_uint64, [P]),
         "vxb_result_launches": (C.c_uint64, [P]),

@@ -350,7 +350,13 @@ struct Engine {
     void share_tables(const Engine& d);
     std::vector<unsigned long long> gen_have_mask;  // dst masks of generated tables
     void advance(uint32_t steps);
-    void run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps);
+    uint32_t advance_begin(uint32_t steps);
+    void launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps, int grid_ctas);
+    void finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps);
+    void chunk_post(uint32_t rel0, uint32_t cs, std::vector<unsigned long long>& phase_ns_all);
+    void advance_end(uint32_t steps, const std::vector<unsigned long long>& phase_ns_all);
+    bool prof = false;
+    DevBuf<unsigned long long> d_prof;
     uint32_t seg_of(uint32_t local) const {
         return (uint32_t)(std::upper_bound(seg_start.begin(), seg_start.end(), local) -
                           seg_start.begin()) -
@@ -1298,6 +1304,8 @@ void Engine::sort_rows() {
     rows_sorted = true;
 }
 
+constexpr uint32_t kTileMinNeurons = 400000;
+
 // SM-tile path: every CTA (one per SM) owns a contiguous tile of neurons and
 // keeps their pending sums in shared memory (vxb_tile.cuh).  Eligible when
 // both parities of the pending tile fit in a CTA's shared memory (shards up
@@ -1310,6 +1318,11 @@ void Engine::setup_tiles() {
     const char* force = knob("VXB_PATH", &knobs);
     if (force && std::string(force) == "l2") return;
     if (!packed || n == 0) return;
+    // small shards stay on the l2_atomic path: the tile kernel's per-phase
+    // fixed costs (bucketing round trips, per-tile queues) dominate there
+    // (config-2 shape, 100k neurons: l2 17 vs tile 24 us/step; 1M neurons:
+    // tile 53.5 vs l2 72)
+    if (!(force && std::string(force) == "tile") && n < kTileMinNeurons) return;
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -1318,10 +1331,11 @@ void Engine::setup_tiles() {
     if (L.total > (uint32_t)optin) return;
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
         tile_cons = (uint32_t)std::min(23, std::max(1, std::atoi(c)));
-    const void* tk = world > 1 ? (const void*)tile_kernel<true> : (const void*)tile_kernel<false>;
-    CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+    for (const void* tk : {(const void*)tile_kernel<false, false>, (const void*)tile_kernel<false, true>,
+                           (const void*)tile_kernel<true, false>, (const void*)tile_kernel<true, true>})
+        CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, world > 1 ? tile_kernel<true> : tile_kernel<false>,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, world > 1 ? tile_kernel<true, true> : tile_kernel<false, true>,
                                                      kTileThreads, L.total));
     if (per_sm < 1) return;
     const uint32_t tiles = (uint32_t)((n + per - 1) / per);
@@ -1550,7 +1564,25 @@ struct Chunk {
     uint32_t t0, rel0, steps;
 };
 
+// advance() = advance_begin (results reset, per-advance tables, buffers),
+// then per chunk launch_chunk + finish_chunk + chunk_post, then advance_end
+// (readback of the advance's results).  vxb_advance_members interleaves the
+// same pieces of several ensemble members.
 void Engine::advance(uint32_t steps) {
+    const uint32_t chunk = advance_begin(steps);
+    if (steps == 0) return;
+    std::vector<unsigned long long> phase_ns_all;
+    phase_ns_all.reserve(steps + 2);
+    for (uint32_t rel0 = 0; rel0 < steps; rel0 += chunk) {
+        const uint32_t cs = std::min(chunk, steps - rel0);
+        launch_chunk(step_done + rel0, rel0, cs, steps, 0);
+        finish_chunk(rel0, cs, steps);
+        chunk_post(rel0, cs, phase_ns_all);
+    }
+    advance_end(steps, phase_ns_all);
+}
+
+uint32_t Engine::advance_begin(uint32_t steps) {
     if (failed) throw SimError("instance is in a failed state");
     res_steps = steps;
     res_start = step_done;
@@ -1563,7 +1595,7 @@ void Engine::advance(uint32_t steps) {
     timings.clear();
     device_ms = 0;
     h2d = d2h = launches = 0;
-    if (steps == 0) return;
+    if (steps == 0) return 0;
     CK(cudaSetDevice(device));
 
     // per-advance tables: forced spikes and injection epochs by relative step
@@ -1662,12 +1694,11 @@ void Engine::advance(uint32_t steps) {
         const unsigned long long none = ~0ull;
         CK(cudaMemcpyAsync(d_hemo_err.p, &none, 8, cudaMemcpyHostToDevice, stream));
     }
+    return chunk;
+}
 
-    std::vector<unsigned long long> phase_ns_all;
-    phase_ns_all.reserve(steps + 2);
-    for (uint32_t rel0 = 0; rel0 < steps; rel0 += chunk) {
-        const uint32_t cs = std::min(chunk, steps - rel0);
-        run_chunk(step_done + rel0, rel0, cs, steps);
+void Engine::chunk_post(uint32_t rel0, uint32_t cs, std::vector<unsigned long long>& phase_ns_all) {
+    {
         if (hemo_on) {  // window_bold (assim.cpp:51-71) over this chunk's rate rows
             const uint32_t work = cs * n_voxels;
             voxel_counts_kernel<<<std::min<uint32_t>(1184, (work + 255) / 256), 256, 0, stream>>>(
@@ -1687,7 +1718,9 @@ void Engine::advance(uint32_t steps) {
         // the next chunk re-runs no phase: its A-only prologue follows this
         // chunk's E-only epilogue; stitch their times together.
     }
+}
 
+void Engine::advance_end(uint32_t steps, const std::vector<unsigned long long>& phase_ns_all) {
     // probes
     if (!probes.empty()) {
         CK(cudaMemcpyAsync(probe_v.data(), d_probe_v.p, 4 * probe_v.size(),
@@ -1810,7 +1843,10 @@ void Engine::account_wire_bytes(uint32_t steps) {
     }
 }
 
-void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
+// Launch one chunk of `steps` steps (grid_ctas > 0: a smaller grid, for
+// members sharing the device).
+void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_steps,
+                          int grid_ctas) {
     Control c0;
     std::memset(&c0, 0, sizeof c0);
     c0.err = ~0ull;
@@ -1883,8 +1919,7 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     a.ch_max = ch_max;
     a.f_policy = f_policy;
     a.early_publish = early_publish ? 1u : 0u;
-    const bool prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
-    DevBuf<unsigned long long> d_prof;
+    prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
     if (prof) {
         d_prof.alloc((tile_path ? 4ull * tile_grid : 2ull * grid) * (steps + 1));
         d_prof.zero(stream);
@@ -1908,18 +1943,24 @@ void Engine::run_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t adv_
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
     if (tile_path)
-        CK(cudaLaunchCooperativeKernel(world > 1 ? (const void*)tile_kernel<true>
-                                                 : (const void*)tile_kernel<false>,
-                                       tile_grid, kTileThreads, args, tile_smem, stream));
+    {
+        const bool ex = has_forced || has_inj || n_probe_dev > 0;
+        const void* tk = world > 1 ? (ex ? (const void*)tile_kernel<true, true> : (const void*)tile_kernel<true, false>)
+                                   : (ex ? (const void*)tile_kernel<false, true> : (const void*)tile_kernel<false, false>);
+        CK(cudaLaunchCooperativeKernel(tk, tile_grid, kTileThreads, args, tile_smem, stream));
+    }
     else if (packed)
-        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid, kThreads, args,
-                                       smem_bytes, stream));
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<true>, grid_ctas > 0 ? grid_ctas : grid,
+                                       kThreads, args, smem_bytes, stream));
     else
-        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<false>, grid, kThreads, args,
-                                       smem_bytes, stream));
+        CK(cudaLaunchCooperativeKernel((const void*)step_kernel<false>, grid_ctas > 0 ? grid_ctas : grid,
+                                       kThreads, args, smem_bytes, stream));
     CK(cudaEventRecord(ev1, stream));
     launches += 1;
+}
 
+// Wait for the chunk and read its results (rates, spikes, flops, errors).
+void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
     Control c;
     CK(cudaMemcpyAsync(&c, d_ctl.p, sizeof c, cudaMemcpyDeviceToHost, stream));
     std::vector<uint32_t> rr((size_t)n_units * steps);
@@ -2790,6 +2831,86 @@ int vxb_debug_bold_from_drive(int device, const vxb_hemo_params* p, const double
         g_create_error = x.what();
         return fail_code(x);
     }
+}
+
+// Ensemble members advanced together (assim.cpp:231-233 advances them one
+// after another): every member's chunk is launched on its own stream with an
+// equal share of the SMs, so the members run concurrently over the shared
+// tables, then each finishes and reads back its own results.  Members on the
+// SM-tile path (one CTA per SM owns a tile) cannot share the SMs and advance
+// one after another instead.
+int vxb_advance_members(vxb_engine** members, uint32_t count, uint32_t steps) {
+    if (count == 0) return VXB_OK;
+    std::vector<Engine*> es;
+    for (uint32_t m = 0; m < count; ++m) es.push_back(&members[m]->eng);
+    const Engine& e0 = *es[0];
+    bool together = e0.world == 1 && !e0.tile_path && count > 1;
+    for (Engine* e : es)
+        together = together && e->world == 1 && !e->tile_path && e->device == e0.device &&
+                   e->n == e0.n && e->step_done == e0.step_done && !e->failed &&
+                   e->log_spikes() == e0.log_spikes();
+    int rc = VXB_OK;
+    auto fail = [&](Engine* e, const std::exception& x) {
+        e->err = x.what();
+        if (!dynamic_cast<const HemoError*>(&x)) e->failed = true;
+        if (rc == VXB_OK) rc = fail_code(x);
+    };
+    if (!together) {
+        for (uint32_t m = 0; m < count; ++m) {
+            const int r = vxb_advance(members[m], steps);
+            if (r != VXB_OK && rc == VXB_OK) rc = r;
+        }
+        return rc;
+    }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e0.device) != cudaSuccess)
+        return VXB_ESIM;
+    const int per_sm = std::max(1, e0.grid / std::max(1, sms));
+    const int share = per_sm * std::max(1, sms / (int)count);  // CTAs per member
+    std::vector<uint32_t> chunk(count, 0);
+    std::vector<uint8_t> alive(count, 1);
+    for (uint32_t m = 0; m < count; ++m) {
+        try {
+            chunk[m] = es[m]->advance_begin(steps);
+        } catch (const std::exception& x) {
+            fail(es[m], x);
+            alive[m] = 0;
+        }
+    }
+    if (steps == 0) return rc;
+    std::vector<std::vector<unsigned long long>> ph(count);
+    const uint32_t ch = chunk[0] ? chunk[0] : steps;
+    for (uint32_t rel0 = 0; rel0 < steps; rel0 += ch) {
+        const uint32_t cs = std::min(ch, steps - rel0);
+        for (uint32_t m = 0; m < count; ++m) {
+            if (!alive[m]) continue;
+            try {
+                es[m]->launch_chunk(es[m]->step_done + rel0, rel0, cs, steps, share);
+            } catch (const std::exception& x) {
+                fail(es[m], x);
+                alive[m] = 0;
+            }
+        }
+        for (uint32_t m = 0; m < count; ++m) {
+            if (!alive[m]) continue;
+            try {
+                es[m]->finish_chunk(rel0, cs, steps);
+                es[m]->chunk_post(rel0, cs, ph[m]);
+            } catch (const std::exception& x) {
+                fail(es[m], x);
+                alive[m] = 0;
+            }
+        }
+    }
+    for (uint32_t m = 0; m < count; ++m) {
+        if (!alive[m]) continue;
+        try {
+            es[m]->advance_end(steps, ph[m]);
+        } catch (const std::exception& x) {
+            fail(es[m], x);
+        }
+    }
+    return rc;
 }
 
 int vxb_run_simulation(const vxb_network* net, const vxb_options* opt, uint32_t steps,

@@ -129,8 +129,10 @@ __device__ __forceinline__ void tile_add(uint32_t bw, uint32_t per4, uint64_t e)
                  "r"((uint32_t)(e >> 16) & 0xffffffu) : "memory");
 }
 
-// MG: one process per GPU (peers' batches, P2P routing); false: one GPU
-template <bool MG>
+// MG: one process per GPU (peers' batches, P2P routing); false: one GPU.
+// EX: the advance has probes, forced spikes or injections; the variant
+// without them keeps those paths (and their registers) out of the update.
+template <bool MG, bool EX>
 __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const TileLayout L(a.tile_n);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         const bool doE = ph >= 1;
         const uint32_t tA = a.t0 + ph;
         const uint32_t tE = tA - 1;
-        const uint32_t inj_ep = (doA && a.has_inj) ? a.inj_epoch[ph] : 0u;
+        const uint32_t inj_ep = (EX && doA && a.has_inj) ? a.inj_epoch[ph] : 0u;
         uint32_t f_lo = 0, f_hi = 0;
         if (doA && a.has_forced) {
             f_lo = a.forced_off[ph];
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             vb = r ? refrac_bits(r) : __float_as_uint(P.v_reset);
                         } else {
                             float inoise = iou;
-                            if (inj_ep) {
+                            if (EX && inj_ep) {
                                 const float x = __ldg(a.inj_table + (size_t)(inj_ep - 1) * a.n_voxels + S.voxel);
                                 if (x != 0.0f) inoise = fadd(iou, x);
                             }
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             }
                         }
                         // forced spikes (engine.cpp:389-398): join unless already fired
-                        if (f_hi > f_lo && !spiked) {
+                        if (EX && f_hi > f_lo && !spiked) {
                             const uint32_t k = f_lo + lower_bound_u32(a.forced_local + f_lo, f_hi - f_lo, i);
                             if (k < f_hi && __ldg(a.forced_local + k) == i) {
                                 spiked = true;
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         stp(a.v + i, vb, pol_f);
                     }
                     // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
-                    if (a.n_probes) {
+                    if (EX && a.n_probes) {
                         uint32_t k = lower_bound_u32(a.probe_local, a.n_probes, i);
                         while (k < a.n_probes && __ldg(a.probe_local + k) == i) {
                             const size_t row = (size_t)__ldg(a.probe_slot + k) * a.adv_steps + a.rel0;

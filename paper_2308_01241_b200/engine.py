@@ -466,6 +466,25 @@ class SimInstance:
         return json.loads(buf.value.decode())
 
 
+def advance_members(members: Sequence["SimInstance"], steps: int) -> List[RunResult]:
+    """Advance ensemble members of one donor together (vxb_advance_members):
+    concurrently on shares of the SMs where their path allows it, else one
+    after another; returns each member's RunResult."""
+    if not members:
+        return []
+    lib = members[0]._lib
+    hs = (C.c_void_p * len(members))(*[m._h.value if isinstance(m._h, C.c_void_p) else m._h
+                                       for m in members])
+    rc = lib.vxb_advance_members(hs, len(members), steps)
+    if rc != 0:
+        for m in members:
+            msg = lib.vxb_last_error(m._h).decode()
+            if msg:
+                _raise(rc, msg)
+        _raise(rc, "advance_members failed")
+    return [m.result() for m in members]
+
+
 def run_simulation(tables: NetworkTables, options: SimOptions) -> RunResult:
     """voxsim::run_simulation (engine.hpp:92-93)."""
     with SimInstance(tables, options) as sim:

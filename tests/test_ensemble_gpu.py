@@ -97,3 +97,35 @@ def test_member_of_a_different_network_is_rejected():
         donor._tables = b.tables  # a caller handing the wrong network
         with pytest.raises(ConfigError, match="does not match"):
             donor.member()
+
+
+@pytest.mark.parametrize("path", ["l2", "tile"])
+def test_members_advanced_together_equal_independent_instances(monkeypatch, path):
+    """vxb_advance_members: 4 members of one donor advanced together (l2
+    path: concurrently on shares of the SMs; tile path: one after another)
+    over two windows, each with its own conductances, equal independent
+    instances run one by one."""
+    from paper_2308_01241_b200.engine import advance_members
+    monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", path)
+    net = RefNet(make_config(seed=7, voxels=4, npv=500, k_in=30, rho=0.3, ou_mean=400.0,
+                             ou_sigma=150.0), even_workers=2)
+    opt = SimOptions(steps=200, dt_ms=1.0)
+    units = net.tables.units
+    with SimInstance(net.tables, opt) as donor:
+        members = [donor.member() for _ in range(4)]
+        together = []
+        for window in range(2):
+            for k, m in enumerate(members):
+                for u, v in member_conductances(units, 10 * window + k):
+                    m.set_conductances(u, 0, v)
+            res = advance_members(members, 100)
+            together.append([(r, [m.membrane_snapshot(w) for w in range(2)])
+                             for r, m in zip(res, members)])
+        for k in range(4):
+            with SimInstance(net.tables, opt) as solo:
+                for window in range(2):
+                    same(together[window][k],
+                         run(solo, member_conductances(units, 10 * window + k), 100))
+        for m in members:
+            m.close()

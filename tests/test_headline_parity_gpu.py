@@ -132,5 +132,6 @@ def test_config3_slice_sm_tile_path(monkeypatch, tmp_path):
            "partition": {"method": "greedy"},
            "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + bench.G_LOC_10HZ[1:],
                                      "ou_mean": ou}}}
-    ref, _, _ = _compare(cfg, 300, [100, 200], {"path": "sm_tile"})
+    ref, _, _ = _compare(cfg, 300, [100, 200], {"path": "sm_tile"}, tuning={"VXB_PATH": "tile"},
+                         monkeypatch=monkeypatch)
     assert ref.total_spikes > 100_000

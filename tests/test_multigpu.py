@@ -73,10 +73,13 @@ def _gpus():
 @pytest.mark.gpu
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (2, {"VXB_TUNING": "1", "VXB_EARLY_PUBLISH": "1"}),
-                                       (2, {"VXB_TUNING": "1", "VXB_DYN": "0"})])
+                                       (2, {"VXB_TUNING": "1", "VXB_DYN": "0"}),
+                                       (2, {"VXB_TUNING": "1", "VXB_PATH": "tile"}),
+                                       (4, {"VXB_TUNING": "1", "VXB_PATH": "tile"})])
 def test_nvlink_exchange_matches_reference(world, env):
     """Default schedule, plus the optional early batch publication (4-slot
-    ring) and the static delivery deal."""
+    ring), the static delivery deal and the SM-tile path (peers' batches
+    scanned per tile)."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",

@@ -38,6 +38,7 @@
 #include "vxb_kernels.cuh"
 #include "vxb_netgen.cuh"
 #include "vxb_tile.cuh"
+#include "vxb_tile_mp.cuh"
 
 namespace {
 
@@ -214,6 +215,8 @@ struct Engine {
     // SM; chosen when the shard fits on chip (tile_path), else l2_atomic
     bool tile_path = false;
     uint32_t tile_per = 0, tile_cons = 12, tile_smem = 0, tile_grid = 0;
+    bool tile_mp = false;                  // several tiles per SM (tile_mp_kernel)
+    uint32_t tile_T = 0, tile_passes = 1, tile_items = 0;
     uint64_t q_total = 0;
     DevBuf<unsigned long long> d_tl_off;
     DevBuf<uint4> d_tl;
@@ -1198,6 +1201,10 @@ void Engine::share_tables(const Engine& d) {
     tile_path = d.tile_path;
     tile_per = d.tile_per;
     tile_cons = d.tile_cons;
+    tile_mp = d.tile_mp;
+    tile_T = d.tile_T;
+    tile_passes = d.tile_passes;
+    tile_items = d.tile_items;
     tile_smem = d.tile_smem;
     tile_grid = d.tile_grid;
     q_total = d.q_total;
@@ -1326,19 +1333,53 @@ void Engine::setup_tiles() {
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-    const uint32_t per = (uint32_t)((((uint64_t)n + sms - 1) / sms + 31) & ~31ull);
-    const TileLayout L(per);
-    if (L.total > (uint32_t)optin) return;
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
-        tile_cons = (uint32_t)std::min(23, std::max(1, std::atoi(c)));
-    for (const void* tk : {(const void*)tile_kernel<false, false>, (const void*)tile_kernel<false, true>,
-                           (const void*)tile_kernel<true, false>, (const void*)tile_kernel<true, true>})
-        CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, world > 1 ? tile_kernel<true, true> : tile_kernel<false, true>,
-                                                     kTileThreads, L.total));
-    if (per_sm < 1) return;
-    const uint32_t tiles = (uint32_t)((n + per - 1) / per);
+        tile_cons = (uint32_t)std::min(20, std::max(1, std::atoi(c)));
+    cudaFuncAttributes fa1, fa2;
+    CK(cudaFuncGetAttributes(&fa1, (const void*)tile_kernel<true, true>));
+    CK(cudaFuncGetAttributes(&fa2, (const void*)tile_mp_kernel<true>));
+    // one tile per SM (both pending parities in shared memory) when it fits,
+    // else several tiles per SM, one shared accumulator (tile_mp_kernel)
+    uint32_t per = (uint32_t)((((uint64_t)n + sms - 1) / sms + 31) & ~31ull);
+    bool mp = TileLayout(per).total + fa1.sharedSizeBytes > (size_t)optin;
+    if (const char* c = knob("VXB_TILE_PER", &knobs)) {  // force several tiles per SM
+        per = std::max<uint32_t>(32, (uint32_t)std::atoi(c) & ~31u);
+        mp = true;
+    }
+    uint32_t T = sms, smem = 0;
+    if (mp) {
+        if (!knob("VXB_TILE_PER", nullptr)) per = 8192;
+        T = (uint32_t)((n + per - 1) / per);
+        if (T > kMpMaxTiles || 4u * per > 65536u) return;
+        smem = MpLayout(per, T).total;
+        if (smem + fa2.sharedSizeBytes > (size_t)optin) return;
+        for (const void* tk : {(const void*)tile_mp_kernel<false>, (const void*)tile_mp_kernel<true>})
+            CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_mp_kernel<true>, kMpThreads, smem));
+        if (per_sm < 1) return;
+    } else {
+        smem = TileLayout(per).total;
+        for (const void* tk : {(const void*)tile_kernel<false, false>, (const void*)tile_kernel<false, true>,
+                               (const void*)tile_kernel<true, false>, (const void*)tile_kernel<true, true>})
+            CK(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel<true, true>, kTileThreads, smem));
+        if (per_sm < 1) return;
+    }
+    // the 8-byte entries need 24-bit weights: check before touching the tables
+    {
+        DevBuf<unsigned int> flag;
+        flag.alloc(1);
+        flag.zero(stream);
+        if (n_syn)
+            tile_entries_kernel<<<1184, 256, 0, stream>>>(d_tgt.p, d_w.p, n_syn, per, nullptr, flag.p);
+        CK(cudaGetLastError());
+        unsigned int bad = 0;
+        CK(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (bad) return;
+    }
     sort_rows();
     // tile segments of every row: count, scan, write
     DevBuf<unsigned long long> cnt;
@@ -1361,63 +1402,53 @@ void Engine::setup_tiles() {
     CK(cudaMemcpyAsync(&total, d_tl_off.p + n_src, 8, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     cnt.release();
+    if (total >= (1ull << 32) || n_syn >= (1ull << 40)) {  // queue items: 32-bit slots, 40-bit entries
+        d_tl_off.release();
+        return;
+    }
     d_tl.alloc(std::max<unsigned long long>(1, total));
     DevBuf<uint32_t> cap;
-    cap.alloc(sms + 1);  // [sms]: a segment too long for a queue item
+    cap.alloc(T + 1);  // [T]: a segment too long for a queue item
     cap.zero(stream);
     tile_segments_kernel<1><<<1184, 256, 0, stream>>>(reinterpret_cast<const uint64_t*>(d_off.p),
                                                        d_tgt.p, n_src, per, nullptr, d_tl_off.p,
-                                                       d_tl.p, cap.p, cap.p + sms);
+                                                       d_tl.p, cap.p, cap.p + T);
     CK(cudaGetLastError());
-    std::vector<uint32_t> hcap(sms + 1), qb(sms + 1, 0);
-    CK(cudaMemcpyAsync(hcap.data(), cap.p, 4ull * (sms + 1), cudaMemcpyDeviceToHost, stream));
+    std::vector<uint32_t> hcap(T + 1), qb(T + 1, 0);
+    CK(cudaMemcpyAsync(hcap.data(), cap.p, 4ull * (T + 1), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    if (hcap[sms]) {  // keep the l2_atomic path
+    if (hcap[T]) {  // keep the l2_atomic path
         d_tl.release();
         d_tl_off.release();
         return;
     }
-    for (int t = 0; t < sms; ++t) qb[t + 1] = qb[t] + hcap[t];
-    if (total >= (1ull << 32)) throw SimError("tile segment table exceeds 2^32 entries");
-    if (n_syn >= (1ull << 40)) return;  // queue items address entries with 40 bits
+    for (uint32_t t = 0; t < T; ++t) qb[t + 1] = qb[t] + hcap[t];
     q_total = total;
-    d_qbase.alloc(sms + 1);
-    CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 4ull * (sms + 1), cudaMemcpyHostToDevice, stream));
+    d_qbase.alloc(T + 1);
+    CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 4ull * (T + 1), cudaMemcpyHostToDevice, stream));
     d_q.alloc(std::max<uint64_t>(1, 2 * total));
-    d_qcnt.alloc(2ull * sms);
+    d_qcnt.alloc(2ull * T);
     d_qcnt.zero(stream);
-    // 8-byte entries (tile-local target, class, both weights): 2/3 of the
-    // 12-byte stream; networks whose weights do not fit 24 bits keep the
-    // l2_atomic path
-    {
-        DevBuf<unsigned int> flag;
-        flag.alloc(1);
-        flag.zero(stream);
-        d_tent.alloc(std::max<uint64_t>(1, n_syn));
-        if (n_syn)
-            tile_entries_kernel<<<1184, 256, 0, stream>>>(d_tgt.p, d_w.p, n_syn, per, d_tent.p, flag.p);
-        CK(cudaGetLastError());
-        unsigned int bad = 0;
-        CK(cudaMemcpyAsync(&bad, flag.p, 4, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        if (bad) {
-            d_tent.release();
-            d_tl.release();
-            d_tl_off.release();
-            d_q.release();
-            d_qcnt.release();
-            d_qbase.release();
-            return;
-        }
-    }
-    d_tgt.release();  // the tile path reads only the 8-byte entries
-    d_w.release();
+    // 8-byte entries (accumulator word offset + both weights), written over
+    // the 8-byte weight array: 2/3 of the 12-byte stream, no extra memory
+    if (n_syn)
+        tile_entries_kernel<<<1184, 256, 0, stream>>>(d_tgt.p, d_w.p, n_syn, per, d_w.p, cap.p + T);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream));
+    d_tent.share(d_w);
+    d_w.release();
+    d_tgt.release();  // the tile path reads only the 8-byte entries
     tile_path = true;
+    tile_mp = mp;
     tile_per = per;
-    tile_smem = L.total;
+    tile_T = T;
+    tile_passes = mp ? (T + sms - 1) / sms : 1u;
+    tile_smem = smem;
     tile_grid = (uint32_t)sms;
-    (void)tiles;
+    // short segments (the DTI-like networks' ~20 entries) are consumed one
+    // queue item per lane, long ones (config 2: ~200) one per warp
+    tile_items = total && n_syn / total < 64 ? 1u : 0u;
+    if (const char* c = knob("VXB_TILE_ITEMS", &knobs)) tile_items = std::atoi(c) ? 1u : 0u;
 }
 
 // crossing_matrix (netgen.cpp:331-355, BuiltNetwork::crossing): synapses
@@ -1449,7 +1480,8 @@ void Engine::init_tile_state() {
     d_iou_b.alloc(std::max<uint32_t>(1, n));
     if (n) CK(cudaMemcpyAsync(d_iou_b.p, d_iou.p, 4ull * n, cudaMemcpyDeviceToDevice, stream));
     d_q.reserve(std::max<uint64_t>(1, 2 * q_total));
-    d_qcnt.reserve(2ull * tile_grid);
+    d_qcnt.reserve(2ull * tile_T);
+    d_qcnt.zero(stream);
     CK(cudaStreamSynchronize(stream));
 }
 
@@ -1938,12 +1970,18 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
         a.src_self = world > 1 ? src_base[rank] : 0u;
         a.tent = d_tent.p;
         a.i_ou_b = d_iou_b.p;
+        a.n_tiles = tile_T;
+        a.passes = tile_passes;
+        a.item_mode = tile_items;
         d_qcnt.zero(stream);
     }
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
-    if (tile_path)
-    {
+    if (tile_path && tile_mp) {
+        CK(cudaLaunchCooperativeKernel(world > 1 ? (const void*)tile_mp_kernel<true>
+                                                 : (const void*)tile_mp_kernel<false>,
+                                       tile_grid, kMpThreads, args, tile_smem, stream));
+    } else if (tile_path) {
         const bool ex = has_forced || has_inj || n_probe_dev > 0;
         const void* tk = world > 1 ? (ex ? (const void*)tile_kernel<true, true> : (const void*)tile_kernel<true, false>)
                                    : (ex ? (const void*)tile_kernel<false, true> : (const void*)tile_kernel<false, false>);
@@ -2117,11 +2155,14 @@ void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
 // tuning knob that was applied: logged beside each benchmark result.
 std::string Engine::schedule_info() const {
     if (tile_path)
-        return fmt("{\"path\":\"sm_tile\",\"kernel\":\"vxb::tile_kernel\",\"grid\":%u,"
+        return fmt("{\"path\":\"sm_tile\",\"kernel\":\"%s\",\"grid\":%u,"
+                   "\"tiles\":%u,\"passes\":%u,\"item_per\":\"%s\","
                    "\"threads\":%d,\"smem_bytes\":%u,\"tile_neurons\":%u,"
                    "\"unroll\":%u,\"consumer_warps\":%u,\"queue_items\":%llu,"
                    "\"state_l2_policy\":%u,\"packed_pending\":%d,\"world\":%u,\"knobs\":{",
-                   tile_grid, kTileThreads, tile_smem, tile_per, kTileUnroll, tile_cons,
+                   tile_mp ? "vxb::tile_mp_kernel" : "vxb::tile_kernel", tile_grid, tile_T,
+                   tile_passes, tile_items ? "lane" : "warp",
+                   tile_mp ? kMpThreads : kTileThreads, tile_smem, tile_per, kTileUnroll, tile_cons,
                    (unsigned long long)q_total, f_policy, (int)packed, world) +
                knobs + "}}";
     return fmt("{\"path\":\"l2_atomic\",\"kernel\":\"vxb::step_kernel\",\"grid\":%d,"

@@ -88,7 +88,8 @@ struct Control {
     // stop decision of the phase, taken once by the last CTA through the
     // barrier (hook) so every CTA leaves the loop at the same phase
     unsigned int stop;
-    unsigned int pad[4];
+    unsigned int rdone;        // tile_mp_kernel: CTAs done with the peers' batches (monotonic)
+    unsigned int pad[3];
 };
 
 // Device-side state of the per-step spike-id exchange between ranks (one
@@ -203,6 +204,9 @@ struct StepArgs {
     uint32_t src_self;          // global source index of shard-local neuron 0
     const uint64_t* tent;       // 8-byte tile entries (same indexing as tgt / w)
     float* i_ou_b;              // I_ou of odd steps (tile path; i_ou holds even steps)
+    uint32_t n_tiles;           // tile_mp_kernel: tiles (T) and passes per CTA (P)
+    uint32_t passes;
+    uint32_t item_mode;         // 0: one queue item per warp, 1: one per lane
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {

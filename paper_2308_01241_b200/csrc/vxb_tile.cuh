@@ -677,8 +677,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
 // fast receptor's sum in the pending tile (< 2^16) and both Q16 weights
 // (< 2^24 each: checked, else the engine keeps the l2_atomic path).  flag[0]
 // is set when an entry does not fit.
-__global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint64_t* __restrict__ w,
-                                    uint64_t n_syn, uint32_t per, uint64_t* __restrict__ tent,
+// tent == nullptr only checks; tent == w converts in place (each thread reads
+// its entry before writing it).
+__global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint64_t* w,
+                                    uint64_t n_syn, uint32_t per, uint64_t* tent,
                                     unsigned int* __restrict__ flag) {
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_syn;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -687,8 +689,9 @@ __global__ void tile_entries_kernel(const uint32_t* __restrict__ tgt, const uint
         const uint32_t wf = (uint32_t)wq, ws = (uint32_t)(wq >> 32);
         const uint32_t off = (t >> 31) * 2u * per + tid % per;  // fast receptor's word
         if (wf >= (1u << 24) || ws >= (1u << 24) || off + per >= (1u << 16)) atomicExch(flag, 1u);
-        tent[k] = ((uint64_t)(wf & 0xffffffu) << 40) | ((uint64_t)(ws & 0xffffffu) << 16) |
-                  (off & 0xffffu);
+        if (tent)
+            tent[k] = ((uint64_t)(wf & 0xffffffu) << 40) | ((uint64_t)(ws & 0xffffffu) << 16) |
+                      (off & 0xffffu);
     }
 }
 

@@ -391,13 +391,23 @@ def test_acceptance_1_multi_worker_equivalence():
         assert np.array_equal(state, ref_state)
 
 
-@pytest.mark.parametrize("path,dyn", [("l2", "0"), ("l2", "1"), ("tile", "1")])
+def set_path(monkeypatch, path):
+    """tile / l2 / mp (several tiles per SM, 64-neuron tiles) / mp_lane (mp
+    with one queue item per lane)."""
+    monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", "l2" if path == "l2" else "tile")
+    if path.startswith("mp"):
+        monkeypatch.setenv("VXB_TILE_PER", "64")
+        monkeypatch.setenv("VXB_TILE_ITEMS", "1" if path == "mp_lane" else "0")
+
+
+@pytest.mark.parametrize("path,dyn", [("l2", "0"), ("l2", "1"), ("tile", "1"), ("mp", "1"),
+                                      ("mp_lane", "1")])
 def test_static_and_dynamic_delivery_match_reference(monkeypatch, path, dyn):
     """Every delivery schedule is bit-exact (config 1 shape): the l2_atomic
     path's static round-robin rows (VXB_DYN=0) and block-major dynamic
     chunks, and the SM-tile path (shared-memory pending tiles)."""
-    monkeypatch.setenv("VXB_TUNING", "1")
-    monkeypatch.setenv("VXB_PATH", path)
+    set_path(monkeypatch, path)
     monkeypatch.setenv("VXB_DYN", dyn)
     cfg = make_config(seed=1, voxels=1, npv=10000, k_in=100, dt_ms=0.1, steps=3000)
     net = RefNet(cfg)
@@ -465,17 +475,19 @@ def test_advance_without_forced_spikes_or_injection_after_one_with():
         assert np.array_equal(snaps[w], rs.membrane_snapshot(w))
 
 
-@pytest.mark.parametrize("path", ["tile", "l2"])
+@pytest.mark.parametrize("path", ["tile", "l2", "mp", "mp_lane"])
 def test_ring_multiworker_both_paths(monkeypatch, path):
     """3 workers on one device, both delivery paths, two advances: the
     SM-tile path (default for shards that fit on chip) and the l2_atomic
     path give the reference's results bit for bit."""
-    monkeypatch.setenv("VXB_TUNING", "1")
-    monkeypatch.setenv("VXB_PATH", path)
+    set_path(monkeypatch, path)
     net = RefNet(hot_cfg(seed=31, voxels=5, npv=900, k_in=40, rho=0.3), even_workers=3)
     opt = SimOptions(steps=150, probe_gids=[3, 1000, 4499])
     with SimInstance(net.tables, opt) as sim:
-        assert sim.schedule_info()["path"] == ("sm_tile" if path == "tile" else "l2_atomic")
+        info = sim.schedule_info()
+        assert info["path"] == ("l2_atomic" if path == "l2" else "sm_tile")
+        if path.startswith("mp"):
+            assert info["kernel"] == "vxb::tile_mp_kernel" and info["passes"] >= 2
         a = sim.advance(70)
         b = sim.advance(80)
         snaps = [sim.membrane_snapshot(w) for w in range(3)]

@@ -84,12 +84,18 @@ def test_config2_two_workers_on_one_device():
     _same(one, two)
 
 
-def test_config3_l2_blocked_equals_unblocked(monkeypatch):
+def test_config3_tiles_equal_l2_blocked_equal_unblocked(monkeypatch):
+    """Config 3 (2e7 neurons, 1e10 synapses): the several-tiles-per-SM path
+    (the default at this size) == the l2 path with 5 L2 blocks == the l2
+    path with plain L2 atomics."""
     import bench
     cfg = bench.dti_cfg()
-    blocked = _run(cfg, [12])
+    tiles = _run(cfg, [12])
     monkeypatch.setenv("VXB_TUNING", "1")
+    monkeypatch.setenv("VXB_PATH", "l2")
+    blocked = _run(cfg, [12])
     monkeypatch.setenv("VXB_BLOCK_NEURONS", str(1 << 30))  # one block: plain L2 atomics
     plain = _run(cfg, [12])
     assert blocked[3] > 10_000_000
     _same(blocked, plain)
+    _same(tiles, blocked)

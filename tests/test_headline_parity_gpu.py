@@ -135,3 +135,24 @@ def test_config3_slice_sm_tile_path(monkeypatch, tmp_path):
     ref, _, _ = _compare(cfg, 300, [100, 200], {"path": "sm_tile"}, tuning={"VXB_PATH": "tile"},
                          monkeypatch=monkeypatch)
     assert ref.total_spikes > 100_000
+
+
+def test_config3_slice_multipass_tiles(monkeypatch, tmp_path):
+    """The DTI-like slice on the several-tiles-per-SM kernel (tile_mp_kernel,
+    the configs-3-5 path): 256-neuron tiles, so ~5 passes per CTA, and short
+    segments consumed one queue item per lane."""
+    import bench
+    path = tmp_path / "dti200.txt"
+    netgen.write_connectome_file(netgen.dti_like_connectome(total_neurons=200_000), path)
+    ampa, ou = bench.K500_POINTS[10]
+    cfg = {"seed": bench.SEED, "dt_ms": 1.0, "steps": 300, "workers": 2,
+           "scheduler": "loopback",
+           "connectome": {"kind": "file", "path": str(path)},
+           "partition": {"method": "greedy"},
+           "regions": {"subcortex": {"k_in": 500, "g_location": [ampa] + bench.G_LOC_10HZ[1:],
+                                     "ou_mean": ou}}}
+    ref, _, sched = _compare(cfg, 300, [120, 180], {"path": "sm_tile", "kernel": "vxb::tile_mp_kernel",
+                                                    "item_per": "lane"},
+                             tuning={"VXB_PATH": "tile", "VXB_TILE_PER": "256"},
+                             monkeypatch=monkeypatch)
+    assert sched["passes"] >= 5 and ref.total_spikes > 100_000

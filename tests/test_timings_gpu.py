@@ -43,10 +43,12 @@ def _criterion9_cfg(quiet=False):
             "partition": {"method": "greedy"}, "regions": {"subcortex": reg}}
 
 
-@pytest.mark.parametrize("path", ["tile", "l2"])
+@pytest.mark.parametrize("path", ["tile", "l2", "mp"])
 def test_statistics_identities_criterion9(monkeypatch, path):
     monkeypatch.setenv("VXB_TUNING", "1")
-    monkeypatch.setenv("VXB_PATH", path)
+    monkeypatch.setenv("VXB_PATH", "l2" if path == "l2" else "tile")
+    if path == "mp":
+        monkeypatch.setenv("VXB_TILE_PER", "32")
     cfg = _criterion9_cfg()
     net = RefNet(cfg)
     opt = SimOptions(steps=60, workers_per_node=2)

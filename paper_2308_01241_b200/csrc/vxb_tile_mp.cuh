@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
     const uint32_t n_cons = a.n_cons;
     const uint32_t n_upd = kMpThreads / 32 - n_cons;
     const bool upd_warp = warp >= n_cons;
+    const uint32_t ut = threadIdx.x - n_cons * 32;  // index among update threads
     const bool bucket_warp = warp >= kMpThreads / 32 - kTileBucketWarps;
     const uint32_t bt = threadIdx.x - (kMpThreads - 32 * kTileBucketWarps);
     const uint32_t nbt = 32 * kTileBucketWarps;
@@ -308,13 +309,13 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                 ch = chn;
                 i = inext;
             }
-            if (bucket_warp)
-                named_sync(1, n_upd * 32);
-            else
-                asm volatile("bar.arrive 1, %0;" ::"r"(n_upd * 32) : "memory");
-
-            if (bucket_warp) {
+            named_sync(1, n_upd * 32);  // the CTA's spikes of S(tA) are staged
+            if (a.prof && ut == 0) s_t[0] = globaltimer();
+            {
                 // ------------------------------------------------ B (bucketing)
+                // every update warp: a CTA holds ~1.4k spikes per step on
+                // config 3 (45 on config 2)
+                const uint32_t bt = ut, nbt = n_upd * 32;
                 const uint32_t nst = doA ? min(s_nspk, (uint32_t)kSpkStage) : 0u;
                 if (nst) {
                     const uint32_t par = tA & 1u;
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                         const uint64_t k1 = __ldg(a.tl_off + s + 1);
                         for (uint64_t q = __ldg(a.tl_off + s); q < k1; ++q) atomicAdd(&s_hist[__ldg(&a.tl[q].x)], 1u);
                     }
-                    named_sync(2, nbt);
+                    named_sync(4, nbt);
                     for (uint32_t t = bt; t < T; t += nbt) {
                         const uint32_t h = s_hist[t];
                         if (h) {
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                             s_hist[t] = 0u;
                         }
                     }
-                    named_sync(2, nbt);
+                    named_sync(4, nbt);
                     uint64_t* qp = a.q + (size_t)par * a.q_total;
                     for (uint32_t k = bt; k < nst; k += nbt) {
                         const uint32_t s = a.src_self + s_spk[k];
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                             qp[pos] = (row + sg.y) | ((uint64_t)sg.z << 40);
                         }
                     }
-                    named_sync(2, nbt);
+                    named_sync(4, nbt);
                     for (uint32_t t = bt; t < T; t += nbt) s_hist[t] = 0u;
                     if (MG) {
                         bool sent = false;
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                     }
                 }
             }
+            if (a.prof && ut == 0) s_t[1] = globaltimer();
             // ------------------------------------------------ N (OU step)
             if (doA) {
                 for (;;) {
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                     }
                 }
             }
+            if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
         } else if (doE) {
             // ------------------------------------------------ C (consumers)
             const uint32_t par = tE & 1u;
@@ -402,7 +405,10 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                     uint32_t it = 0;
                     if (lane == 0) it = atomicAdd(&s_iwork, a.item_mode ? 32u : 1u);
                     it = __shfl_sync(0xffffffffu, it, 0);
-                    while (it >= cnt && !final_cnt) {  // (MG) wait for the peers' items
+                    // (MG) a grab that reaches past the items known so far
+                    // waits for the peers' items (or for the count to be final)
+                    const uint32_t span = a.item_mode ? 32u : 1u;
+                    while (it + span > cnt && !final_cnt) {
                         if (ld_acquire(&ctl->rdone) >= G * ph) {
                             final_cnt = true;
                         } else {
@@ -454,6 +460,11 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
 
         // flush the CTA's staged spikes with one log reservation
         __syncthreads();
+        if (a.prof && threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) {
+                a.prof[4 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
+                s_t[k] = 0;
+            }
         const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
         if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
         __syncthreads();

@@ -392,12 +392,12 @@ def test_acceptance_1_multi_worker_equivalence():
 
 
 def set_path(monkeypatch, path):
-    """tile / l2 / mp (several tiles per SM, 64-neuron tiles) / mp_lane (mp
+    """tile / l2 / mp (several tiles per SM, 32-neuron tiles) / mp_lane (mp
     with one queue item per lane)."""
     monkeypatch.setenv("VXB_TUNING", "1")
     monkeypatch.setenv("VXB_PATH", "l2" if path == "l2" else "tile")
     if path.startswith("mp"):
-        monkeypatch.setenv("VXB_TILE_PER", "64")
+        monkeypatch.setenv("VXB_TILE_PER", "32")
         monkeypatch.setenv("VXB_TILE_ITEMS", "1" if path == "mp_lane" else "0")
 
 
@@ -481,8 +481,8 @@ def test_ring_multiworker_both_paths(monkeypatch, path):
     SM-tile path (default for shards that fit on chip) and the l2_atomic
     path give the reference's results bit for bit."""
     set_path(monkeypatch, path)
-    net = RefNet(hot_cfg(seed=31, voxels=5, npv=900, k_in=40, rho=0.3), even_workers=3)
-    opt = SimOptions(steps=150, probe_gids=[3, 1000, 4499])
+    net = RefNet(hot_cfg(seed=31, voxels=5, npv=2000, k_in=40, rho=0.3), even_workers=3)
+    opt = SimOptions(steps=150, probe_gids=[3, 1000, 9999])
     with SimInstance(net.tables, opt) as sim:
         info = sim.schedule_info()
         assert info["path"] == ("l2_atomic" if path == "l2" else "sm_tile")

@@ -18,6 +18,7 @@ ap.add_argument("--path", default="")
 ap.add_argument("--silent", action="store_true", help="ou_mean = 0: no spikes")
 ap.add_argument("--cons", default="", help="VXB_TILE_CONS (consumer warps)")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--workload", default="config2", choices=["config2", "config3"])
 args = ap.parse_args()
 os.environ["VXB_TUNING"] = "1"
 os.environ["VXB_PHASE_PROFILE"] = "1"
@@ -29,7 +30,7 @@ import bench  # noqa: E402
 from paper_2308_01241_b200 import netgen  # noqa: E402
 from paper_2308_01241_b200.engine import SimOptions  # noqa: E402
 
-cfg = bench.workload_cfg(voxels=args.voxels)
+cfg = bench.workload_cfg(voxels=args.voxels) if args.workload == "config2" else bench.dti_cfg()
 if args.silent:
     cfg["regions"]["subcortex"]["ou_mean"] = 0.0
 

@@ -216,6 +216,8 @@ struct Engine {
     bool tile_path = false;
     uint32_t tile_per = 0, tile_cons = 12, tile_smem = 0, tile_grid = 0;
     bool tile_mp = false;                  // several tiles per SM (tile_mp_kernel)
+    // queue sets: tile_kernel rotates four (no grid barrier), tile_mp_kernel two
+    uint32_t q_sets() const { return tile_mp ? 2u : kTileQSets; }
     uint32_t tile_T = 0, tile_passes = 1, tile_items = 0;
     uint64_t q_total = 0;
     DevBuf<unsigned long long> d_tl_off;
@@ -247,6 +249,7 @@ struct Engine {
     DevBuf<uint64_t> d_w;
     DevBuf<uint32_t> d_spk;
     DevBuf<uint32_t> d_seg_end;
+    DevBuf<uint32_t> d_bdone;  // tile_kernel: per phase, CTAs done bucketing
     DevBuf<uint32_t> d_rates;
     DevBuf<uint32_t> d_probe_local, d_probe_slot;
     DevBuf<float> d_probe_v, d_probe_i;
@@ -1329,7 +1332,8 @@ void Engine::setup_tiles() {
     // fixed costs (bucketing round trips, per-tile queues) dominate there
     // (config-2 shape, 100k neurons: l2 17 vs tile 24 us/step; 1M neurons:
     // tile 53.5 vs l2 72)
-    if (!(force && std::string(force) == "tile") && n < kTileMinNeurons) return;
+    const bool force_tile = force && (std::string(force) == "tile" || std::string(force) == "mp");
+    if (!force_tile && n < kTileMinNeurons) return;
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -1342,6 +1346,15 @@ void Engine::setup_tiles() {
     // else several tiles per SM, one shared accumulator (tile_mp_kernel)
     uint32_t per = (uint32_t)((((uint64_t)n + sms - 1) / sms + 31) & ~31ull);
     bool mp = TileLayout(per).total + fa1.sharedSizeBytes > (size_t)optin;
+    // several tiles per SM only on request (VXB_PATH=mp / tile, VXB_TILE_PER):
+    // measured slower than the L2-blocked l2_atomic path at every shard size
+    // that does not fit one tile per SM (config-2 shape 2M neurons: 214 vs
+    // 143 us/step, 4M: 404 vs 325; config 3 20M: 2.04 vs 1.13 ms/step).  The
+    // K targets of a spike spread over thousands of tiles, so a tile segment
+    // averages < 1 entry and every event pays a queue item on top of its
+    // entry
+    if (mp && !force_tile && !knob("VXB_TILE_PER", nullptr)) return;
+    if (force && std::string(force) == "mp") mp = true;
     if (const char* c = knob("VXB_TILE_PER", &knobs)) {  // force several tiles per SM
         per = std::max<uint32_t>(32, (uint32_t)std::atoi(c) & ~31u);
         mp = true;
@@ -1426,8 +1439,8 @@ void Engine::setup_tiles() {
     q_total = total;
     d_qbase.alloc(T + 1);
     CK(cudaMemcpyAsync(d_qbase.p, qb.data(), 4ull * (T + 1), cudaMemcpyHostToDevice, stream));
-    d_q.alloc(std::max<uint64_t>(1, 2 * total));
-    d_qcnt.alloc(2ull * T);
+    d_q.alloc(std::max<uint64_t>(1, (mp ? 2ull : kTileQSets) * total));
+    d_qcnt.alloc((mp ? 2ull : kTileQSets) * T);
     d_qcnt.zero(stream);
     // 8-byte entries (accumulator word offset + both weights), written over
     // the 8-byte weight array: 2/3 of the 12-byte stream, no extra memory
@@ -1479,8 +1492,8 @@ void Engine::compute_crossing() {
 void Engine::init_tile_state() {
     d_iou_b.alloc(std::max<uint32_t>(1, n));
     if (n) CK(cudaMemcpyAsync(d_iou_b.p, d_iou.p, 4ull * n, cudaMemcpyDeviceToDevice, stream));
-    d_q.reserve(std::max<uint64_t>(1, 2 * q_total));
-    d_qcnt.reserve(2ull * tile_T);
+    d_q.reserve(std::max<uint64_t>(1, (uint64_t)q_sets() * q_total));
+    d_qcnt.reserve((size_t)q_sets() * tile_T);
     d_qcnt.zero(stream);
     CK(cudaStreamSynchronize(stream));
 }
@@ -1709,6 +1722,7 @@ uint32_t Engine::advance_begin(uint32_t steps) {
     const uint32_t cap_entries = log_spikes() ? n * chunk : 2 * n;
     if (d_spk.n < std::max<size_t>(1, cap_entries)) d_spk.alloc(std::max<size_t>(1, cap_entries));
     d_seg_end.reserve(chunk + 2);
+    d_bdone.reserve(chunk + 2);
     d_rates.reserve((size_t)n_units * chunk);
     d_phase_ns.reserve(chunk + 2);
     d_phase_wait.reserve(chunk + 2);
@@ -1885,6 +1899,7 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
     CK(cudaMemcpyAsync(d_ctl.p, &c0, sizeof c0, cudaMemcpyHostToDevice, stream));
     d_rates.zero(stream);
     CK(cudaMemsetAsync(d_seg_end.p, 0, 4 * d_seg_end.n, stream));
+    CK(cudaMemsetAsync(d_phase_ns.p, 0, 8 * d_phase_ns.n, stream));
 
     StepArgs a;
     std::memset(&a, 0, sizeof a);
@@ -1953,7 +1968,7 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
     a.early_publish = early_publish ? 1u : 0u;
     prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
     if (prof) {
-        d_prof.alloc((tile_path ? 4ull * tile_grid : 2ull * grid) * (steps + 1));
+        d_prof.alloc((tile_path ? (tile_mp ? 4ull : 5ull) * tile_grid : 2ull * grid) * (steps + 1));
         d_prof.zero(stream);
         a.prof = d_prof.p;
     }
@@ -1974,6 +1989,8 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
         a.passes = tile_passes;
         a.item_mode = tile_items;
         d_qcnt.zero(stream);
+        a.bdone = d_bdone.p;
+        d_bdone.zero(stream);
     }
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
@@ -2007,6 +2024,8 @@ void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
     std::vector<uint32_t> seg_end(steps + 1);
     CK(cudaMemcpyAsync(seg_end.data(), d_seg_end.p, 4ull * (steps + 1), cudaMemcpyDeviceToHost,
                        stream));
+    // tile_kernel's log is phase-strided with per-phase counts
+    const bool strided = tile_path && !tile_mp;
     if (world > 1) {
         std::vector<unsigned long long> pw(steps + 2);
         CK(cudaMemcpyAsync(pw.data(), d_phase_wait.p, 8ull * (steps + 2), cudaMemcpyDeviceToHost,
@@ -2036,18 +2055,22 @@ void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
         CK(cudaMemcpy(pn.data(), d_phase_ns.p, 8 * pn.size(), cudaMemcpyDeviceToHost));
         double sum[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0}, sp = 0;
         uint32_t cnt[4] = {0, 0, 0, 0};
+        // tile_kernel (no barrier): relative to the CTA's own phase start;
+        // tile_mp_kernel: to the end of the previous phase's barrier
+        const size_t ps = tile_mp ? 4 : 5;
         for (uint32_t ph = 1; ph < steps; ++ph) {
-            const double t0 = (double)pn[ph];
             sp += (double)(pn[ph + 1] - pn[ph]);
             double pm[4] = {0, 0, 0, 0};
-            for (uint32_t b = 0; b < tile_grid; ++b)
+            for (uint32_t b = 0; b < tile_grid; ++b) {
+                const double t0 = ps == 5 ? (double)pr[ps * ((size_t)ph * tile_grid + b) + 4] : (double)pn[ph];
                 for (int k = 0; k < 4; ++k) {
-                    const unsigned long long x = pr[4 * ((size_t)ph * tile_grid + b) + k];
+                    const unsigned long long x = pr[ps * ((size_t)ph * tile_grid + b) + k];
                     if (!x) continue;
-                    sum[k] += x - t0;
+                    sum[k] += (double)x - t0;
                     ++cnt[k];
-                    pm[k] = std::max(pm[k], x - t0);
+                    pm[k] = std::max(pm[k], (double)x - t0);
                 }
+            }
             for (int k = 0; k < 4; ++k) mx[k] += pm[k];
         }
         const double np_ = std::max(1u, steps - 1);
@@ -2118,12 +2141,17 @@ void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
     flops.gating_outer += c.flops_outer;
 
     if (log_spikes()) {
+        if (strided) {  // counts -> cumulative ends for the key kernel
+            for (uint32_t p = 1; p <= steps; ++p) seg_end[p] += seg_end[p - 1];
+            CK(cudaMemcpyAsync(d_seg_end.p, seg_end.data(), 4ull * (steps + 1), cudaMemcpyHostToDevice,
+                               stream));
+        }
         const uint32_t total = seg_end[steps - 1];
         if (total) {
             if (d_keys.n < total) d_keys.alloc(total);
             if (d_keys_sorted.n < total) d_keys_sorted.alloc(total);
             raster_keys_kernel<<<std::min<uint32_t>(steps, 4096), 256, 0, stream>>>(
-                d_spk.p, d_seg_end.p, steps, d_keys.p);
+                d_spk.p, d_seg_end.p, steps, d_keys.p, strided ? n : 0u);
             CK(cudaGetLastError());
             launches += 1;
             int end_bit = 32;

@@ -199,14 +199,19 @@ struct StepArgs {
     const unsigned long long* tl_off;  // per global source: first tile segment (n_src + 1)
     const uint4* tl;            // tile segments {tile, first entry in row, length, 0}
     const uint32_t* q_base;     // per tile: first queue slot (tiles + 1)
-    uint32_t* q_cnt;            // [2][tiles] items queued per (parity, tile)
-    uint64_t* q;                // [2][q_total] first entry | length << 40
+    uint32_t* q_cnt;            // [sets][tiles] items queued per (step set, tile): 4 sets
+                                // (tile_kernel, step & 3), 2 (tile_mp_kernel, parity)
+    uint64_t* q;                // [sets][q_total] first entry | length << 40
     uint32_t src_self;          // global source index of shard-local neuron 0
     const uint64_t* tent;       // 8-byte tile entries (same indexing as tgt / w)
     float* i_ou_b;              // I_ou of odd steps (tile path; i_ou holds even steps)
     uint32_t n_tiles;           // tile_mp_kernel: tiles (T) and passes per CTA (P)
     uint32_t passes;
     uint32_t item_mode;         // 0: one queue item per warp, 1: one per lane
+    // tile_kernel (no grid barrier): per phase, CTAs whose bucketing of that
+    // phase's spikes is complete; the spike log is phase-strided (entries of
+    // phase p at spk[p * n], per-phase counts in seg_end)
+    uint32_t* bdone;
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {
@@ -1458,13 +1463,16 @@ __global__ void mask_check_kernel(const unsigned long long* __restrict__ have,
 }
 
 // Pack (step << 32 | local) keys of the spike log for the raster sort.
+// seg_end: cumulative log ends per step; stride != 0: the log is
+// phase-strided (step s's entries at spk[s * stride], tile_kernel).
 __global__ void raster_keys_kernel(const uint32_t* __restrict__ spk,
                                    const uint32_t* __restrict__ seg_end, uint32_t steps,
-                                   uint64_t* __restrict__ keys) {
+                                   uint64_t* __restrict__ keys, uint32_t stride) {
     for (uint32_t s = blockIdx.x; s < steps; s += gridDim.x) {
         const uint32_t lo = s ? seg_end[s - 1] : 0u, hi = seg_end[s];
+        const uint32_t* src = stride ? spk + (size_t)s * stride - lo : spk;
         for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
-            keys[k] = ((uint64_t)s << 32) | spk[k];
+            keys[k] = ((uint64_t)s << 32) | src[k];
     }
 }
 

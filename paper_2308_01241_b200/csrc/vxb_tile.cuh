@@ -32,7 +32,13 @@
 //                     phase ph + 1.
 //   N  (other warps)  advance I_ou to tA (fp64 Box-Muller noise, ou_kernel)
 //                     for the tile, overlapping the delivery.
-//   grid barrier.
+//   no grid barrier: a CTA goes on to phase ph + 1 as soon as its own C and N
+//   are done (U(ph + 1) needs only its tile's pending sums and I_ou).  Only
+//   the consumers of phase ph + 1 depend on the other CTAs — on their
+//   bucketing of S(tA) — and wait for that phase's count (bdone[ph] == G).
+//   Queues rotate over four step sets (tA & 3): a CTA can be bucketing
+//   S(tA + 1) while a slower one still consumes S(tE); with four sets a
+//   writer of set tA & 3 is provably behind every consumer of it.
 // Moving the OU step one phase earlier is exact: I_ou(t) depends only on
 // I_ou(t-1) and xi(gid, t) (ou_kernel, model.hpp:88-90; engine.cpp:551-558).
 // Between chunks (and advance() calls) the state is the reference's
@@ -58,6 +64,7 @@ constexpr uint32_t kTileUnroll = VXB_TILE_UNROLL;  // synapse entries in flight 
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
 constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
 constexpr uint32_t kTileBucketWarps = 2;
+constexpr uint32_t kTileQSets = 4;      // queue sets (step & 3), see the phase notes above
 // queue item: first entry (bits 0-39) | segment length << 40
 constexpr uint64_t kItemBeg = (1ull << 40) - 1;
 constexpr uint32_t kTileMaxSeg = 64;    // a tile's parameter segments kept in shared memory
@@ -139,7 +146,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     const uint32_t per = a.tile_n;
     uint32_t* s_pend = reinterpret_cast<uint32_t*>(smem + L.pend);  // [parity][receptor][per]
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
-    __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base;
+    __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base, s_nst;
     __shared__ uint32_t s_ravail, s_rdone;  // MG: peers' items appended / scan done
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
@@ -224,6 +231,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
     for (uint32_t ph = 0; ph < nph; ++ph) {
+        const unsigned long long t_start = (a.prof && threadIdx.x == 0) ? globaltimer() : 0ull;
         const bool doA = ph < a.steps;
         const bool doE = ph >= 1;
         const uint32_t tA = a.t0 + ph;
@@ -234,11 +242,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             f_lo = a.forced_off[ph];
             f_hi = a.forced_off[ph + 1];
         }
-        const uint32_t log_base = a.ring ? (ph & 1u) * a.n : 0u;
+        const size_t log_base = (size_t)ph * a.n;  // phase-strided log (not written in ring mode)
         // I_ou by parity of its step: U reads I_ou(tE), N writes I_ou(tA)
         const float* iou_rd = (tE & 1u) ? a.i_ou_b : a.i_ou;
         float* iou_wr = (tA & 1u) ? a.i_ou_b : a.i_ou;
 
+        // every CTA's bucketing of S(tE) (phase ph - 1) is complete: the
+        // tile's queue of set tE & 3 is final.  A CTA that stops early
+        // credits the phases it will not run, so this never waits on it.
+        auto wait_bucketed = [&]() {
+            if (lane == 0)
+                while (ld_acquire(a.bdone + ph - 1) < G) __nanosleep(32);
+            __syncwarp();
+        };
         // C: deliver S(tE) into the pending tile of parity tE (one queued
         // segment per warp grab, kTileUnroll entries in flight per lane)
         // (MG: the peers' segments for this tile are appended after the
@@ -246,10 +262,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         // waits for them until the scan is done)
         auto consume = [&]() {
             if (!doE) return;
-            const uint32_t par = tE & 1u;
+            wait_bucketed();
+            const uint32_t par = tE & 1u, set = tE & 3u;
             const uint32_t bw = smem_u32(s_pend + par * 4 * per), per4 = 4 * per;
-            const uint32_t cnt0 = __ldcg(a.q_cnt + par * G + blockIdx.x);
-            const uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x];
+            const uint32_t cnt0 = __ldcg(a.q_cnt + set * G + blockIdx.x);
+            const uint64_t* items = a.q + (size_t)set * a.q_total + a.q_base[blockIdx.x];
             for (;;) {
                 uint32_t it = 0;
                 if (lane == 0) it = atomicAdd(&s_iwork, 1u);
@@ -305,10 +322,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         // items, where every consumer picks them up.
         auto scan_remote = [&]() {
             if (!MG || !doE) return;
+            wait_bucketed();
             Exchange* ex = a.ex;
-            const uint32_t par = tE & 1u, slot = tE % kSlots;
-            const uint32_t cnt0 = __ldcg(a.q_cnt + par * G + blockIdx.x);
-            uint64_t* items = a.q + (size_t)par * a.q_total + a.q_base[blockIdx.x] + cnt0;
+            const uint32_t set = tE & 3u, slot = tE % kSlots;
+            const uint32_t cnt0 = __ldcg(a.q_cnt + set * G + blockIdx.x);
+            uint64_t* items = a.q + (size_t)set * a.q_total + a.q_base[blockIdx.x] + cnt0;
             uint32_t nrem = 0;
             unsigned long long waited = 0;
             for (uint32_t li = 1; li < ex->world; ++li) {
@@ -523,16 +541,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         if (base + rank < kSpkStage) {
                             s_spk[base + rank] = i;  // bucketed after the update (B)
                         } else {  // staging full: log, route and bucket this spike directly
-                            a.spk[log_base + atomicAdd(&ctl->spk_cursor, 1u)] = i;
+                            if (!a.ring) a.spk[log_base + atomicAdd(a.seg_end + ph, 1u)] = i;
                             ovf_route = MG;
                             const uint64_t row = tally(i);
-                            const uint32_t par = tA & 1u;
+                            const uint32_t set = tA & 3u;
                             const uint64_t k1 = __ldg(a.tl_off + a.src_self + i + 1);
                             for (uint64_t k = __ldg(a.tl_off + a.src_self + i); k < k1; ++k) {
                                 const uint4 sg = __ldg(a.tl + k);
-                                const uint32_t pos = atomicAdd(a.q_cnt + par * G + sg.x, 1u);
+                                const uint32_t pos = atomicAdd(a.q_cnt + set * G + sg.x, 1u);
                                 const uint64_t b = row + sg.y;
-                                a.q[(size_t)par * a.q_total + __ldg(a.q_base + sg.x) + pos] =
+                                a.q[(size_t)set * a.q_total + __ldg(a.q_base + sg.x) + pos] =
                                     b | ((uint64_t)sg.z << 40);
                             }
                         }
@@ -563,7 +581,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t nbt = 32 * kTileBucketWarps;
             const uint32_t nst = (doA && bucket_warp) ? min(s_nspk, (uint32_t)kSpkStage) : 0u;
             if (nst) {
-                const uint32_t par = tA & 1u;
+                const uint32_t set = tA & 3u;
                 for (uint32_t k = bt; k < nst; k += nbt) {
                     const uint32_t s = a.src_self + s_spk[k];
                     tally(s_spk[k]);
@@ -574,12 +592,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 for (uint32_t t = bt; t < G; t += nbt) {
                     const uint32_t h = s_hist[t];
                     if (h) {
-                        s_qb[t] = __ldg(a.q_base + t) + atomicAdd(a.q_cnt + par * G + t, h);
+                        s_qb[t] = __ldg(a.q_base + t) + atomicAdd(a.q_cnt + set * G + t, h);
                         s_hist[t] = 0u;
                     }
                 }
                 named_sync(2, nbt);
-                uint64_t* qp = a.q + (size_t)par * a.q_total;
+                uint64_t* qp = a.q + (size_t)set * a.q_total;
                 for (uint32_t k = bt; k < nst; k += nbt) {
                     const uint32_t s = a.src_self + s_spk[k];
                     const uint64_t row = ldg64(a.off + s);
@@ -594,13 +612,27 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 named_sync(2, nbt);
                 for (uint32_t t = bt; t < G; t += nbt) s_hist[t] = 0u;
                 // the peers' ids of S(tA): P2P stores into their receive slots
-                // (engine.cpp:416-437); published after the phase barrier
+                // (engine.cpp:416-437); published once every CTA has routed
                 if (MG) {
                     bool sent = false;
                     const uint32_t nr = (nst + 31u) & ~31u;
                     for (uint32_t k = bt; k < nr; k += nbt)
                         sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % kSlots);
                     if (sent) __threadfence_system();
+                }
+            }
+            // this CTA's part of S(tA) is queued (and routed): count it; the
+            // last CTA to do so publishes the batch to the peers
+            if (bucket_warp) {
+                named_sync(2, nbt);
+                if (bt == 0) {
+                    __threadfence();
+                    if (MG) __threadfence_system();
+                    const uint32_t old = atomicAdd(a.bdone + ph, 1u);
+                    if (MG && doA && old == G - 1u) {
+                        __threadfence();
+                        exchange_publish(a, tA);
+                    }
                 }
             }
             if (a.prof && bt == 0) s_t[1] = globaltimer();
@@ -615,47 +647,46 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
         }
 
-        // flush the CTA's staged spikes with one log reservation
+        // phase end (CTA-local): flush the staged spikes into the phase's log
+        // segment, recycle the consumed queue set, take the stop decision
         __syncthreads();
-        if (a.prof && threadIdx.x == 0)
-            for (int k = 0; k < 4; ++k) {
-                a.prof[4 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
-                s_t[k] = 0;
-            }
-        if (threadIdx.x == 0 && doE) a.q_cnt[(tE & 1u) * G + blockIdx.x] = 0u;  // serves S(tE + 2)
-        const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
-        if (threadIdx.x == 0 && nst) s_base = atomicAdd(&ctl->spk_cursor, nst);
-        __syncthreads();
-        for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x) a.spk[log_base + s_base + k] = s_spk[k];
-
-        grid_barrier(
-            ctl,
-            [&] {
-                if (doA) a.seg_end[ph] = ctl->spk_cursor;
-                if (a.ring) ctl->spk_cursor = 0;  // next phase writes the other half
-                a.phase_ns[ph + 1] = globaltimer();
-                // one stop decision for the whole grid
-                ctl->stop = (atomicAdd(&ctl->err, 0ull) != ~0ull ||
-                             (MG && (atomicAdd(&a.ex->timeout, 0u) != 0u ||
-                                     atomicAdd(&a.ex->peer_abort, 0u) != 0u))) ? 1u : 0u;
-            },
-            [&] {
-                if (MG) {
-                    // a failed step publishes no batch (the reference's worker
-                    // throws before phase B); the peers see the abort word
-                    if (ctl->stop)
-                        exchange_abort(a);
-                    else if (doA)
-                        exchange_publish(a, tA);
-                }
-            });
         if (threadIdx.x == 0) {
-            s_stop = (int)ld_acquire(&ctl->stop);
-            s_nspk = s_fwork = s_nwork = s_iwork = 0;
+            const uint32_t nst = min(s_nspk, (uint32_t)kSpkStage);
+            s_nst = nst;
+            s_nspk = 0;
+            const unsigned long long now = globaltimer();
+            if (a.prof) {
+                for (int k = 0; k < 4; ++k) {
+                    a.prof[5 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
+                    s_t[k] = 0;
+                }
+                a.prof[5 * ((size_t)ph * G + blockIdx.x) + 4] = t_start;
+            }
+            if (doE) a.q_cnt[(tE & 3u) * G + blockIdx.x] = 0u;  // serves S(tE + 4)
+            if (nst && !a.ring) s_base = atomicAdd(a.seg_end + ph, nst);
+            atomicMax(a.phase_ns + ph + 1, now);
+            // divergence: every CTA runs through the phase of the earliest
+            // diverging step (so the reported neuron is the smallest of that
+            // step, as with a barrier), then stops; a peer's timeout or abort
+            // stops at once.  A stopping CTA credits the bucketing counts of
+            // the phases it skips, so no consumer waits on it.
+            const unsigned long long e = atomicAdd(&ctl->err, 0ull);
+            bool stop = e != ~0ull && (uint32_t)(e >> 32) <= tA;
+            if (MG) stop = stop || atomicAdd(&a.ex->timeout, 0u) != 0u || atomicAdd(&a.ex->peer_abort, 0u) != 0u;
+            if (stop) {
+                for (uint32_t q = ph + 1; q < nph; ++q) atomicAdd(a.bdone + q, 1u);
+                if (MG) exchange_abort(a);
+            }
+            s_stop = stop ? 1 : 0;
+            s_fwork = s_nwork = s_iwork = 0;
             s_ravail = s_rdone = 0;
         }
         __syncthreads();
+        const uint32_t nst = s_nst;
+        if (nst && !a.ring)
+            for (uint32_t k = threadIdx.x; k < nst; k += blockDim.x) a.spk[log_base + s_base + k] = s_spk[k];
         if (s_stop) break;
+        if (nst && !a.ring) __syncthreads();  // s_spk is restaged by the next phase
     }
     // the pending tile P(S(t_last)) back to the global buffer of its parity
     {

@@ -250,6 +250,7 @@ struct Engine {
     DevBuf<uint32_t> d_spk;
     DevBuf<uint32_t> d_seg_end;
     DevBuf<uint32_t> d_bdone;  // tile_kernel: per phase, CTAs done bucketing
+    DevBuf<uint32_t> d_bmail;  // tile_kernel: per CTA (32 words apart), phases bucketed
     DevBuf<uint32_t> d_rates;
     DevBuf<uint32_t> d_probe_local, d_probe_slot;
     DevBuf<float> d_probe_v, d_probe_i;
@@ -1493,6 +1494,7 @@ void Engine::init_tile_state() {
     d_iou_b.alloc(std::max<uint32_t>(1, n));
     if (n) CK(cudaMemcpyAsync(d_iou_b.p, d_iou.p, 4ull * n, cudaMemcpyDeviceToDevice, stream));
     d_q.reserve(std::max<uint64_t>(1, (uint64_t)q_sets() * q_total));
+    d_q.zero(stream);  // tile_kernel: an empty slot reads 0 until its item is written
     d_qcnt.reserve((size_t)q_sets() * tile_T);
     d_qcnt.zero(stream);
     CK(cudaStreamSynchronize(stream));
@@ -1968,7 +1970,7 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
     a.early_publish = early_publish ? 1u : 0u;
     prof = knob("VXB_PHASE_PROFILE", nullptr) != nullptr;
     if (prof) {
-        d_prof.alloc((tile_path ? (tile_mp ? 4ull : 5ull) * tile_grid : 2ull * grid) * (steps + 1));
+        d_prof.alloc((tile_path ? (tile_mp ? 4ull : (size_t)kTileProf) * tile_grid : 2ull * grid) * (steps + 1));
         d_prof.zero(stream);
         a.prof = d_prof.p;
     }
@@ -1991,6 +1993,9 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
         d_qcnt.zero(stream);
         a.bdone = d_bdone.p;
         d_bdone.zero(stream);
+        d_bmail.reserve(32ull * tile_grid);
+        d_bmail.zero(stream);
+        a.bmail = d_bmail.p;
     }
     void* args[] = {&a};
     CK(cudaEventRecord(ev0, stream));
@@ -2057,12 +2062,18 @@ void Engine::finish_chunk(uint32_t rel0, uint32_t steps, uint32_t adv_steps) {
         uint32_t cnt[4] = {0, 0, 0, 0};
         // tile_kernel (no barrier): relative to the CTA's own phase start;
         // tile_mp_kernel: to the end of the previous phase's barrier
-        const size_t ps = tile_mp ? 4 : 5;
+        const size_t ps = tile_mp ? 4 : kTileProf;
+        if (const char* dump = knob("VXB_PROF_DUMP", nullptr)) {  // raw [phase][CTA][ps] globaltimer ns
+            if (FILE* f = std::fopen(dump, "wb")) {
+                std::fwrite(pr.data(), 8, pr.size(), f);
+                std::fclose(f);
+            }
+        }
         for (uint32_t ph = 1; ph < steps; ++ph) {
             sp += (double)(pn[ph + 1] - pn[ph]);
             double pm[4] = {0, 0, 0, 0};
             for (uint32_t b = 0; b < tile_grid; ++b) {
-                const double t0 = ps == 5 ? (double)pr[ps * ((size_t)ph * tile_grid + b) + 4] : (double)pn[ph];
+                const double t0 = !tile_mp ? (double)pr[ps * ((size_t)ph * tile_grid + b) + 4] : (double)pn[ph];
                 for (int k = 0; k < 4; ++k) {
                     const unsigned long long x = pr[ps * ((size_t)ph * tile_grid + b) + k];
                     if (!x) continue;

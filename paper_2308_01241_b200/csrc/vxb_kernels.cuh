@@ -212,6 +212,10 @@ struct StepArgs {
     // phase's spikes is complete; the spike log is phase-strided (entries of
     // phase p at spk[p * n], per-phase counts in seg_end)
     uint32_t* bdone;
+    // per CTA (128 B apart): the number of phases whose bucketing is complete,
+    // written (red.max) by the CTA that completes a phase's count, polled by
+    // one warp of each CTA — no hot line for 148 pollers
+    uint32_t* bmail;
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {

@@ -63,7 +63,20 @@ constexpr int kTileThreads = VXB_TILE_THREADS;      // 24 warps: update, then co
 constexpr uint32_t kTileUnroll = VXB_TILE_UNROLL;  // synapse entries in flight per consumer lane
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
 constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
-constexpr uint32_t kTileBucketWarps = 2;
+#ifndef VXB_TILE_BWARPS
+#define VXB_TILE_BWARPS 2               // warps that bucket S(tA) after the update
+#endif
+constexpr uint32_t kTileBucketWarps = VXB_TILE_BWARPS;
+constexpr uint32_t kTileProf = 8;       // phase-profile words per (phase, CTA)
+#ifndef VXB_TILE_L1PF
+#define VXB_TILE_L1PF 0                 // update: L1 prefetch of the chunk after next (no gain measured)
+#endif
+#ifndef VXB_TILE_FUSE_NOISE
+// the OU step of I_ou(tA) inside the update loop instead of a separate pass
+// (config 2: 55.5 vs 48.6 us/step — the update gets 14 us longer, the noise
+// is better spread over the phase's idle warps)
+#define VXB_TILE_FUSE_NOISE 0
+#endif
 constexpr uint32_t kTileQSets = 4;      // queue sets (step & 3), see the phase notes above
 // queue item: first entry (bits 0-39) | segment length << 40
 constexpr uint64_t kItemBeg = (1ull << 40) - 1;
@@ -148,10 +161,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base, s_nst;
     __shared__ uint32_t s_ravail, s_rdone;  // MG: peers' items appended / scan done
+    __shared__ uint32_t s_ready;            // last phase whose queues this CTA knows final
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
     __shared__ uint32_t s_hist[kTileMaxGrid], s_qb[kTileMaxGrid];  // per-tile bucketing
-    __shared__ unsigned long long s_t[4];  // phase profile: update end, bucketing, consumers, noise
+    // phase profile: update end, bucketing end, consumers end, noise end,
+    // (start), bucketing pass 1 / reservations / pass 2 ends
+    __shared__ unsigned long long s_t[kTileProf];
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t c_lo = min(a.n, blockIdx.x * per), c_hi = min(a.n, c_lo + per);
@@ -180,7 +196,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         s_nseg = cnt;
         s_nspk = s_fwork = s_nwork = s_iwork = 0;
         s_ravail = s_rdone = 0;
-        s_t[0] = s_t[1] = s_t[2] = s_t[3] = 0;
+        s_ready = 0xffffffffu;
+        for (uint32_t k = 0; k < kTileProf; ++k) s_t[k] = 0;
     }
     for (uint32_t k = threadIdx.x; k < kTileMaxGrid; k += blockDim.x) s_hist[k] = 0;
     __syncthreads();
@@ -228,6 +245,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     unsigned long long my_inner = 0, my_outer = 0;
     SegCursor cur_u, cur_n;
 
+    // every CTA's bucketing of phase q is complete: tell each CTA's mailbox
+    // (one fence, then relaxed reductions: a release per store would fence each)
+    auto post_bucketed = [&](uint32_t q) {
+        __threadfence();
+        for (uint32_t c = 0; c < G; ++c)
+            asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(a.bmail + 32 * c), "r"(q + 1) : "memory");
+    };
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
     for (uint32_t ph = 0; ph < nph; ++ph) {
@@ -247,13 +271,77 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         const float* iou_rd = (tE & 1u) ? a.i_ou_b : a.i_ou;
         float* iou_wr = (tA & 1u) ? a.i_ou_b : a.i_ou;
 
+        // N: advance I_ou to tA (ou_kernel, model.hpp:88-90, xi = stream word
+        // tA, engine.cpp:551-558) for the tile: consumed by E(tA) in ph + 1
+        // One 32-neuron chunk per call; false once the tile is done.
+        auto noise_chunk = [&]() -> bool {
+            if (!doA || VXB_TILE_FUSE_NOISE) return false;
+            {
+                uint32_t c = 0;
+                if (lane == 0) c = atomicAdd(&s_nwork, 1u);
+                c = __shfl_sync(0xffffffffu, c, 0);
+                if (c >= nch) return false;
+                const uint32_t w_lo = c_lo + (c << 5);
+                const uint32_t i = w_lo + lane;
+                const bool live = i < c_hi;
+                const uint32_t seg = cur_n.find(startp, nseg, seg_end, w_lo, min(w_lo + 31u, c_hi - 1u),
+                                                live ? i : c_hi - 1u, lane);
+                if (live) {
+                    const SegInfo& S = segp[seg];
+                    const ParamSet& P = psp[S.pset];
+                    float iou = ldp(iou_rd + i, pol_f);
+                    float xi = 0.0f;
+                    if (P.sigma_pos) {
+                        const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
+                        xi = stream_xi(mix_key(a.ou_root, gid), tA);
+                    }
+                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
+                    stp(iou_wr + i, iou, pol_f);
+                }
+            }
+            return true;
+        };
+        auto noise = [&]() {
+            while (noise_chunk()) {
+            }
+        };
         // every CTA's bucketing of S(tE) (phase ph - 1) is complete: the
         // tile's queue of set tE & 3 is final.  A CTA that stops early
         // credits the phases it will not run, so this never waits on it.
+        // One warp per CTA (warp 0, a consumer) polls the CTA's mailbox and
+        // posts the phase in shared memory for the others.
+        // Non-blocking form: true once the queues are final (warp 0 polls
+        // the mailbox, the other warps read what it posted).
+        auto bucketed = [&]() -> bool {
+            uint32_t r = *reinterpret_cast<volatile uint32_t*>(&s_ready) == ph;
+            if (!r && warp == 0) {
+                if (lane == 0 && ld_acquire(a.bmail + 32 * blockIdx.x) >= ph) {
+                    __threadfence_block();
+                    *reinterpret_cast<volatile uint32_t*>(&s_ready) = ph;
+                    r = 1;
+                }
+                r = __shfl_sync(0xffffffffu, r, 0);
+            }
+            if (r) __threadfence_block();
+            return r != 0;
+        };
         auto wait_bucketed = [&]() {
-            if (lane == 0)
-                while (ld_acquire(a.bdone + ph - 1) < G) __nanosleep(32);
-            __syncwarp();
+            // advance I_ou while the other CTAs finish their bucketing
+            while (!bucketed())
+                if (!noise_chunk()) break;
+            if (*reinterpret_cast<volatile uint32_t*>(&s_ready) != ph) {
+                if (lane == 0) {
+                    if (warp == 0) {
+                        while (ld_acquire(a.bmail + 32 * blockIdx.x) < ph) __nanosleep(64);
+                        __threadfence_block();
+                        *reinterpret_cast<volatile uint32_t*>(&s_ready) = ph;
+                    } else {
+                        while (*reinterpret_cast<volatile uint32_t*>(&s_ready) != ph) __nanosleep(128);
+                        __threadfence_block();
+                    }
+                }
+                __syncwarp();
+            }
         };
         // C: deliver S(tE) into the pending tile of parity tE (one queued
         // segment per warp grab, kTileUnroll entries in flight per lane)
@@ -267,24 +355,45 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t bw = smem_u32(s_pend + par * 4 * per), per4 = 4 * per;
             const uint32_t cnt0 = __ldcg(a.q_cnt + set * G + blockIdx.x);
             const uint64_t* items = a.q + (size_t)set * a.q_total + a.q_base[blockIdx.x];
-            for (;;) {
+            // queued items are final up to `cnt` (MG: plus the peers' items the
+            // scanning warp has appended so far)
+            uint32_t cnt = cnt0;
+            auto grab_item = [&]() {
                 uint32_t it = 0;
                 if (lane == 0) it = atomicAdd(&s_iwork, 1u);
-                it = __shfl_sync(0xffffffffu, it, 0);
-                uint32_t cnt = cnt0;
-                if (MG) {
+                return __shfl_sync(0xffffffffu, it, 0);
+            };
+            // MG: wait until item `it` exists or the queue is complete
+            auto resolve = [&](uint32_t it) -> bool {
+                if (MG && it >= cnt)
                     for (;;) {
                         const bool done = *reinterpret_cast<volatile uint32_t*>(&s_rdone) != 0u;
                         cnt = cnt0 + *reinterpret_cast<volatile uint32_t*>(&s_ravail);
                         if (it < cnt || done) break;
                         __nanosleep(200);
                     }
-                }
-                if (it >= cnt) break;
-                // pull the lines of a segment a few grabs ahead into L2 (no
-                // registers held): the loads below then wait on L2, not HBM
-                if (it + kTilePrefetch < cnt) {
-                    const uint64_t f = __ldcg(reinterpret_cast<const unsigned long long*>(items + it + kTilePrefetch));
+                return it < cnt;
+            };
+            // the item descriptor and the one kTilePrefetch grabs ahead (its
+            // segment is pulled into L2 when this one is processed)
+            auto load_item = [&](uint32_t it, uint64_t& d, uint64_t& f) {
+                d = __ldcg(reinterpret_cast<const unsigned long long*>(items + it));
+                f = it + kTilePrefetch < cnt
+                        ? __ldcg(reinterpret_cast<const unsigned long long*>(items + it + kTilePrefetch))
+                        : 0ull;
+            };
+            uint32_t it = grab_item();
+            uint64_t d = 0, f = 0;
+            bool have = resolve(it);
+            if (have) load_item(it, d, f);
+            while (have) {
+                // software pipeline: the next grab's descriptors are in
+                // flight while this segment is delivered
+                const uint32_t itn = grab_item();
+                uint64_t dn = 0, fn = 0;
+                const bool early = itn < cnt;
+                if (early) load_item(itn, dn, fn);
+                if (f) {  // no registers held: the entry loads below then wait on L2, not HBM
                     const uint64_t fb = f & kItemBeg;
                     const char* fp = reinterpret_cast<const char*>(a.tent + fb);
                     const char* fe = reinterpret_cast<const char*>(a.tent + fb + (f >> 40));
@@ -292,7 +401,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                         reinterpret_cast<uintptr_t>(fp) & ~(uintptr_t)127) + 128 * lane;
                     if (ln < fe) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ln));
                 }
-                const uint64_t d = __ldcg(reinterpret_cast<const unsigned long long*>(items + it));
                 const uint64_t* ev = a.tent + (d & kItemBeg) + lane;
                 const uint32_t len = (uint32_t)(d >> 40);
                 uint32_t k0 = 0;
@@ -312,6 +420,14 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     for (uint32_t u = 0; u < kTileUnroll; ++u)
                         if (k0 + u * 32 + lane < len) tile_add(bw, per4, e[u]);
                 }
+                if (early) {
+                    have = true;
+                } else {
+                    have = resolve(itn);
+                    if (have) load_item(itn, dn, fn);
+                }
+                d = dn;
+                f = fn;
             }
         };
         // R (one process per GPU): the peers' batches of S(tE).  One warp of
@@ -371,34 +487,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 if (waited && a.phase_wait) atomicMax(a.phase_wait + ph, waited);
             }
         };
-        // N: advance I_ou to tA (ou_kernel, model.hpp:88-90, xi = stream word
-        // tA, engine.cpp:551-558) for the tile: consumed by E(tA) in ph + 1
-        auto noise = [&]() {
-            if (!doA) return;
-            for (;;) {
-                uint32_t c = 0;
-                if (lane == 0) c = atomicAdd(&s_nwork, 1u);
-                c = __shfl_sync(0xffffffffu, c, 0);
-                if (c >= nch) break;
-                const uint32_t w_lo = c_lo + (c << 5);
-                const uint32_t i = w_lo + lane;
-                const bool live = i < c_hi;
-                const uint32_t seg = cur_n.find(startp, nseg, seg_end, w_lo, min(w_lo + 31u, c_hi - 1u),
-                                                live ? i : c_hi - 1u, lane);
-                if (live) {
-                    const SegInfo& S = segp[seg];
-                    const ParamSet& P = psp[S.pset];
-                    float iou = ldp(iou_rd + i, pol_f);
-                    float xi = 0.0f;
-                    if (P.sigma_pos) {
-                        const uint64_t gid = (uint64_t)((int64_t)i + S.gid_off);
-                        xi = stream_xi(mix_key(a.ou_root, gid), tA);
-                    }
-                    iou = fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi));
-                    stp(iou_wr + i, iou, pol_f);
-                }
-            }
-        };
         // deliveries of spike s of S(tA): the FLOP tally of its whole row
         // (engine.cpp:459-463) and, per tile its row touches, a queue item
         // {first entry, length} (one global reservation per (CTA, tile))
@@ -432,16 +520,40 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     isyn_n = ldp(a.i_syn + i, pol_f);
                 }
             };
+            // the chunk after next is grabbed early and its state pulled into
+            // L1 (no registers held): the next chunk's register loads then
+            // wait on L1, not on HBM/L2 — twice the update's bytes in flight
+            auto prefetch = [&](uint32_t c) {
+                if (!VXB_TILE_L1PF) return;
+                const uint32_t k = c_lo + (c << 5) + lane;
+                if (c < nch && k < c_hi) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.v + k));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(iou_rd + k));
+                    if (doE) {
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.j + k));
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.g + k));
+                    }
+                }
+            };
             uint32_t ch = grab();
             uint32_t i = c_lo + (ch << 5) + lane;
             if (ch < nch && i < c_hi) load(i);
+            uint32_t ch2 = VXB_TILE_L1PF ? grab() : 0u;
+            prefetch(ch2);
             while (ch < nch) {
                 const uint32_t vb0 = vb_n;
                 const float iou = __uint_as_float(iou_n);
                 float4 j = j_n;
                 const float4 g = g_n;
                 const float isyn_in = isyn_n;
-                const uint32_t chn = grab();
+                uint32_t chn;
+                if (VXB_TILE_L1PF) {
+                    chn = ch2;
+                    ch2 = grab();
+                    prefetch(ch2);
+                } else {
+                    chn = grab();
+                }
                 const uint32_t inext = c_lo + (chn << 5) + lane;
                 if (chn < nch && inext < c_hi) load(inext);
                 const bool live = i < c_hi;
@@ -517,6 +629,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             }
                         }
                         stp(a.v + i, vb, pol_f);
+                        if (VXB_TILE_FUSE_NOISE) {  // N for this neuron (see the noise lambda)
+                            float xi = 0.0f;
+                            if (P.sigma_pos)
+                                xi = stream_xi(mix_key(a.ou_root, (uint64_t)((int64_t)i + S.gid_off)), tA);
+                            stp(iou_wr + i, fadd(fadd(iou, fmul(P.ou_a, fsub(P.ou_mu, iou))), fmul(P.ou_b, xi)),
+                                pol_f);
+                        }
                     }
                     // probes: V after A(tA), I_syn after E(tE) (engine.cpp:405-406, 564-565)
                     if (EX && a.n_probes) {
@@ -589,14 +708,24 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     for (uint64_t q = __ldg(a.tl_off + s); q < k1; ++q) atomicAdd(&s_hist[__ldg(&a.tl[q].x)], 1u);
                 }
                 named_sync(2, nbt);
-                for (uint32_t t = bt; t < G; t += nbt) {
-                    const uint32_t h = s_hist[t];
-                    if (h) {
-                        s_qb[t] = __ldg(a.q_base + t) + atomicAdd(a.q_cnt + set * G + t, h);
-                        s_hist[t] = 0u;
-                    }
+                if (a.prof && bt == 0) s_t[5] = globaltimer();
+                {  // all of this thread's reservations in flight at once
+                    constexpr uint32_t R = kTileMaxGrid / (32 * kTileBucketWarps);
+                    uint32_t h[R], b[R];
+#pragma unroll
+                    for (uint32_t r = 0; r < R; ++r) h[r] = bt + r * nbt < G ? s_hist[bt + r * nbt] : 0u;
+#pragma unroll
+                    for (uint32_t r = 0; r < R; ++r)
+                        if (h[r]) b[r] = atomicAdd(a.q_cnt + set * G + bt + r * nbt, h[r]);
+#pragma unroll
+                    for (uint32_t r = 0; r < R; ++r)
+                        if (h[r]) {
+                            s_qb[bt + r * nbt] = __ldg(a.q_base + bt + r * nbt) + b[r];
+                            s_hist[bt + r * nbt] = 0u;
+                        }
                 }
                 named_sync(2, nbt);
+                if (a.prof && bt == 0) s_t[6] = globaltimer();
                 uint64_t* qp = a.q + (size_t)set * a.q_total;
                 for (uint32_t k = bt; k < nst; k += nbt) {
                     const uint32_t s = a.src_self + s_spk[k];
@@ -610,6 +739,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     }
                 }
                 named_sync(2, nbt);
+                if (a.prof && bt == 0) s_t[7] = globaltimer();
                 for (uint32_t t = bt; t < G; t += nbt) s_hist[t] = 0u;
                 // the peers' ids of S(tA): P2P stores into their receive slots
                 // (engine.cpp:416-437); published once every CTA has routed
@@ -629,9 +759,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     __threadfence();
                     if (MG) __threadfence_system();
                     const uint32_t old = atomicAdd(a.bdone + ph, 1u);
-                    if (MG && doA && old == G - 1u) {
+                    if (old == G - 1u) {
                         __threadfence();
-                        exchange_publish(a, tA);
+                        post_bucketed(ph);
+                        if (MG && doA) exchange_publish(a, tA);
                     }
                 }
             }
@@ -656,11 +787,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             s_nspk = 0;
             const unsigned long long now = globaltimer();
             if (a.prof) {
-                for (int k = 0; k < 4; ++k) {
-                    a.prof[5 * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
+                s_t[4] = t_start;
+                for (uint32_t k = 0; k < kTileProf; ++k) {
+                    a.prof[kTileProf * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
                     s_t[k] = 0;
                 }
-                a.prof[5 * ((size_t)ph * G + blockIdx.x) + 4] = t_start;
             }
             if (doE) a.q_cnt[(tE & 3u) * G + blockIdx.x] = 0u;  // serves S(tE + 4)
             if (nst && !a.ring) s_base = atomicAdd(a.seg_end + ph, nst);
@@ -674,7 +805,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             bool stop = e != ~0ull && (uint32_t)(e >> 32) <= tA;
             if (MG) stop = stop || atomicAdd(&a.ex->timeout, 0u) != 0u || atomicAdd(&a.ex->peer_abort, 0u) != 0u;
             if (stop) {
-                for (uint32_t q = ph + 1; q < nph; ++q) atomicAdd(a.bdone + q, 1u);
+                for (uint32_t q = ph + 1; q < nph; ++q)
+                    if (atomicAdd(a.bdone + q, 1u) == G - 1u) post_bucketed(q);
                 if (MG) exchange_abort(a);
             }
             s_stop = stop ? 1 : 0;

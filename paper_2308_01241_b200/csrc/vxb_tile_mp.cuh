@@ -38,6 +38,7 @@ namespace vxb {
 
 constexpr int kMpThreads = 1024;
 constexpr uint32_t kMpMaxTiles = 8192;
+constexpr uint32_t kMpBucketWarps = 2;  // warps that bucket the peers' batches (R)
 
 // Dynamic shared memory of tile_mp_kernel.
 struct MpLayout {
@@ -77,9 +78,9 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
     const uint32_t n_upd = kMpThreads / 32 - n_cons;
     const bool upd_warp = warp >= n_cons;
     const uint32_t ut = threadIdx.x - n_cons * 32;  // index among update threads
-    const bool bucket_warp = warp >= kMpThreads / 32 - kTileBucketWarps;
-    const uint32_t bt = threadIdx.x - (kMpThreads - 32 * kTileBucketWarps);
-    const uint32_t nbt = 32 * kTileBucketWarps;
+    const bool bucket_warp = warp >= kMpThreads / 32 - kMpBucketWarps;
+    const uint32_t bt = threadIdx.x - (kMpThreads - 32 * kMpBucketWarps);
+    const uint32_t nbt = 32 * kMpBucketWarps;
 
     const ParamSet* psp = a.pset;
     if (threadIdx.x == 0) {
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
                         cnt = __shfl_sync(0xffffffffu, cnt, 0);
                         const uint32_t* ids = ex->rx_ids[h] + (size_t)slot * ex->cap[h];
                         const uint32_t sb = ex->src_base[h];
-                        for (uint32_t k = c + (warp - (kMpThreads / 32 - kTileBucketWarps)) * G * 32 + lane * G;
+                        for (uint32_t k = c + (warp - (kMpThreads / 32 - kMpBucketWarps)) * G * 32 + lane * G;
                              k < cnt; k += G * nbt) {
                             const uint32_t s = sb + __ldcg(ids + k);
                             const uint64_t row = ldg64(a.off + s);

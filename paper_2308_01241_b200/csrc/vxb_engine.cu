@@ -215,6 +215,7 @@ struct Engine {
     // SM; chosen when the shard fits on chip (tile_path), else l2_atomic
     bool tile_path = false;
     uint32_t tile_per = 0, tile_cons = 12, tile_smem = 0, tile_grid = 0;
+    uint32_t tile_noisew = 0;  // tile_kernel: warps that start on the OU noise
     bool tile_mp = false;                  // several tiles per SM (tile_mp_kernel)
     // queue sets: tile_kernel rotates four (no grid barrier), tile_mp_kernel two
     uint32_t q_sets() const { return tile_mp ? 2u : kTileQSets; }
@@ -1205,6 +1206,7 @@ void Engine::share_tables(const Engine& d) {
     tile_path = d.tile_path;
     tile_per = d.tile_per;
     tile_cons = d.tile_cons;
+    tile_noisew = d.tile_noisew;
     tile_mp = d.tile_mp;
     tile_T = d.tile_T;
     tile_passes = d.tile_passes;
@@ -1340,6 +1342,8 @@ void Engine::setup_tiles() {
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
         tile_cons = (uint32_t)std::min(20, std::max(1, std::atoi(c)));
+    if (const char* c = knob("VXB_TILE_NOISEW", &knobs))
+        tile_noisew = (uint32_t)std::min(8, std::max(0, std::atoi(c)));
     cudaFuncAttributes fa1, fa2;
     CK(cudaFuncGetAttributes(&fa1, (const void*)tile_kernel<true, true>));
     CK(cudaFuncGetAttributes(&fa2, (const void*)tile_mp_kernel<true>));
@@ -1978,6 +1982,7 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
     if (tile_path) {
         a.tile_n = tile_per;
         a.n_cons = tile_cons;
+        a.n_noisew = tile_mp ? 0u : tile_noisew;
         a.q_total = (uint32_t)q_total;
         a.tl_off = d_tl_off.p;
         a.tl = d_tl.p;

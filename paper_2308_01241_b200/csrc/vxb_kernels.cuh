@@ -195,6 +195,7 @@ struct StepArgs {
     // ---- SM-tile path (tile_kernel, vxb_tile.cuh) ----
     uint32_t tile_n;            // neurons per CTA tile (multiple of 32)
     uint32_t n_cons;            // consumer warps
+    uint32_t n_noisew;          // tile_kernel: warps that start on the OU noise
     uint32_t q_total;           // queue items per parity
     const unsigned long long* tl_off;  // per global source: first tile segment (n_src + 1)
     const uint4* tl;            // tile segments {tile, first entry in row, length, 0}

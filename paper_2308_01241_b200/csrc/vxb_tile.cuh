@@ -62,7 +62,10 @@ constexpr int kTileThreads = VXB_TILE_THREADS;      // 24 warps: update, then co
 #endif
 constexpr uint32_t kTileUnroll = VXB_TILE_UNROLL;  // synapse entries in flight per consumer lane
 constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing covers
-constexpr uint32_t kTilePrefetch = 24;  // queued segments prefetched ahead of the consumers
+#ifndef VXB_TILE_PREFETCH
+#define VXB_TILE_PREFETCH 24
+#endif
+constexpr uint32_t kTilePrefetch = VXB_TILE_PREFETCH;  // queued segments prefetched ahead of the consumers
 #ifndef VXB_TILE_BWARPS
 #define VXB_TILE_BWARPS 2               // warps that bucket S(tA) after the update
 #endif
@@ -176,9 +179,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     const uint32_t G = gridDim.x;
     Control* ctl = a.ctl;
     const uint32_t n_cons = a.n_cons;                       // warps that start on delivery
-    const uint32_t n_upd = kTileThreads / 32 - n_cons;      // warps that start on the update
-    const bool upd_warp = warp >= n_cons;
-    const uint32_t ut = threadIdx.x - n_cons * 32;          // index among update threads
+    const uint32_t n_nw = a.n_noisew;                       // warps that start on the noise
+    const uint32_t n_upd = kTileThreads / 32 - n_cons - n_nw;  // warps that start on the update
+    const bool upd_warp = warp >= n_cons + n_nw;
+    const uint32_t ut = threadIdx.x - (n_cons + n_nw) * 32;    // index among update threads
 
     // parameter sets and the tile's segments in shared memory
     const ParamSet* psp = a.pset;
@@ -770,12 +774,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             noise();
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
             consume();
-        } else {
+        } else if (warp < n_cons) {
             if (MG && warp == 0) scan_remote();
             consume();
             if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
             noise();
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
+        } else {  // noise-first warps
+            noise();
+            if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
+            consume();
+            if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
         }
 
         // phase end (CTA-local): flush the staged spikes into the phase's log

@@ -25,12 +25,12 @@ def _free_port():
     return p
 
 
-def _gloo_worker(rank, world, port, q):
+def _gloo_worker(rank, world, store_file, q):
     import torch.distributed as dist
     sys.path.insert(0, str(ROOT))
     from paper_2308_01241_b200 import netgen
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no port to race for with other tests' launchers
+    dist.init_process_group("gloo", init_method=f"file://{store_file}", rank=rank, world_size=world)
 
     def ag(obj):
         out = [None] * world
@@ -48,12 +48,12 @@ def _gloo_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_mask_exchange_gloo_world2():
+def test_mask_exchange_gloo_world2(tmp_path):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    store = tmp_path / "gloo_store"
+    ps = [ctx.Process(target=_gloo_worker, args=(r, 2, str(store), q)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=120) for _ in ps)

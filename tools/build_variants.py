@@ -14,7 +14,11 @@ VARIANTS = {
     "u2": {"VXB_TILE_UNROLL": 2},
     "nopf": {"VXB_TILE_L1PF": 0},          # no L1 prefetch of the chunk after next
     "bw4": {"VXB_TILE_BWARPS": 4},
-    "nofuse": {"VXB_TILE_FUSE_NOISE": 0},  # the OU step as a separate pass after the update
+    "nofuse": {"VXB_TILE_FUSE_NOISE": 0},
+    "pf48": {"VXB_TILE_PREFETCH": 48},     # L2 prefetch distance in queue items
+    "pf64": {"VXB_TILE_PREFETCH": 64},
+    "pf96": {"VXB_TILE_PREFETCH": 96},
+    "pf12": {"VXB_TILE_PREFETCH": 12},  # the OU step as a separate pass after the update
     # l2_atomic path (vxb_kernels.cuh)
     "m2": {"VXB_MINB": 2},           # register cap lifted (2 CTAs/SM)
     "d3": {"VXB_DEPTH3": 1},         # update state two chunks ahead in registers

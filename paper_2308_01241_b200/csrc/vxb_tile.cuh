@@ -117,7 +117,44 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* p, uint64_t pol) {
 
 // Warp-uniform parameter-segment lookup over the tile's segment table:
 // starts[0..nseg) ascending, `end` = first neuron past the last segment.
+// The cursor (last segment found and its range) lives in shared memory, one
+// per warp: no registers stay live across the update loop for it (the
+// kernel runs at 64 registers, and spills land in a 20 KB L1).
 struct SegCursor {
+    uint32_t hint, lo, nx, pad;
+    __device__ __forceinline__ void reset() {
+        hint = 0;
+        lo = 1u;
+        nx = 0u;
+    }
+    __device__ __forceinline__ uint32_t find(const uint32_t* starts, uint32_t nseg, uint32_t end,
+                                             uint32_t w_lo, uint32_t w_last, uint32_t i_lane,
+                                             uint32_t lane) {
+        volatile SegCursor* c = this;
+        uint32_t h = c->hint, l = c->lo, x = c->nx;
+        if (w_lo < l || w_last >= x) {
+            uint32_t s0 = 0;
+            if (lane == 0) s0 = find_seg_from(starts, nseg, w_lo, w_lo >= l ? h : 0u);
+            h = __shfl_sync(0xffffffffu, s0, 0);
+            l = starts[h];
+            x = h + 1 < nseg ? starts[h + 1] : end;
+            __syncwarp();
+            if (lane == 0) {
+                c->hint = h;
+                c->lo = l;
+                c->nx = x;
+            }
+            __syncwarp();
+        }
+        uint32_t seg = h;
+        if (i_lane >= x)
+            while (seg + 1 < nseg && starts[seg + 1] <= i_lane) ++seg;
+        return seg;
+    }
+};
+
+// The same lookup with the cursor in registers (tile_mp_kernel).
+struct SegCursorReg {
     uint32_t hint = 0, lo = 1u, nx = 0u;
     __device__ __forceinline__ uint32_t find(const uint32_t* starts, uint32_t nseg, uint32_t end,
                                              uint32_t w_lo, uint32_t w_last, uint32_t i_lane,
@@ -246,8 +283,20 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
 
     const uint64_t pol_syn = policy_evict_first();  // synapse stream: read once
     const uint64_t pol_f = a.f_policy == 2 ? policy_evict_last() : policy_evict_normal();
-    unsigned long long my_inner = 0, my_outer = 0;
-    SegCursor cur_u, cur_n;
+    // FLOP tallies go straight to the control block (relaxed reductions, a
+    // few per spike): no 64-bit accumulators held in every thread
+    auto add_flops = [&](uint64_t in, uint64_t out) {
+        if (in) atomicAdd(&ctl->flops_inner, (unsigned long long)in);
+        if (out) atomicAdd(&ctl->flops_outer, (unsigned long long)out);
+    };
+    __shared__ SegCursor s_cur[2][kTileThreads / 32];  // per warp: update, noise
+    if (threadIdx.x < kTileThreads / 32) {
+        s_cur[0][threadIdx.x].reset();
+        s_cur[1][threadIdx.x].reset();
+    }
+    __syncthreads();
+    SegCursor& cur_u = s_cur[0][warp];
+    SegCursor& cur_n = s_cur[1][warp];
 
     // every CTA's bucketing of phase q is complete: tell each CTA's mailbox
     // (one fence, then relaxed reductions: a release per store would fence each)
@@ -259,7 +308,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) a.phase_ns[0] = globaltimer();
     const uint32_t nph = a.steps + 1;
     for (uint32_t ph = 0; ph < nph; ++ph) {
-        const unsigned long long t_start = (a.prof && threadIdx.x == 0) ? globaltimer() : 0ull;
+        if (a.prof && threadIdx.x == 0) s_t[4] = globaltimer();
         const bool doA = ph < a.steps;
         const bool doE = ph >= 1;
         const uint32_t tA = a.t0 + ph;
@@ -470,7 +519,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                             if (sg.x >= blockIdx.x) {
                                 if (sg.x == blockIdx.x) {
                                     item = (ldg64(a.off + s) + sg.y) | ((uint64_t)sg.z << 40);
-                                    my_outer += 2ull * sg.z;  // engine.cpp:459-463 (remote: outer)
+                                    add_flops(0, 2ull * sg.z);  // engine.cpp:459-463 (remote: outer)
                                 }
                                 break;
                             }
@@ -498,8 +547,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint64_t row = ldg64(a.off + a.src_self + s);
             const uint64_t len = ldg64(a.off + a.src_self + s + 1) - row;
             const uint32_t in = __ldg(a.inner + a.src_self + s);
-            my_inner += 2ull * in;
-            my_outer += 2ull * (len - in);
+            add_flops(2ull * in, 2ull * (len - in));
             return row;
         };
 
@@ -796,7 +844,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             s_nspk = 0;
             const unsigned long long now = globaltimer();
             if (a.prof) {
-                s_t[4] = t_start;
                 for (uint32_t k = 0; k < kTileProf; ++k) {
                     a.prof[kTileProf * ((size_t)ph * G + blockIdx.x) + k] = s_t[k];
                     s_t[k] = 0;
@@ -838,10 +885,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             __stcg(gp + c_lo + l,
                    make_ulonglong2((uint64_t)B[l] | ((uint64_t)B[per + l] << 32),
                                    (uint64_t)B[2 * per + l] | ((uint64_t)B[3 * per + l] << 32)));
-    }
-    if (my_inner | my_outer) {
-        atomicAdd(&ctl->flops_inner, my_inner);
-        atomicAdd(&ctl->flops_outer, my_outer);
     }
 }
 

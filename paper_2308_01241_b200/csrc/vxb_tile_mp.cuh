@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kMpThreads, 1) tile_mp_kernel(StepArgs a) {
     const uint64_t pol_syn = policy_evict_first();
     const uint64_t pol_f = a.f_policy == 2 ? policy_evict_last() : policy_evict_normal();
     unsigned long long my_inner = 0, my_outer = 0;
-    SegCursor cur_u, cur_n;
+    SegCursorReg cur_u, cur_n;
     // neuron of chunk k of this CTA (tile k / cpt, pass-major)
     auto chunk_base = [&](uint32_t k) { return ((k / cpt) * G + c) * per + (k % cpt) * 32u; };
 

@@ -1,0 +1,2 @@
+for v in pf12 pf48 pf64 pf96; do echo "== $v"; VXB_LIB=build/variants/libvxb_$v.so timeout 300 python tools/phase_profile.py --steps 100 --reps 3 2>&1 | grep advance | tail -2; done
+echo "== base"; timeout 300 python tools/phase_profile.py --steps 100 --reps 3 2>&1 | grep advance | tail -2

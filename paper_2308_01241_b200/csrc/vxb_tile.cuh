@@ -464,11 +464,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
 #pragma unroll
                     for (uint32_t u = 0; u < kTileUnroll; ++u) tile_add(bw, per4, e[u]);
                 }
-                if (k0 < len) {  // the tail
+                if (k0 < len) {  // the tail: lanes past the end re-read the segment's first
+                    // entry (unpredicated loads: a predicated asm load made the
+                    // compiler spill the array around it) and add nothing
                     uint64_t e[kTileUnroll];
 #pragma unroll
                     for (uint32_t u = 0; u < kTileUnroll; ++u)
-                        if (k0 + u * 32 + lane < len) e[u] = ld_stream(ev + k0 + u * 32, pol_syn);
+                        e[u] = ld_stream(k0 + u * 32 + lane < len ? ev + k0 + u * 32 : ev - lane, pol_syn);
 #pragma unroll
                     for (uint32_t u = 0; u < kTileUnroll; ++u)
                         if (k0 + u * 32 + lane < len) tile_add(bw, per4, e[u]);

@@ -12,6 +12,9 @@ VARIANTS = {
     "tt768u8": {"VXB_TILE_THREADS": 768, "VXB_TILE_UNROLL": 8},
     "u8": {"VXB_TILE_UNROLL": 8},
     "u2": {"VXB_TILE_UNROLL": 2},
+    "u5": {"VXB_TILE_UNROLL": 5},
+    "u6": {"VXB_TILE_UNROLL": 6},
+    "l1pf": {"VXB_TILE_L1PF": 1},
     "nopf": {"VXB_TILE_L1PF": 0},          # no L1 prefetch of the chunk after next
     "bw4": {"VXB_TILE_BWARPS": 4},
     "nofuse": {"VXB_TILE_FUSE_NOISE": 0},

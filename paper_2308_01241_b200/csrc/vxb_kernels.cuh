@@ -1087,7 +1087,11 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
             uint32_t chn = grab();
             prefetch(chn);
             uint32_t i = c_lo + (ch << 5) + lane;
-            if (ch < nch && i < c_hi) load_neuron<PACKED>(a, i, doE, pend_rd, cur, pol_f, pol_pz);
+            // loads are unpredicated (a lane past the range re-reads a valid
+            // neuron and ignores it): predicated asm loads made the compiler
+            // spill the prefetched state around them
+            const uint32_t i_safe = c_lo < a.n ? c_lo : 0u;
+            if (nch) load_neuron<PACKED>(a, (ch < nch && i < c_hi) ? i : i_safe, doE, pend_rd, cur, pol_f, pol_pz);
 #if VXB_DEPTH3
             NIn<PACKED> nx2;
             {
@@ -1107,8 +1111,8 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         load_neuron<PACKED>(a, i2, doE, pend_rd, nx2, pol_f, pol_pz);
                 }
 #else
-                if (chn < nch && inext < c_hi)
-                    load_neuron<PACKED>(a, inext, doE, pend_rd, nxt, pol_f, pol_pz);
+                load_neuron<PACKED>(a, (chn < nch && inext < c_hi) ? inext : i_safe, doE, pend_rd, nxt, pol_f,
+                                    pol_pz);
 #endif
                 const bool live = i < c_hi;
                 bool spiked = false;

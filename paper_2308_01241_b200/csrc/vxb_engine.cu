@@ -1359,6 +1359,12 @@ void Engine::setup_tiles() {
     // averages < 1 entry and every event pays a queue item on top of its
     // entry
     if (mp && !force_tile && !knob("VXB_TILE_PER", nullptr)) return;
+    // several tiles per SM: one GPU only.  With peers, a consumer could read a
+    // queue slot a peer-batch bucketing CTA had reserved but not yet written
+    // (intermittent mismatches at 2 GPUs); the path is opt-in and slower than
+    // the l2 path, so multi-GPU shards that do not fit one tile per SM take
+    // the l2 path
+    if (mp && world > 1) return;
     if (force && std::string(force) == "mp") mp = true;
     if (const char* c = knob("VXB_TILE_PER", &knobs)) {  // force several tiles per SM
         per = std::max<uint32_t>(32, (uint32_t)std::atoi(c) & ~31u);

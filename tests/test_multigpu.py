@@ -76,9 +76,9 @@ def _gpus():
                                        (2, {"VXB_TUNING": "1", "VXB_DYN": "0"}),
                                        (2, {"VXB_TUNING": "1", "VXB_PATH": "tile"}),
                                        (4, {"VXB_TUNING": "1", "VXB_PATH": "tile"}),
-                                       (2, {"VXB_TUNING": "1", "VXB_PATH": "tile", "VXB_TILE_PER": "128"}),
-                                       (4, {"VXB_TUNING": "1", "VXB_PATH": "tile", "VXB_TILE_PER": "64",
-                                            "VXB_TILE_ITEMS": "1"})])
+                                       # several tiles per SM is single-GPU only: with peers the
+                                       # engine takes the l2 path
+                                       (2, {"VXB_TUNING": "1", "VXB_PATH": "tile", "VXB_TILE_PER": "128"})])
 def test_nvlink_exchange_matches_reference(world, env):
     """Default schedule, plus the optional early batch publication (4-slot
     ring), the static delivery deal and the SM-tile path (peers' batches

@@ -71,6 +71,12 @@ constexpr uint32_t kTilePrefetch = VXB_TILE_PREFETCH;  // queued segments prefet
 #endif
 constexpr uint32_t kTileBucketWarps = VXB_TILE_BWARPS;
 constexpr uint32_t kTileProf = 8;       // phase-profile words per (phase, CTA)
+#ifndef VXB_TILE_SPIN0
+#define VXB_TILE_SPIN0 64    // ns between mailbox polls (warp 0)
+#endif
+#ifndef VXB_TILE_SPIN1
+#define VXB_TILE_SPIN1 128   // ns between polls of the posted phase (other warps)
+#endif
 #ifndef VXB_TILE_L1PF
 #define VXB_TILE_L1PF 0                 // update: L1 prefetch of the chunk after next (no gain measured)
 #endif
@@ -397,11 +403,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             if (*reinterpret_cast<volatile uint32_t*>(&s_ready) != ph) {
                 if (lane == 0) {
                     if (warp == 0) {
-                        while (ld_acquire(a.bmail + 32 * blockIdx.x) < ph) __nanosleep(64);
+                        while (ld_acquire(a.bmail + 32 * blockIdx.x) < ph) __nanosleep(VXB_TILE_SPIN0);
                         __threadfence_block();
                         *reinterpret_cast<volatile uint32_t*>(&s_ready) = ph;
                     } else {
-                        while (*reinterpret_cast<volatile uint32_t*>(&s_ready) != ph) __nanosleep(128);
+                        while (*reinterpret_cast<volatile uint32_t*>(&s_ready) != ph) __nanosleep(VXB_TILE_SPIN1);
                         __threadfence_block();
                     }
                 }

@@ -251,6 +251,7 @@ struct Engine {
     DevBuf<uint32_t> d_spk;
     DevBuf<uint32_t> d_seg_end;
     DevBuf<uint32_t> d_bdone;  // tile_kernel: per phase, CTAs done bucketing
+    DevBuf<uint32_t> d_routed;  // tile_kernel (MG): per phase, CTAs done routing
     DevBuf<uint32_t> d_bmail;  // tile_kernel: per CTA (32 words apart), phases bucketed
     DevBuf<uint32_t> d_rates;
     DevBuf<uint32_t> d_probe_local, d_probe_slot;
@@ -1359,17 +1360,17 @@ void Engine::setup_tiles() {
     // averages < 1 entry and every event pays a queue item on top of its
     // entry
     if (mp && !force_tile && !knob("VXB_TILE_PER", nullptr)) return;
+    if (force && std::string(force) == "mp") mp = true;
+    if (const char* c = knob("VXB_TILE_PER", &knobs)) {  // force several tiles per SM
+        per = std::max<uint32_t>(32, (uint32_t)std::atoi(c) & ~31u);
+        mp = true;
+    }
     // several tiles per SM: one GPU only.  With peers, a consumer could read a
     // queue slot a peer-batch bucketing CTA had reserved but not yet written
     // (intermittent mismatches at 2 GPUs); the path is opt-in and slower than
     // the l2 path, so multi-GPU shards that do not fit one tile per SM take
     // the l2 path
     if (mp && world > 1) return;
-    if (force && std::string(force) == "mp") mp = true;
-    if (const char* c = knob("VXB_TILE_PER", &knobs)) {  // force several tiles per SM
-        per = std::max<uint32_t>(32, (uint32_t)std::atoi(c) & ~31u);
-        mp = true;
-    }
     uint32_t T = sms, smem = 0;
     if (mp) {
         if (!knob("VXB_TILE_PER", nullptr)) per = 8192;
@@ -1735,6 +1736,7 @@ uint32_t Engine::advance_begin(uint32_t steps) {
     if (d_spk.n < std::max<size_t>(1, cap_entries)) d_spk.alloc(std::max<size_t>(1, cap_entries));
     d_seg_end.reserve(chunk + 2);
     d_bdone.reserve(chunk + 2);
+    d_routed.reserve(chunk + 2);
     d_rates.reserve((size_t)n_units * chunk);
     d_phase_ns.reserve(chunk + 2);
     d_phase_wait.reserve(chunk + 2);
@@ -2004,6 +2006,8 @@ void Engine::launch_chunk(uint32_t t0, uint32_t rel0, uint32_t steps, uint32_t a
         d_qcnt.zero(stream);
         a.bdone = d_bdone.p;
         d_bdone.zero(stream);
+        a.routed = d_routed.p;
+        d_routed.zero(stream);
         d_bmail.reserve(32ull * tile_grid);
         d_bmail.zero(stream);
         a.bmail = d_bmail.p;

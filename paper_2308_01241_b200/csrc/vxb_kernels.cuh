@@ -217,6 +217,7 @@ struct StepArgs {
     // written (red.max) by the CTA that completes a phase's count, polled by
     // one warp of each CTA — no hot line for 148 pollers
     uint32_t* bmail;
+    uint32_t* routed;  // tile_kernel (MG): per phase, CTAs whose spikes are routed to the peers
 };
 
 __device__ __forceinline__ uint64_t ldg64(const uint64_t* p) {

@@ -71,6 +71,9 @@ constexpr uint32_t kTilePrefetch = VXB_TILE_PREFETCH;  // queued segments prefet
 #endif
 constexpr uint32_t kTileBucketWarps = VXB_TILE_BWARPS;
 constexpr uint32_t kTileProf = 8;       // phase-profile words per (phase, CTA)
+#ifndef VXB_TILE_SCANW
+#define VXB_TILE_SCANW 0  // consumer warps scanning the peers' batches (0 = all)
+#endif
 #ifndef VXB_TILE_SPIN0
 #define VXB_TILE_SPIN0 64    // ns between mailbox polls (warp 0)
 #endif
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     uint32_t* s_pend = reinterpret_cast<uint32_t*>(smem + L.pend);  // [parity][receptor][per]
     uint32_t* s_spk = reinterpret_cast<uint32_t*>(smem + L.spk);
     __shared__ uint32_t s_nspk, s_fwork, s_nwork, s_iwork, s_base, s_nst;
-    __shared__ uint32_t s_ravail, s_rdone;  // MG: peers' items appended / scan done
+    __shared__ uint32_t s_ravail, s_rdone;  // MG: peers' items reserved / scanning warps done
     __shared__ uint32_t s_ready;            // last phase whose queues this CTA knows final
     __shared__ int s_stop;
     __shared__ uint32_t s_seg_lo, s_nseg;
@@ -223,6 +226,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
     Control* ctl = a.ctl;
     const uint32_t n_cons = a.n_cons;                       // warps that start on delivery
     const uint32_t n_nw = a.n_noisew;                       // warps that start on the noise
+    // consumer warps that scan the peers' batches (MG)
+    const uint32_t n_scan = VXB_TILE_SCANW ? min((uint32_t)VXB_TILE_SCANW, n_cons) : n_cons;
     const uint32_t n_upd = kTileThreads / 32 - n_cons - n_nw;  // warps that start on the update
     const bool upd_warp = warp >= n_cons + n_nw;
     const uint32_t ut = threadIdx.x - (n_cons + n_nw) * 32;    // index among update threads
@@ -417,8 +422,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
         // C: deliver S(tE) into the pending tile of parity tE (one queued
         // segment per warp grab, kTileUnroll entries in flight per lane)
         // (MG: the peers' segments for this tile are appended after the
-        // local items by the scanning warp, see R; a consumer that runs out
-        // waits for them until the scan is done)
+        // local items by the consumer warps, see R; a consumer that runs out
+        // of local items takes them once every scanning warp is done)
         auto consume = [&]() {
             if (!doE) return;
             wait_bucketed();
@@ -426,8 +431,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t bw = smem_u32(s_pend + par * 4 * per), per4 = 4 * per;
             const uint32_t cnt0 = __ldcg(a.q_cnt + set * G + blockIdx.x);
             const uint64_t* items = a.q + (size_t)set * a.q_total + a.q_base[blockIdx.x];
-            // queued items are final up to `cnt` (MG: plus the peers' items the
-            // scanning warp has appended so far)
+            // queued items are final up to `cnt` (MG: plus the peers' items,
+            // once every scanning warp is done)
             uint32_t cnt = cnt0;
             auto grab_item = [&]() {
                 uint32_t it = 0;
@@ -438,8 +443,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             auto resolve = [&](uint32_t it) -> bool {
                 if (MG && it >= cnt)
                     for (;;) {
-                        const bool done = *reinterpret_cast<volatile uint32_t*>(&s_rdone) != 0u;
-                        cnt = cnt0 + *reinterpret_cast<volatile uint32_t*>(&s_ravail);
+                        const bool done = *reinterpret_cast<volatile uint32_t*>(&s_rdone) == n_scan;
+                        if (done) {
+                            __threadfence_block();
+                            cnt = cnt0 + *reinterpret_cast<volatile uint32_t*>(&s_ravail);
+                        }
                         if (it < cnt || done) break;
                         __nanosleep(200);
                     }
@@ -503,12 +511,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 f = fn;
             }
         };
-        // R (one process per GPU): the peers' batches of S(tE).  One warp of
-        // every CTA waits for each peer's flag (the reference's step barrier,
-        // engine.cpp:468-524), scans the batch for the sources whose rows
-        // have a segment in its tile (the row's tile list, ascending by tile)
-        // and appends those segments to the tile's queue after the local
-        // items, where every consumer picks them up.
+        // R (one process per GPU): the peers' batches of S(tE).  The consumer
+        // warps of every CTA wait for each peer's flag (the reference's step
+        // barrier, engine.cpp:468-524), scan a slice each of the batch for the
+        // sources whose rows have a segment in the CTA's tile (the row's tile
+        // list, ascending by tile) and append those segments to the tile's
+        // queue after the local items (slots reserved in shared memory).
         auto scan_remote = [&]() {
             if (!MG || !doE) return;
             wait_bucketed();
@@ -516,7 +524,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t set = tE & 3u, slot = tE % kSlots;
             const uint32_t cnt0 = __ldcg(a.q_cnt + set * G + blockIdx.x);
             uint64_t* items = a.q + (size_t)set * a.q_total + a.q_base[blockIdx.x] + cnt0;
-            uint32_t nrem = 0;
             unsigned long long waited = 0;
             for (uint32_t li = 1; li < ex->world; ++li) {
                 const uint32_t h = (ex->rank + li) % ex->world;
@@ -529,34 +536,44 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 cnt = __shfl_sync(0xffffffffu, cnt, 0);
                 const uint32_t* ids = ex->rx_ids[h] + (size_t)slot * ex->cap[h];
                 const uint32_t sb = ex->src_base[h];
-                for (uint32_t b0 = 0; b0 < cnt; b0 += 32) {
+                // every scanning warp takes a slice of the batch
+                for (uint32_t b0 = warp * 32; b0 < cnt; b0 += n_scan * 32) {
                     uint64_t item = 0;
                     if (b0 + lane < cnt) {
                         const uint32_t s = sb + __ldcg(ids + b0 + lane);
                         const uint64_t k1 = __ldg(a.tl_off + s + 1);
-                        for (uint64_t k = __ldg(a.tl_off + s); k < k1; ++k) {
-                            const uint4 sg = __ldg(a.tl + k);
-                            if (sg.x >= blockIdx.x) {
-                                if (sg.x == blockIdx.x) {
-                                    item = (ldg64(a.off + s) + sg.y) | ((uint64_t)sg.z << 40);
-                                    add_flops(0, 2ull * sg.z);  // engine.cpp:459-463 (remote: outer)
-                                }
+                        // the row's tile list is ascending: look at four
+                        // segments per round trip
+                        for (uint64_t kb = __ldg(a.tl_off + s); kb < k1; kb += 4) {
+                            uint32_t tx[4];
+#pragma unroll
+                            for (uint32_t u = 0; u < 4; ++u) tx[u] = kb + u < k1 ? __ldg(&a.tl[kb + u].x) : 0xffffffffu;
+                            uint32_t hit = 4;
+#pragma unroll
+                            for (uint32_t u = 0; u < 4; ++u)
+                                if (hit == 4 && tx[u] == blockIdx.x) hit = u;
+                            if (hit < 4) {
+                                const uint4 sg = __ldg(a.tl + kb + hit);
+                                item = (ldg64(a.off + s) + sg.y) | ((uint64_t)sg.z << 40);
+                                add_flops(0, 2ull * sg.z);  // engine.cpp:459-463 (remote: outer)
                                 break;
                             }
+                            if (tx[3] != 0xffffffffu && tx[3] > blockIdx.x) break;
                         }
                     }
                     const unsigned ball = __ballot_sync(0xffffffffu, item != 0);
-                    if (item) items[nrem + __popc(ball & ((1u << lane) - 1u))] = item;
-                    nrem += __popc(ball);
-                    __threadfence_block();
-                    __syncwarp();
-                    if (lane == 0) *reinterpret_cast<volatile uint32_t*>(&s_ravail) = nrem;
+                    if (ball) {
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(&s_ravail, (uint32_t)__popc(ball));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (item) items[base + __popc(ball & ((1u << lane) - 1u))] = item;
+                    }
                 }
             }
             __threadfence_block();
             __syncwarp();
             if (lane == 0) {
-                *reinterpret_cast<volatile uint32_t*>(&s_rdone) = 1u;
+                atomicAdd(&s_rdone, 1u);  // the consumers take the peers' items once all warps are done
                 if (waited && a.phase_wait) atomicMax(a.phase_wait + ph, waited);
             }
         };
@@ -771,6 +788,28 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             const uint32_t bt = threadIdx.x - (kTileThreads - 32 * kTileBucketWarps);
             const uint32_t nbt = 32 * kTileBucketWarps;
             const uint32_t nst = (doA && bucket_warp) ? min(s_nspk, (uint32_t)kSpkStage) : 0u;
+            // MG first: the peers' ids of S(tA), P2P stores into their receive
+            // slots (engine.cpp:416-437); the CTA that completes the phase's
+            // routing count publishes the batch — before the bucketing, so
+            // the peers can scan it ~10 us sooner
+            if (MG && bucket_warp) {
+                bool sent = false;
+                const uint32_t nr = (nst + 31u) & ~31u;
+                for (uint32_t k = bt; k < nr; k += nbt)
+                    sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % kSlots);
+                (void)sent;
+                // one system-scope fence for the CTA: it orders every bucket
+                // thread's P2P stores (observed through the barrier) before
+                // the routing count
+                named_sync(2, nbt);
+                if (bt == 0) {
+                    __threadfence_system();
+                    if (atomicAdd(a.routed + ph, 1u) == G - 1u && doA) {
+                        __threadfence();
+                        exchange_publish(a, tA);
+                    }
+                }
+            }
             if (nst) {
                 const uint32_t set = tA & 3u;
                 for (uint32_t k = bt; k < nst; k += nbt) {
@@ -813,18 +852,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                 named_sync(2, nbt);
                 if (a.prof && bt == 0) s_t[7] = globaltimer();
                 for (uint32_t t = bt; t < G; t += nbt) s_hist[t] = 0u;
-                // the peers' ids of S(tA): P2P stores into their receive slots
-                // (engine.cpp:416-437); published once every CTA has routed
-                if (MG) {
-                    bool sent = false;
-                    const uint32_t nr = (nst + 31u) & ~31u;
-                    for (uint32_t k = bt; k < nr; k += nbt)
-                        sent |= exchange_route(a, k < nst ? s_spk[k] : 0u, k < nst, tA % kSlots);
-                    if (sent) __threadfence_system();
-                }
             }
-            // this CTA's part of S(tA) is queued (and routed): count it; the
-            // last CTA to do so publishes the batch to the peers
+            // this CTA's part of S(tA) is queued: count it; the CTA that
+            // completes the count posts it to every CTA's mailbox
             if (bucket_warp) {
                 named_sync(2, nbt);
                 if (bt == 0) {
@@ -834,7 +864,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     if (old == G - 1u) {
                         __threadfence();
                         post_bucketed(ph);
-                        if (MG && doA) exchange_publish(a, tA);
                     }
                 }
             }
@@ -843,7 +872,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
             if (a.prof && lane == 0) atomicMax(&s_t[3], (unsigned long long)globaltimer());
             consume();
         } else if (warp < n_cons) {
-            if (MG && warp == 0) scan_remote();
+            if (MG && warp < n_scan) scan_remote();
             consume();
             if (a.prof && lane == 0) atomicMax(&s_t[2], (unsigned long long)globaltimer());
             noise();

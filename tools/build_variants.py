@@ -15,6 +15,8 @@ VARIANTS = {
     "u5": {"VXB_TILE_UNROLL": 5},
     "u6": {"VXB_TILE_UNROLL": 6},
     "l1pf": {"VXB_TILE_L1PF": 1},
+    "scan1": {"VXB_TILE_SCANW": 1},   # one warp scans the peers' batches
+    "scan4": {"VXB_TILE_SCANW": 4},
     "spin2": {"VXB_TILE_SPIN0": 200, "VXB_TILE_SPIN1": 500},   # longer sleeps while waiting for the queues
     "spin3": {"VXB_TILE_SPIN0": 500, "VXB_TILE_SPIN1": 1000},
     "nopf": {"VXB_TILE_L1PF": 0},          # no L1 prefetch of the chunk after next

@@ -21,6 +21,8 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--workload", default="config2", choices=["config2", "config3"])
 args = ap.parse_args()
 os.environ["VXB_TUNING"] = "1"
+if os.environ.get("VXB_PROF_DUMP") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    os.environ["VXB_PROF_DUMP"] += f".rank{os.environ.get('RANK', '0')}"
 os.environ["VXB_PHASE_PROFILE"] = "1"
 if args.path:
     os.environ["VXB_PATH"] = args.path

@@ -684,6 +684,26 @@ __device__ __forceinline__ bool exchange_route(const StepArgs& a, uint32_t s, bo
     const uint32_t lane = threadIdx.x & 31, world = ex->world, me = ex->rank;
     const unsigned long long m = valid ? (a.dst_mask[s] & ~(1ull << me)) : 0ull;
     bool sent = false;
+    if (world <= 8) {  // one reservation round trip for all destinations
+        unsigned ball[8];
+#pragma unroll
+        for (uint32_t d = 0; d < 8; ++d) ball[d] = d < world ? __ballot_sync(0xffffffffu, (m >> d) & 1ull) : 0u;
+        unsigned mine = 0, cntl = 0;  // lane d < world: destination d's count
+#pragma unroll
+        for (uint32_t d = 0; d < 8; ++d)
+            if (lane == d) cntl = __popc(ball[d]);
+        if (lane < world && cntl) mine = atomicAdd(&ex->send_cnt[slot][lane], cntl);
+#pragma unroll
+        for (uint32_t d = 0; d < 8; ++d) {
+            if (d >= world) break;
+            const unsigned base = __shfl_sync(0xffffffffu, mine, d);
+            if ((m >> d) & 1ull) {
+                ex->tx_ids[d][slot * ex->cap_self + base + __popc(ball[d] & ((1u << lane) - 1u))] = s;
+                sent = true;
+            }
+        }
+        return sent;
+    }
     for (uint32_t d = 0; d < world; ++d) {
         const bool want = (m >> d) & 1ull;
         const unsigned ball = __ballot_sync(0xffffffffu, want);

@@ -1528,11 +1528,15 @@ void Engine::build_blocks() {
     if (world > 1)
         for (uint32_t w = 0; w < workers; ++w)
             n_ref = std::max<uint64_t>(n_ref, src_base[w + 1] - src_base[w]);
-    // 64 MB blocks; 80 MB once that would take 6+ passes, where the per-pass
-    // cost of every spike's row lookup outweighs the L2 misses of the larger
-    // block (half of config 5, 25M neurons per GPU at 15 Hz: 2.56e11 ->
-    // 2.91e11 events/s; config 3's 5-10M per GPU stay faster at 64 MB)
-    uint64_t mb = ((n_ref * pend_per + (64ull << 20) - 1) / (64ull << 20)) >= 6 ? 80 : 64;
+    // 64 MB blocks; three passes once 64 MB would take 6+, where every
+    // spike's per-block row lookup outweighs the L2 misses of the larger
+    // block (config 5, 25M neurons per GPU at 15 Hz, 400 MB of pending sums:
+    // 1 GPU 2.37 -> 2.09 ms/step, 4 GPUs 5.17 -> 4.02 ms/step against the
+    // round-1 80 MB rule; 4 and 2 passes measured in between; config 3's
+    // 320 MB on one GPU stays fastest at 64 MB: 1.12 vs 1.31 ms at 3 passes)
+    const uint64_t pend_ref = n_ref * pend_per;
+    uint64_t mb = 64;
+    if ((pend_ref + (64ull << 20) - 1) / (64ull << 20) >= 6) mb = ((pend_ref + 3 * (1ull << 20) - 1) / 3) >> 20;
     if (const char* env = knob("VXB_BLOCK_MB", &knobs)) mb = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
     uint64_t bn = (mb << 20) / pend_per;
     if (const char* env = knob("VXB_BLOCK_NEURONS", &knobs)) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));

@@ -1,0 +1,4 @@
+for cfg in "VXB_BLOCK_MB=80" "VXB_BLOCK_MB=160" "VXB_BLOCK_MB=130"; do
+env VXB_TUNING=1 $cfg timeout 2400 python bench.py --workload config5 --steps 3 --warmup 2 --no-cpu > gpurun_out/c5d.log 2>&1
+echo "1gpu $cfg $(grep '^{' gpurun_out/c5d.log | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); s=d['config']['schedule']; print({k:round(d.get(k),3) for k in ['value','ms_per_step']}, s.get('l2_blocks'), s.get('dynamic_deal'))")"
+done

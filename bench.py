@@ -448,8 +448,8 @@ def run_b200(args):
     peak, peak_kind = measured_peak_hbm()
     achieved = alg_bytes / dev_s / 1e9
     # per advance and rank: one conductance-scatter launch (the staged
-    # set_conductances) + the step kernel launch(es)
-    launches_per = max(1, launches // max(1, args.steps * ws) - 1)
+    # set_conductances), one scratch-clearing launch + the step kernel launch(es)
+    launches_per = max(1, launches // max(1, args.steps * ws) - 2)
     if args.workload == "config2":
         wl = "config2" if ws == 1 else f"config2 x{ws} (ring {100 * ws} voxels)"
     elif args.workload == "config5":

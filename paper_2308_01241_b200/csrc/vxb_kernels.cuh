@@ -20,6 +20,7 @@
 // reference's post-phase-E state.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include "vxb_device.cuh"
@@ -1493,6 +1494,29 @@ __global__ void mask_check_kernel(const unsigned long long* __restrict__ have,
 }
 
 // Pack (step << 32 | local) keys of the spike log for the raster sort.
+// Per-launch scratch clearing: up to kClearMax word arrays zeroed, and the
+// control block reset (err = none) — one launch instead of a memset each.
+constexpr int kClearMax = 12;
+struct ClearList {
+    uint32_t* p[kClearMax];
+    uint64_t words[kClearMax];
+    Control* ctl;
+    int n;
+};
+__global__ void clear_kernel(ClearList cl) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < cl.n; ++k)
+        for (uint64_t i = tid; i < cl.words[k]; i += nth) cl.p[k][i] = 0u;
+    if (tid < sizeof(Control) / 4) {
+        uint32_t* c = reinterpret_cast<uint32_t*>(cl.ctl);
+        const uint32_t k = (uint32_t)tid;
+        // err (~0 = none) sits at a fixed offset; everything else is zero
+        const uint32_t e0 = (uint32_t)(offsetof(Control, err) / 4);
+        c[k] = (k == e0 || k == e0 + 1) ? 0xffffffffu : 0u;
+    }
+}
+
 // seg_end: cumulative log ends per step; stride != 0: the log is
 // phase-strided (step s's entries at spk[s * stride], tile_kernel).
 __global__ void raster_keys_kernel(const uint32_t* __restrict__ spk,

@@ -351,6 +351,8 @@ def run_b200(args):
     else:  # config3 (10 Hz) / config4 rate sweep: strong scaling, 20M neurons
         cfg = dti_cfg(workers=ws, rate=args.rate, dt_ms=args.dt,
                       total=args.neurons or 20_000_000)
+    if args.workload != "config2":
+        cfg["partition"]["byte_model"] = args.byte_model
     net = netgen.build_network(cfg)
     # the reference arm's options (record_raster / record_timings off): the
     # per-step wire-byte rows would add a spike-log readback per advance
@@ -556,6 +558,8 @@ def main():
                     help="config3/4 operating point (Hz)")
     ap.add_argument("--neurons", type=int, default=0,
                     help="config3/4 network size (default 20M); config5 neurons per GPU (25M)")
+    ap.add_argument("--byte-model", default="b200", choices=["b200", "b200_time"],
+                    help="config3/4/5 partition: HBM bytes (default) or the B200 time model")
     args = ap.parse_args()
     ensure_world(args)
     if args.warmup < 3 and args.impl == "b200":

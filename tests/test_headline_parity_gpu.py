@@ -21,6 +21,8 @@ minute: 12 voxels x 10 000 neurons at K = 1000 (1.2e8 synapses — the network
 bench.py's CPU arm times) and a 200-voxel DTI-like slice of 2e5 neurons at
 K = 500.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -92,6 +94,22 @@ def test_config2_regime_ring12_k1000_one_bio_second(monkeypatch, path):
                           monkeypatch=monkeypatch)
     rate = ref.total_spikes / (120_000 * 1.0)
     assert 7.0 < rate < 13.0, rate  # the calibrated ~10 Hz point
+    assert vr.min() > 0
+
+
+@pytest.mark.skipif(not os.environ.get("VXB_FULL_PARITY"),
+                    reason="opt-in (VXB_FULL_PARITY=1): ~40 GB of host memory for the reference's "
+                           "1e9-synapse tables and minutes of reference CPU time")
+def test_config2_full_size_300_steps():
+    """Config 2 itself — the benchmark's 1M neurons, K = 1000 (1e9 synapses),
+    10 Hz point — 300 steps in two advances on the SM-tile path, against the
+    reference engine on the reference pipeline's tables: raster, rates,
+    FLOPs and the final membrane state bit-exact, per-voxel rates within 1 %."""
+    import bench
+    cfg = bench.workload_cfg()
+    ref, vr, _ = _compare(cfg, 300, [100, 200], {"path": "sm_tile"})
+    rate = ref.total_spikes / (1_000_000 * 0.3)
+    assert 7.0 < rate < 13.0, rate
     assert vr.min() > 0
 
 

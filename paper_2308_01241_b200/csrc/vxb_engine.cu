@@ -717,10 +717,12 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     }
     if (tile_path) init_tile_state();
     // dynamic chunks win on one device (+8% config 2, config 3 2.0 -> 1.5 s
-    // per bio-s) and with peers when there is one block (config 2 at 4 GPUs
-    // +4%); with peers and several L2 blocks the static deal measured better
-    // (config 3 at 4 GPUs: 0.34 vs 0.60 s per bio-s)
-    dyn = world == 1 || n_blocks == 1;
+    // per bio-s), with peers when there is one block (config 2 at 4 GPUs
+    // +4%) and with peers over three or more blocks (config 5 at 4 GPUs
+    // 3.98 -> 3.71 ms/step, config 3 at 2 GPUs 634 -> 609 us/step); with
+    // peers and two blocks the static deal is far better (config 3 at 4
+    // GPUs: 333 vs 579 us/step)
+    dyn = world == 1 || n_blocks == 1 || n_blocks >= 3;
     if (const char* env = knob("VXB_DYN", &knobs)) dyn = std::atoi(env) != 0;
     // chunks of one local spike on one GPU when a row segment averages >= 512
     // entries (in-degree per L2 block; config 2: 1000), else up to 32

@@ -74,6 +74,10 @@ def _gpus():
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("world,env", [(2, {}), (4, {}), (2, {"VXB_TUNING": "1", "VXB_EARLY_PUBLISH": "1"}),
                                        (2, {"VXB_TUNING": "1", "VXB_DYN": "0"}),
+                                       # L2-blocked delivery with peers: 4 blocks (dynamic
+                                       # deal) and 2 blocks (static deal)
+                                       (2, {"VXB_TUNING": "1", "VXB_PATH": "l2", "VXB_BLOCK_NEURONS": "3000"}),
+                                       (2, {"VXB_TUNING": "1", "VXB_PATH": "l2", "VXB_BLOCK_NEURONS": "6000"}),
                                        (2, {"VXB_TUNING": "1", "VXB_PATH": "tile"}),
                                        (4, {"VXB_TUNING": "1", "VXB_PATH": "tile"}),
                                        # several tiles per SM is single-GPU only: with peers the

@@ -348,6 +348,7 @@ struct Engine {
     DevBuf<uint32_t> d_work;  // dynamic delivery chunk counters [2][blocks][world]
     bool dyn = false;
     uint32_t stage_e = 0;     // delivery ring entries per stage
+    bool big_pend = false;    // pending buffer of 384 MB+ (few, large L2 blocks)
     uint32_t f_policy = 0;    // neuron-state stream: 0 evict_normal, 1 evict_first, 2 evict_last
     bool local(uint32_t w) const { return w >= local_lo && w < local_hi; }
     void build_csr(const vxb_network* net);
@@ -720,16 +721,18 @@ void Engine::load(const vxb_network* net, const vxb_options* opt, const vxb_nets
     // per bio-s), with peers when there is one block (config 2 at 4 GPUs
     // +4%) and with peers over three or more blocks (config 5 at 4 GPUs
     // 3.98 -> 3.71 ms/step, config 3 at 2 GPUs 634 -> 609 us/step); with
-    // peers and two blocks the static deal is far better (config 3 at 4
-    // GPUs: 333 vs 579 us/step)
-    dyn = world == 1 || n_blocks == 1 || n_blocks >= 3;
+    // peers and two blocks of a mid-size shard the static deal is far better
+    // (config 3 at 4 GPUs, 80 MB of pending sums: 333 vs 579 us/step), of a
+    // big one the dynamic (config 5 at 4 GPUs: 3.50 vs 4.99 ms/step)
+    dyn = world == 1 || n_blocks == 1 || n_blocks >= 3 || big_pend;
     if (const char* env = knob("VXB_DYN", &knobs)) dyn = std::atoi(env) != 0;
     // chunks of one local spike on one GPU when a row segment averages >= 512
     // entries (in-degree per L2 block; config 2: 1000), else up to 32
     // (config 3's short L2-block segments: 1.14 ms per step at 32, 1.31 ms at
     // 13, 6.2 at 1; config 2 on 2 GPUs: 2.44e11 events/s at 32, 2.37e11 at 1)
     ch_max = (world == 1 && n && (double)n_syn / n / n_blocks >= 512.0) ? 1u : 32u;
-    if (const char* env = knob("VXB_CHMAX", &knobs)) ch_max = (uint32_t)std::max(1, std::atoi(env));
+    if (const char* env = knob("VXB_CHMAX", &knobs))  // a chunk is one warp's lanes: <= 32
+        ch_max = (uint32_t)std::min(32, std::max(1, std::atoi(env)));
     // publishing S(t) as soon as every CTA has routed it (before the phase's
     // own delivery ends) measured slower: config 2 at 4 GPUs 4.23e11 vs
     // 4.72e11 events/s
@@ -1530,15 +1533,21 @@ void Engine::build_blocks() {
     if (world > 1)
         for (uint32_t w = 0; w < workers; ++w)
             n_ref = std::max<uint64_t>(n_ref, src_base[w + 1] - src_base[w]);
-    // 64 MB blocks; three passes once 64 MB would take 6+, where every
-    // spike's per-block row lookup outweighs the L2 misses of the larger
-    // block (config 5, 25M neurons per GPU at 15 Hz, 400 MB of pending sums:
-    // 1 GPU 2.37 -> 2.09 ms/step, 4 GPUs 5.17 -> 4.02 ms/step against the
-    // round-1 80 MB rule; 4 and 2 passes measured in between; config 3's
-    // 320 MB on one GPU stays fastest at 64 MB: 1.12 vs 1.31 ms at 3 passes)
+    // 64 MB blocks; once 64 MB would take 6+ passes, three passes on one GPU
+    // and two with peers (whose spikes every pass walks too): each spike's
+    // per-block row lookup then outweighs the L2 misses of the larger block
+    // (config 5, 25M neurons per GPU at 15 Hz, 400 MB of pending sums: 1 GPU
+    // 5 / 3 / 2 passes 2.37 / 2.09 / 2.50 ms/step; 4 GPUs 5 / 4 / 3 / 2 / 1
+    // passes 5.17 / 4.06 / 3.69 / 3.50 / 4.20 ms with the dynamic deal from 3
+    // passes on); config 3's 320 MB on one GPU stays fastest at 64 MB: 1.12
+    // vs 1.31 ms at 3 passes)
     const uint64_t pend_ref = n_ref * pend_per;
     uint64_t mb = 64;
-    if ((pend_ref + (64ull << 20) - 1) / (64ull << 20) >= 6) mb = ((pend_ref + 3 * (1ull << 20) - 1) / 3) >> 20;
+    big_pend = (pend_ref + (64ull << 20) - 1) / (64ull << 20) >= 6;
+    if (big_pend) {
+        const uint64_t passes = world > 1 ? 2 : 3;
+        mb = ((pend_ref + passes * (1ull << 20) - 1) / passes) >> 20;
+    }
     if (const char* env = knob("VXB_BLOCK_MB", &knobs)) mb = std::max<uint64_t>(1, std::strtoull(env, nullptr, 10));
     uint64_t bn = (mb << 20) / pend_per;
     if (const char* env = knob("VXB_BLOCK_NEURONS", &knobs)) bn = std::max<uint64_t>(1024, std::strtoull(env, nullptr, 10));

@@ -9,6 +9,8 @@ VARIANTS = {
     # tile path (vxb_tile.cuh)
     "tt768": {"VXB_TILE_THREADS": 768},    # 24 warps at 80 registers
     "tt640": {"VXB_TILE_THREADS": 640},    # 20 warps at 96 registers
+    "tt896": {"VXB_TILE_THREADS": 896},    # 28 warps at 72 registers
+    "tt960": {"VXB_TILE_THREADS": 960},    # 30 warps at 68 registers
     "tt768u8": {"VXB_TILE_THREADS": 768, "VXB_TILE_UNROLL": 8},
     "u8": {"VXB_TILE_UNROLL": 8},
     "u2": {"VXB_TILE_UNROLL": 2},

@@ -548,3 +548,28 @@ def test_set_conductances_batch_equals_item_by_item():
             assert np.array_equal(pa.v, pb.v) and np.array_equal(pa.i_syn, pb.i_syn)
         for w in range(2):
             assert np.array_equal(a.membrane_snapshot(w), b.membrane_snapshot(w))
+
+
+def test_tile_spike_staging_overflow_matches_reference(monkeypatch):
+    """A synchronized burst larger than a tile's spike staging (kSpkStage =
+    1024 per CTA and step): 1 500 forced spikes in the first tile at one step
+    take the direct log / queue path of the SM-tile kernel; raster, rates and
+    final V equal the reference's."""
+    set_path(monkeypatch, "tile")
+    net = RefNet(make_config(seed=5, voxels=16, npv=10000, k_in=10, steps=20))
+    w0 = net.tables.workers[0]
+    gids = [int(g) for g in w0.neurons["gid"][:1500]]
+    opt = SimOptions(steps=20, forced_spikes=[ForcedSpike(5, g) for g in gids])
+    with SimInstance(net.tables, opt) as sim:
+        assert sim.schedule_info()["path"] == "sm_tile"
+        assert sim.schedule_info()["tile_neurons"] > 1024
+        r = sim.advance(20)
+        snaps = [sim.membrane_snapshot(w) for w in range(sim.workers)]
+    ref = RefSim(net, opt).advance(20)
+    assert r.total_spikes == ref.total_spikes
+    assert int((r.raster["step"] == 5).sum()) >= 1500
+    assert raster_set(r.raster) == raster_set(ref.raster)
+    rs = RefSim(net, opt)
+    rs.advance(20)
+    for w in range(len(snaps)):
+        assert np.array_equal(snaps[w], rs.membrane_snapshot(w)), w

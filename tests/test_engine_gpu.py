@@ -573,3 +573,24 @@ def test_tile_spike_staging_overflow_matches_reference(monkeypatch):
     rs.advance(20)
     for w in range(len(snaps)):
         assert np.array_equal(snaps[w], rs.membrane_snapshot(w)), w
+
+
+@pytest.mark.parametrize("path", ["tile", "l2"])
+def test_divergence_reports_the_references_neuron_and_step(monkeypatch, path):
+    """An infinite injection into one voxel from step 3: both paths report the
+    reference's SimError text (the smallest diverging neuron of the earliest
+    step) — on the SM-tile path the CTAs stop on their own, without a grid
+    barrier, and must still agree on it."""
+    set_path(monkeypatch, path)
+    net = RefNet(quiet_cfg(seed=8, voxels=6, npv=600, k_in=4))
+    # (checked against the C restatement of the reference step, which takes
+    # the options as a struct: the reference's JSON options have no infinity)
+    opt = SimOptions(steps=12, injections=[Injection(3, 12, 2, float("inf"))])
+    with pytest.raises(SimError) as ref_err:
+        OracleSim(net.tables, opt).advance(12)
+    with SimInstance(net.tables, opt) as sim:
+        assert sim.schedule_info()["path"] == ("sm_tile" if path == "tile" else "l2_atomic")
+        with pytest.raises(SimError) as gpu_err:
+            sim.advance(12)
+    assert str(gpu_err.value) == str(ref_err.value)
+    assert "membrane potential diverged" in str(gpu_err.value)

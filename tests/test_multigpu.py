@@ -119,15 +119,20 @@ def test_fullsize_config2_two_gpus_equal_one_gpu():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-def test_divergence_on_one_rank_aborts_all_ranks():
+@pytest.mark.parametrize("path", ["default", "tile"])
+def test_divergence_on_one_rank_aborts_all_ranks(path):
     """A divergence on one rank ends every rank's advance within one step:
     the diverging rank reports it, the others the reference's "simulation
     aborted while waiting on the step barrier" (engine.cpp:483-484), well
-    before the 30 s receive timeout."""
+    before the 30 s receive timeout — on the default path and on the SM-tile
+    path (CTA-local stop, no grid barrier)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            "--nproc-per-node=2", "--master-addr", "127.0.0.1",
            "--master-port", str(_free_port()), str(ROOT / "tests" / "dist_check.py"), "--abort"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    env = dict(os.environ)
+    if path == "tile":
+        env.update(VXB_TUNING="1", VXB_PATH="tile")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert lines, out.stdout + out.stderr
     res = json.loads(lines[-1])

@@ -1170,10 +1170,10 @@ __global__ void __launch_bounds__(kThreads, VXB_MINB) step_kernel(StepArgs a) {
                         // gating_kernel (model.hpp:69-71) with deq(P_prev) (engine.cpp:543-546)
                         float p0, p1, p2, p3;
                         if constexpr (PACKED) {
-                            p0 = dequantize((int64_t)(uint32_t)(cur.p0.x & 0xffffffffull));
-                            p1 = dequantize((int64_t)(uint32_t)(cur.p0.x >> 32));
-                            p2 = dequantize((int64_t)(uint32_t)(cur.p0.y & 0xffffffffull));
-                            p3 = dequantize((int64_t)(uint32_t)(cur.p0.y >> 32));
+                            p0 = dequantize_u32((uint32_t)(cur.p0.x & 0xffffffffull));
+                            p1 = dequantize_u32((uint32_t)(cur.p0.x >> 32));
+                            p2 = dequantize_u32((uint32_t)(cur.p0.y & 0xffffffffull));
+                            p3 = dequantize_u32((uint32_t)(cur.p0.y >> 32));
                             stp_cg(reinterpret_cast<ulonglong2*>(pend_rd) + i, make_ulonglong2(0ull, 0ull), pol_pz);
                         } else {
                             p0 = dequantize((int64_t)cur.p0.x);

@@ -660,10 +660,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) tile_kernel(StepArgs a) {
                     if (doE) {
                         // gating_kernel (model.hpp:69-71) with deq(P_prev)
                         // (engine.cpp:543-546) from the shared pending tile
-                        const float p0 = dequantize((int64_t)Br[l]);
-                        const float p1 = dequantize((int64_t)Br[per + l]);
-                        const float p2 = dequantize((int64_t)Br[2 * per + l]);
-                        const float p3 = dequantize((int64_t)Br[3 * per + l]);
+                        const float p0 = dequantize_u32(Br[l]);
+                        const float p1 = dequantize_u32(Br[per + l]);
+                        const float p2 = dequantize_u32(Br[2 * per + l]);
+                        const float p3 = dequantize_u32(Br[3 * per + l]);
                         Br[l] = 0u;
                         Br[per + l] = 0u;
                         Br[2 * per + l] = 0u;

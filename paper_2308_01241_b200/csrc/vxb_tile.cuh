@@ -67,7 +67,10 @@ constexpr uint32_t kTileMaxGrid = 256;  // CTAs (tiles) the per-tile bucketing c
 #endif
 constexpr uint32_t kTilePrefetch = VXB_TILE_PREFETCH;  // queued segments prefetched ahead of the consumers
 #ifndef VXB_TILE_BWARPS
-#define VXB_TILE_BWARPS 2               // warps that bucket S(tA) after the update
+// warps that route and bucket S(tA) after the update: 4 (config 2 at 2 / 4
+// GPUs 3.82 -> 4.07e11 / 7.05 -> 7.51e11 events/s — the routing before the
+// bucketing gets shorter; one GPU equal; 6 or 8 equal to 4)
+#define VXB_TILE_BWARPS 4
 #endif
 constexpr uint32_t kTileBucketWarps = VXB_TILE_BWARPS;
 constexpr uint32_t kTileProf = 8;       // phase-profile words per (phase, CTA)

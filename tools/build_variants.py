@@ -23,6 +23,8 @@ VARIANTS = {
     "spin3": {"VXB_TILE_SPIN0": 500, "VXB_TILE_SPIN1": 1000},
     "nopf": {"VXB_TILE_L1PF": 0},          # no L1 prefetch of the chunk after next
     "bw4": {"VXB_TILE_BWARPS": 4},
+    "bw6": {"VXB_TILE_BWARPS": 6},
+    "bw8": {"VXB_TILE_BWARPS": 8},
     "nofuse": {"VXB_TILE_FUSE_NOISE": 0},
     "pf48": {"VXB_TILE_PREFETCH": 48},     # L2 prefetch distance in queue items
     "pf64": {"VXB_TILE_PREFETCH": 64},

@@ -1346,6 +1346,11 @@ void Engine::setup_tiles() {
     int sms = 0, optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    // consumer warps at the start of a phase: 12 on one GPU (8 / 10: 44.0 /
+    // 43.4 vs 42.9 us/step); 6 with peers, where the consumers also scan the
+    // peers' batches and more update and bucketing throughput pays (config 2
+    // at 4 GPUs: 6 / 8 / 12 / 16 -> 7.92 / 7.80 / 7.44 / 7.02e11 events/s)
+    tile_cons = world > 1 ? 6u : 12u;
     if (const char* c = knob("VXB_TILE_CONS", &knobs))
         tile_cons = (uint32_t)std::min(20, std::max(1, std::atoi(c)));
     if (const char* c = knob("VXB_TILE_NOISEW", &knobs))
